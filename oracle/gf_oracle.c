@@ -1,0 +1,400 @@
+/*
+ * gf_oracle.c -- CPU ORACLE (test infrastructure, NOT the product).
+ *
+ * A plain-C restatement of the reference's matrix-free contraction kernels and
+ * per-summand pass drivers (gatefit, arXiv 2506.23775), used only by tests/,
+ * __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference leg.
+ * The product path (paper_2506_23775_b200 + libgfcuda.so) never links this.
+ *
+ * Every function cites the reference file:line it restates.  Conventions
+ * (reference kernels.py:1-22): qubit 0 is the MOST significant bit; a gate on
+ * q1 < q2 sees legs (p, 2, q, 2, n) = (2^q1, 2^(q2-q1-1), 2^(k-1-q2)); gate
+ * matrices are row-major 4x4 with index 2*b(q1)+b(q2) (already wire-swap
+ * normalised by the caller, reference objective.py:179-185).
+ *
+ * Parity status: pinned -- tests/test_oracle.py checks these routines against
+ * fixtures produced by the unmodified reference (tests/golden/make_golden.py).
+ */
+#include <complex.h>
+#include <stdint.h>
+#include <string.h>
+
+typedef double complex cplx;
+typedef int64_t i64;
+
+#define C_GATE 0
+#define C_ARRAY 1
+#define C_HOLE_APPLY 2
+#define C_HOLE_CONTRACT 3
+#define C_PAIR 4
+
+/* ---- kernels.py:132-205, 283-322: gate application (general 5-leg form;
+ * the adjacent case is q == 1, reference kernels.py:132-151 gives the same
+ * row addresses).  sparse != 0 skips the 8 structural zeros of a
+ * parity-conserving gate (kernels.py:283-322). */
+void or_apply(const cplx *psi, const cplx *g, i64 p, i64 q, i64 n, int sparse, cplx *out)
+{
+    for (i64 i0 = 0; i0 < p; ++i0)
+        for (i64 i2 = 0; i2 < q; ++i2) {
+            i64 b0 = ((i0 * 2) * q + i2) * 2 * n;
+            i64 b1 = ((i0 * 2 + 1) * q + i2) * 2 * n;
+            for (i64 i4 = 0; i4 < n; ++i4) {
+                cplx x0 = psi[b0 + i4], x1 = psi[b0 + n + i4];
+                cplx x2 = psi[b1 + i4], x3 = psi[b1 + n + i4];
+                if (sparse) {
+                    out[b0 + i4] = g[0] * x0 + g[3] * x3;
+                    out[b0 + n + i4] = g[5] * x1 + g[6] * x2;
+                    out[b1 + i4] = g[9] * x1 + g[10] * x2;
+                    out[b1 + n + i4] = g[12] * x0 + g[15] * x3;
+                } else {
+                    out[b0 + i4] = g[0] * x0 + g[1] * x1 + g[2] * x2 + g[3] * x3;
+                    out[b0 + n + i4] = g[4] * x0 + g[5] * x1 + g[6] * x2 + g[7] * x3;
+                    out[b1 + i4] = g[8] * x0 + g[9] * x1 + g[10] * x2 + g[11] * x3;
+                    out[b1 + n + i4] = g[12] * x0 + g[13] * x1 + g[14] * x2 + g[15] * x3;
+                }
+            }
+        }
+}
+
+/* ---- kernels.py:208-242: environment D[i][j] = sum bra(i) ket(j), bra not
+ * conjugated; out is overwritten. */
+void or_hole_contract(const cplx *bra, const cplx *ket, i64 p, i64 q, i64 n, cplx *out)
+{
+    cplx d[16];
+    for (int e = 0; e < 16; ++e) d[e] = 0;
+    for (i64 i0 = 0; i0 < p; ++i0)
+        for (i64 i2 = 0; i2 < q; ++i2) {
+            i64 b0 = ((i0 * 2) * q + i2) * 2 * n;
+            i64 b1 = ((i0 * 2 + 1) * q + i2) * 2 * n;
+            for (i64 i4 = 0; i4 < n; ++i4) {
+                i64 r[4] = {b0 + i4, b0 + n + i4, b1 + i4, b1 + n + i4};
+                for (int i = 0; i < 4; ++i) {
+                    cplx y = bra[r[i]];
+                    for (int j = 0; j < 4; ++j) d[4 * i + j] += y * ket[r[j]];
+                }
+            }
+        }
+    memcpy(out, d, sizeof d);
+}
+
+/* ---- kernels.py:245-280: hole application into an interleaved array
+ * out[phys * arity + a] (arity index fastest, kernels.py:12-15). */
+void or_hole_apply(const cplx *psi, i64 p, i64 q, i64 n, const i64 *rows, const i64 *cols, i64 arity,
+                   cplx *out)
+{
+    i64 N = p * q * n * 4;
+    memset(out, 0, sizeof(cplx) * N * arity);
+    for (i64 i0 = 0; i0 < p; ++i0)
+        for (i64 i2 = 0; i2 < q; ++i2) {
+            i64 b0 = ((i0 * 2) * q + i2) * 2 * n;
+            i64 b1 = ((i0 * 2 + 1) * q + i2) * 2 * n;
+            for (i64 i4 = 0; i4 < n; ++i4) {
+                i64 r[4] = {b0 + i4, b0 + n + i4, b1 + i4, b1 + n + i4};
+                for (i64 a = 0; a < arity; ++a) out[r[rows[a]] * arity + a] = psi[r[cols[a]]];
+            }
+        }
+}
+
+/* ---- kernels.py:325-414: gate on every logical vector of an array. */
+void or_array_apply(const cplx *arr, i64 arity, const cplx *g, i64 p, i64 q, i64 n, int sparse, cplx *out)
+{
+    for (i64 i0 = 0; i0 < p; ++i0)
+        for (i64 i2 = 0; i2 < q; ++i2) {
+            i64 b0 = ((i0 * 2) * q + i2) * 2 * n;
+            i64 b1 = ((i0 * 2 + 1) * q + i2) * 2 * n;
+            for (i64 i4 = 0; i4 < n; ++i4) {
+                i64 r[4] = {b0 + i4, b0 + n + i4, b1 + i4, b1 + n + i4};
+                for (i64 a = 0; a < arity; ++a) {
+                    cplx x0 = arr[r[0] * arity + a], x1 = arr[r[1] * arity + a];
+                    cplx x2 = arr[r[2] * arity + a], x3 = arr[r[3] * arity + a];
+                    if (sparse) {
+                        out[r[0] * arity + a] = g[0] * x0 + g[3] * x3;
+                        out[r[1] * arity + a] = g[5] * x1 + g[6] * x2;
+                        out[r[2] * arity + a] = g[9] * x1 + g[10] * x2;
+                        out[r[3] * arity + a] = g[12] * x0 + g[15] * x3;
+                    } else {
+                        out[r[0] * arity + a] = g[0] * x0 + g[1] * x1 + g[2] * x2 + g[3] * x3;
+                        out[r[1] * arity + a] = g[4] * x0 + g[5] * x1 + g[6] * x2 + g[7] * x3;
+                        out[r[2] * arity + a] = g[8] * x0 + g[9] * x1 + g[10] * x2 + g[11] * x3;
+                        out[r[3] * arity + a] = g[12] * x0 + g[13] * x1 + g[14] * x2 + g[15] * x3;
+                    }
+                }
+            }
+        }
+}
+
+/* ---- kernels.py:417-458: outT[c][a] = sum bra(i_c) arr(j_c, a). */
+void or_hole_contract_array(const cplx *bra, const cplx *arr, i64 arity, i64 p, i64 q, i64 n, const i64 *rows,
+                            const i64 *cols, i64 ncols, cplx *outT)
+{
+    memset(outT, 0, sizeof(cplx) * ncols * arity);
+    for (i64 i0 = 0; i0 < p; ++i0)
+        for (i64 i2 = 0; i2 < q; ++i2) {
+            i64 b0 = ((i0 * 2) * q + i2) * 2 * n;
+            i64 b1 = ((i0 * 2 + 1) * q + i2) * 2 * n;
+            for (i64 i4 = 0; i4 < n; ++i4) {
+                i64 r[4] = {b0 + i4, b0 + n + i4, b1 + i4, b1 + n + i4};
+                for (i64 c = 0; c < ncols; ++c) {
+                    cplx y = bra[r[rows[c]]];
+                    const cplx *src = arr + r[cols[c]] * arity;
+                    for (i64 a = 0; a < arity; ++a) outT[c * arity + a] += y * src[a];
+                }
+            }
+        }
+}
+
+static cplx dot_plain(const cplx *a, const cplx *b, i64 N)
+{ /* objective.py:283-288 */
+    cplx s = 0;
+    for (i64 i = 0; i < N; ++i) s += a[i] * b[i];
+    return s;
+}
+
+typedef struct {
+    i64 k, nslots;
+    const cplx *mats;   /* [n][16] normalised */
+    const cplx *mats_t; /* [n][16] transposes (NOT conjugated) */
+    const int32_t *sparse;
+    const i64 *ps, *qs, *ns;
+} or_plan;
+
+static void apply_slot(const or_plan *P, const cplx *src, const cplx *mats, i64 l, int sparse, cplx *dst)
+{
+    or_apply(src, mats + 16 * l, P->ps[l], P->qs[l], P->ns[l], sparse, dst);
+}
+
+/* ---- objective.py:291-304 (_value_chunk), over an explicit index list. */
+void or_value_chunk(const or_plan *P, const i64 *js, i64 nj, const cplx *phi0s, cplx *buf_a, cplx *buf_b,
+                    i64 *counts, cplx *value)
+{
+    i64 N = (i64)1 << P->k, n = P->nslots;
+    cplx v = 0;
+    for (i64 t = 0; t < nj; ++t) {
+        memset(buf_a, 0, sizeof(cplx) * N);
+        buf_a[js[t]] = 1.0;
+        cplx *cur = buf_a, *nxt = buf_b;
+        for (i64 l = 0; l < n; ++l) {
+            apply_slot(P, cur, P->mats, l, P->sparse[l], nxt);
+            cplx *tmp = cur; cur = nxt; nxt = tmp;
+        }
+        counts[C_GATE] += n;
+        v += dot_plain(phi0s + t * N, cur, N);
+    }
+    *value = v;
+}
+
+/* ---- objective.py:307-319 (_run_passes). */
+static cplx run_passes(const or_plan *P, i64 j, const cplx *phi0, cplx *psis, cplx *phis, i64 *counts)
+{
+    i64 N = (i64)1 << P->k, n = P->nslots;
+    memset(psis, 0, sizeof(cplx) * N);
+    psis[j] = 1.0;
+    for (i64 l = 0; l < n; ++l) apply_slot(P, psis + l * N, P->mats, l, P->sparse[l], psis + (l + 1) * N);
+    memcpy(phis, phi0, sizeof(cplx) * N);
+    for (i64 m = 1; m <= n; ++m) {
+        i64 l = n - m;
+        apply_slot(P, phis + (m - 1) * N, P->mats_t, l, P->sparse[l], phis + m * N);
+    }
+    counts[C_GATE] += 2 * n;
+    return dot_plain(phi0, psis + n * N, N);
+}
+
+/* ---- objective.py:322-337 (_gradient_chunk); dacc[n][16] accumulates. */
+void or_gradient_chunk(const or_plan *P, const i64 *js, i64 nj, const cplx *phi0s, cplx *psis, cplx *phis,
+                       cplx *dacc, i64 *counts, cplx *value)
+{
+    i64 N = (i64)1 << P->k, n = P->nslots;
+    cplx v = 0, tmp[16];
+    for (i64 t = 0; t < nj; ++t) {
+        v += run_passes(P, js[t], phi0s + t * N, psis, phis, counts);
+        for (i64 l = 0; l < n; ++l) {
+            or_hole_contract(phis + (n - l - 1) * N, psis + l * N, P->ps[l], P->qs[l], P->ns[l], tmp);
+            for (int e = 0; e < 16; ++e) dacc[16 * l + e] += tmp[e];
+        }
+        counts[C_HOLE_CONTRACT] += n;
+    }
+    *value = v;
+}
+
+/* ---- objective.py:432-482 (_hvp_chunk); zmats applied densely. */
+void or_hvp_chunk(const or_plan *P, const cplx *zmats, const cplx *zmats_t, const i64 *js, i64 nj,
+                  const cplx *phi0s, cplx *psis, cplx *phis, cplx *vbuf, cplx *tbuf, cplx *oacc, i64 *counts)
+{
+    i64 N = (i64)1 << P->k, n = P->nslots;
+    cplx tmp[16];
+    for (i64 t = 0; t < nj; ++t) {
+        run_passes(P, js[t], phi0s + t * N, psis, phis, counts);
+        cplx *v = vbuf, *tb = tbuf;
+        memset(v, 0, sizeof(cplx) * N);
+        for (i64 s = 1; s < n; ++s) { /* ascending, objective.py:461-471 */
+            apply_slot(P, v, P->mats, s - 1, P->sparse[s - 1], tb);
+            cplx *sw = v; v = tb; tb = sw;
+            apply_slot(P, psis + (s - 1) * N, zmats, s - 1, 0, tb);
+            for (i64 i = 0; i < N; ++i) v[i] += tb[i];
+            counts[C_GATE] += 2;
+            or_hole_contract(phis + (n - s - 1) * N, v, P->ps[s], P->qs[s], P->ns[s], tmp);
+            counts[C_HOLE_CONTRACT] += 1;
+            for (int e = 0; e < 16; ++e) oacc[16 * s + e] += tmp[e];
+        }
+        memset(v, 0, sizeof(cplx) * N);
+        for (i64 s = n - 2; s >= 0; --s) { /* descending, objective.py:472-482 */
+            apply_slot(P, v, P->mats_t, s + 1, P->sparse[s + 1], tb);
+            cplx *sw = v; v = tb; tb = sw;
+            apply_slot(P, phis + (n - s - 2) * N, zmats_t, s + 1, 0, tb);
+            for (i64 i = 0; i < N; ++i) v[i] += tb[i];
+            counts[C_GATE] += 2;
+            or_hole_contract(v, psis + s * N, P->ps[s], P->qs[s], P->ns[s], tmp);
+            counts[C_HOLE_CONTRACT] += 1;
+            for (int e = 0; e < 16; ++e) oacc[16 * s + e] += tmp[e];
+        }
+    }
+}
+
+/* ---- objective.py:340-423 (_hessian_chunk). Pair CSR as in _pair_csr
+ * (objective.py:209-247). block_acc[R][A][A]. */
+void or_hessian_chunk(const or_plan *P, const i64 *hole_row, const i64 *hole_col, i64 arity, const i64 *first_list,
+                      i64 nfirst, const i64 *first_start, const i64 *pair_second, const double *pair_mult,
+                      const i64 *pair_route, const int32_t *pair_sym, const int32_t *pair_flip, const i64 *js,
+                      i64 nj, const cplx *phi0s, cplx *psis, cplx *phis, cplx *harr, cplx *harr2, cplx *dacc,
+                      cplx *block_acc, cplx *out_t, i64 *counts, cplx *value)
+{
+    i64 N = (i64)1 << P->k, n = P->nslots, A = arity;
+    cplx v = 0, tmp[16];
+    for (i64 t = 0; t < nj; ++t) {
+        v += run_passes(P, js[t], phi0s + t * N, psis, phis, counts);
+        for (i64 l = 0; l < n; ++l) {
+            or_hole_contract(phis + (n - l - 1) * N, psis + l * N, P->ps[l], P->qs[l], P->ns[l], tmp);
+            for (int e = 0; e < 16; ++e) dacc[16 * l + e] += tmp[e];
+        }
+        counts[C_HOLE_CONTRACT] += n;
+        for (i64 fi = 0; fi < nfirst; ++fi) {
+            i64 l = first_list[fi], lo = first_start[fi], hi = first_start[fi + 1];
+            i64 last = pair_second[hi - 1];
+            or_hole_apply(psis + l * N, P->ps[l], P->qs[l], P->ns[l], hole_row + l * A, hole_col + l * A, A, harr);
+            counts[C_HOLE_APPLY] += 1;
+            cplx *cur = harr, *nxt = harr2;
+            i64 pi = lo;
+            for (i64 lp = l + 1; lp <= last; ++lp) {
+                if (pi < hi && pair_second[pi] == lp) {
+                    or_hole_contract_array(phis + (n - lp - 1) * N, cur, A, P->ps[lp], P->qs[lp], P->ns[lp],
+                                           hole_row + lp * A, hole_col + lp * A, A, out_t);
+                    counts[C_PAIR] += 1;
+                    double m = pair_mult[pi];
+                    cplx *blk = block_acc + pair_route[pi] * A * A;
+                    for (i64 a = 0; a < A; ++a)
+                        for (i64 b = 0; b < A; ++b) {
+                            cplx val = m * out_t[b * A + a];
+                            if (pair_sym[pi]) {
+                                blk[a * A + b] += val;
+                                blk[b * A + a] += val;
+                            } else if (pair_flip[pi]) {
+                                blk[b * A + a] += val;
+                            } else {
+                                blk[a * A + b] += val;
+                            }
+                        }
+                    pi += 1;
+                }
+                if (lp < last) {
+                    or_array_apply(cur, A, P->mats + 16 * lp, P->ps[lp], P->qs[lp], P->ns[lp], P->sparse[lp], nxt);
+                    counts[C_ARRAY] += 1;
+                    cplx *sw = cur; cur = nxt; nxt = sw;
+                }
+            }
+        }
+    }
+    *value = v;
+}
+
+/* ---- parity sector index maps (no reference implementation; SURVEY 8(a)
+ * a43).  Even sector (sector = 0): drop qubit k-1 (the LSB):
+ *   rank(x) = x >> 1,  unrank(i) = (i << 1) | (popcount(i) & 1 ^ sector). */
+void or_sector_unrank(const i64 *idx, i64 m, int sector, i64 *out)
+{
+    for (i64 t = 0; t < m; ++t) {
+        uint64_t i = (uint64_t)idx[t];
+        out[t] = (i64)((i << 1) | (uint64_t)((__builtin_popcountll(i) & 1) ^ sector));
+    }
+}
+
+void or_sector_rank(const i64 *x, i64 m, i64 *out)
+{
+    for (i64 t = 0; t < m; ++t) out[t] = x[t] >> 1;
+}
+
+/* ---- translation orbit of a full index: T moves qubit
+ * c*L + s to c*L + ((s + 2) mod L) on both spin chains (c = 0 up, 1 down);
+ * the bit of qubit q sits at position k-1-q.  Returns canonical rep (min over
+ * T^m, m = 0..L/2-1 for even L, else 0..L-1) and the orbit size. */
+static uint64_t shift2(uint64_t x, int L)
+{
+    int k = 2 * L;
+    uint64_t y = 0;
+    for (int q = 0; q < k; ++q) {
+        if (!((x >> (k - 1 - q)) & 1)) continue;
+        int c = q / L, s = q % L;
+        int qq = c * L + (s + 2) % L;
+        y |= (uint64_t)1 << (k - 1 - qq);
+    }
+    return y;
+}
+
+void or_orbit_canon(const i64 *x, i64 m, int L, i64 *rep, i64 *size)
+{
+    int period = (L % 2 == 0) ? L / 2 : L;
+    for (i64 t = 0; t < m; ++t) {
+        uint64_t cur = (uint64_t)x[t], best = cur;
+        int sz = period;
+        uint64_t y = cur;
+        for (int s = 1; s < period; ++s) {
+            y = shift2(y, L);
+            if (y == cur && sz == period) sz = s; /* first return fixes the orbit size */
+            if (y < best) best = y;
+        }
+        rep[t] = (i64)best;
+        size[t] = sz;
+    }
+}
+
+/* Count/list canonical orbit representatives of the parity sector: reps are
+ * returned as compressed (ranked) indices in ascending order with weights.
+ * Returns the number of reps; writes at most cap entries. */
+i64 or_sector_orbit_reps(int L, int sector, i64 *reps, i64 *weights, i64 cap)
+{
+    int k = 2 * L;
+    i64 M = (i64)1 << (k - 1), cnt = 0;
+    for (i64 i = 0; i < M; ++i) {
+        i64 x, r, s;
+        or_sector_unrank(&i, 1, sector, &x);
+        or_orbit_canon(&x, 1, L, &r, &s);
+        if (r == x) {
+            if (cnt < cap) {
+                reps[cnt] = i;
+                weights[cnt] = s;
+            }
+            ++cnt;
+        }
+    }
+    return cnt;
+}
+
+/* ---- models.py:247-255 specialised to the hard-core-boson term list:
+ * out = H psi for terms (a, b, coeff, is_hop) where hop = |01><10|+|10><01|
+ * and nn = |11><11| on qubits a, b (qubit 0 = MSB).  out is overwritten. */
+void or_hamiltonian_apply(int k, const i64 *ta, const i64 *tb, const double *coef, const int32_t *is_hop,
+                          i64 nterms, const cplx *psi, cplx *out)
+{
+    i64 N = (i64)1 << k;
+    memset(out, 0, sizeof(cplx) * N);
+    for (i64 t = 0; t < nterms; ++t) {
+        uint64_t ma = (uint64_t)1 << (k - 1 - ta[t]), mb = (uint64_t)1 << (k - 1 - tb[t]);
+        for (i64 x = 0; x < N; ++x) {
+            int ba = (x & ma) != 0, bb = (x & mb) != 0;
+            if (is_hop[t]) {
+                if (ba != bb) out[x] += coef[t] * psi[x ^ (ma | mb)];
+            } else if (ba && bb) {
+                out[x] += coef[t] * psi[x];
+            }
+        }
+    }
+}
