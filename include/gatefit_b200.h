@@ -1,0 +1,167 @@
+/*
+ * gatefit_b200.h -- C ABI of libgfcuda.so, the B200 (sm_100a) matrix-free
+ * contraction engine that is a drop-in for the hot path of the reference
+ * `gatefit` package (arXiv 2506.23775).
+ *
+ * Plain pointers and sizes only.  Device pointers are raw CUDA device
+ * addresses (complex128 = two doubles, re then im); `stream` is a cudaStream_t
+ * (NULL = legacy default stream).  All calls are asynchronous on `stream`
+ * unless stated otherwise.  Every call returns a gf_status; on failure
+ * gf_last_error() returns a thread-local message.  Error mapping used by the
+ * Python layer mirrors the reference's exceptions:
+ *   GF_EINVAL    -> ValueError          (reference kernels.py:75-79, 115-124, 500-501)
+ *   GF_ENONFINITE-> FloatingPointError  (reference objective.py:575-578)
+ *   GF_ECUDA     -> RuntimeError,  GF_ENOMEM -> MemoryError
+ *
+ * Conventions (reference kernels.py:1-22): qubit 0 is the most significant
+ * bit; a gate on targets (t1, t2) has matrix index 2*bit(t1) + bit(t2);
+ * targets with t1 > t2 are normalised internally by the wire swap
+ * [0,2,1,3] and outputs are returned in the caller's (t1, t2) orientation.
+ */
+#ifndef GATEFIT_B200_H
+#define GATEFIT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    GF_OK = 0,
+    GF_EINVAL = 1,
+    GF_ENONFINITE = 2,
+    GF_ECUDA = 3,
+    GF_ENOMEM = 4
+} gf_status;
+
+/* Thread-local description of the last failure on this thread. */
+const char *gf_last_error(void);
+/* ABI version (major*100 + minor). */
+int gf_abi_version(void);
+
+/* ------------------------------------------------------------------ *
+ * Kernel-level operations.  Each replaces one public op of the
+ * reference's kernels.py (file:line given) and is batched over `nvec`
+ * contiguous vectors of length 2^k.
+ * ------------------------------------------------------------------ */
+
+/* out = G in for every vector (out may equal in: in-place).
+ * Replaces kernels.apply_gate (kernels.py:484-515) and the numba cores
+ * _apply_{adjacent,general}_{kernel,plain,parity} (kernels.py:132-205,
+ * 283-322).  mat: host pointer to 16 complex (32 doubles), row-major.
+ * parity_sparse != 0 skips the 8 structurally zero entries. */
+int gf_apply_gate(const void *in, void *out, int k, int t1, int t2, const double *mat, int parity_sparse,
+                  int64_t nvec, void *stream);
+
+/* Parity-controlled one-qubit gate of the parity-sector compressed space
+ * (no reference counterpart): a 4x4 parity-conserving gate
+ * on full-space qubits (a, k_full-1) acting on the compressed vector of
+ * k_full-1 bits; `sector` 0 = even, 1 = odd.  mat in the (a, k_full-1)
+ * orientation. */
+int gf_apply_gate_sector_c1q(const void *in, void *out, int k_full, int a, int sector, const double *mat,
+                             int64_t nvec, void *stream);
+
+/* D[4][4] = sum_env bra(i) ket(j) (bra not conjugated) summed over the nvec
+ * vector pairs; written to out_dev (16 complex).  Replaces
+ * kernels.hole_contract (kernels.py:518-537, core kernels.py:208-242). */
+int gf_hole_contract(const void *bra, const void *ket, int k, int t1, int t2, int64_t nvec, void *out_dev,
+                     void *stream);
+
+/* out[phys][a] (arity fastest): psi with target bits := j_a, supported where
+ * target bits == i_a, a over support (flat 4*i+j, host array).  Replaces
+ * kernels.hole_apply (kernels.py:540-565, core kernels.py:245-280). */
+int gf_hole_apply(const void *psi, void *out, int k, int t1, int t2, const int64_t *support, int arity,
+                  void *stream);
+
+/* Gate applied to each of `arity` interleaved vectors ([2^k][arity]).
+ * Replaces kernels.apply_gate_to_array (kernels.py:574-597, cores
+ * kernels.py:325-414).  out must not alias in. */
+int gf_apply_gate_to_array(const void *in, void *out, int k, int arity, int t1, int t2, const double *mat,
+                           int parity_sparse, void *stream);
+
+/* B[a][c] = hole_contract(bra, arr[:, a], targets).flat[support[c]], written
+ * to out_dev as [arity][ncols] complex.  Replaces kernels.hole_contract_array
+ * (kernels.py:600-623, core kernels.py:417-458). */
+int gf_hole_contract_array(const void *bra, const void *arr, int k, int arity, int t1, int t2,
+                           const int64_t *support, int ncols, void *out_dev, void *stream);
+
+/* ------------------------------------------------------------------ *
+ * Parity-sector index maps and lattice-translation folding (new; SURVEY
+ * 8(a) a43/a44).  Bit-exact integer maps over device int64 arrays.
+ * ------------------------------------------------------------------ */
+/* full index x = (i << 1) | ((popcount(i) & 1) ^ sector) */
+int gf_sector_unrank(const int64_t *idx_dev, int64_t m, int sector, int64_t *out_dev, void *stream);
+/* i = x >> 1 */
+int gf_sector_rank(const int64_t *x_dev, int64_t m, int64_t *out_dev, void *stream);
+/* canonical representative (min over 2-site shifts of both spin chains of
+ * L sites) and orbit size of full indices x (k = 2L qubits). */
+int gf_orbit_canon(const int64_t *x_dev, int64_t m, int L, int64_t *rep_dev, int64_t *size_dev, void *stream);
+/* mark[i] = orbit size if compressed index (i0 + i) is the canonical rep of
+ * its orbit, else 0; for building the folded basis of the sector. */
+int gf_sector_orbit_mark(int64_t i0, int64_t m, int L, int sector, int32_t *mark_dev, void *stream);
+
+/* ------------------------------------------------------------------ *
+ * Engine: one plan per circuit topology and device.  Replaces the jitted
+ * pass drivers _value_chunk / _gradient_chunk / _hvp_chunk
+ * (objective.py:291-337, 432-482) and the chunk protocol of
+ * parallel_reduce (objective.py:490-558) for one rank's share of the
+ * basis sum.
+ * ------------------------------------------------------------------ */
+typedef struct gf_plan gf_plan;
+
+enum { GF_VALUE = 1, GF_GRAD = 2, GF_HVP = 4 };
+
+/* t1/t2/logical: per slot, as in the reference Circuit (circuit.py:30-67).
+ * sector: -1 = full space (reference semantics), 0/1 = even/odd parity
+ * sector compressed on qubit k-1.  max_batch: summands per gf_plan_eval
+ * call.  chunk_states: summands per output chunk (the reference uses 64,
+ * objective.py:75); every batch must start on a chunk boundary. */
+int gf_plan_create(gf_plan **plan, int k, int sector, int n_slots, const int32_t *t1, const int32_t *t2,
+                   const int32_t *logical, int n_logical, int64_t max_batch, int chunk_states);
+/* Logical gate matrices [n_logical][4][4] complex (host), caller orientation
+ * of each logical gate (the reference's logical_gates[i].matrix). */
+int gf_plan_set_gates(gf_plan *plan, const double *mats);
+/* HVP directions Z per logical gate [n_logical][4][4] complex (host). */
+int gf_plan_set_directions(gf_plan *plan, const double *zmats);
+/* Evaluate `nvec` summands.  basis_dev: int64 [nvec] basis indices (in the
+ * compressed space when sector >= 0).  weights_dev: double [nvec] or NULL
+ * (translation-fold orbit sizes).  phi0_dev: complex [nvec][2^K] target
+ * columns conj(U|j>) (K = k, or k-1 with a sector).  out_dev: double
+ * [ceil(nvec/chunk_states)][rec] with rec = 2 + 64*n_logical doubles:
+ *   value (complex), D[n_logical][4][4] (holomorphic, logical orientation,
+ *   accumulated over shared slots), H[n_logical][4][4] (holomorphic HVP);
+ * each record is the deterministic sum over its chunk (the reference's
+ * _Partial, objective.py:536-558).  value is phi0 . C|j> summed (the
+ * objective is f = -Re of the total, objective.py:606). */
+int gf_plan_eval(gf_plan *plan, int flags, int64_t nvec, const int64_t *basis_dev, const double *weights_dev,
+                 const void *phi0_dev, double *out_dev, void *stream);
+/* Per-slot (normalised orientation) derivative sums of the last eval,
+ * [n_slots][16] complex each for D and H (device), for tests. */
+int gf_plan_slot_outputs(gf_plan *plan, int64_t nvec, double *d_dev, double *h_dev, void *stream);
+/* Number of this library's kernels launched by the last gf_plan_eval. */
+int64_t gf_plan_last_launches(const gf_plan *plan);
+int gf_plan_destroy(gf_plan *plan);
+
+/* ------------------------------------------------------------------ *
+ * Matrix-free target oracle (replaces the CPU
+ * KrylovOracle / DenseOracle of reference models.py:305-393 as the
+ * producer of phi0 = conj(exp(-iHt)|j>)).  Terms are two-site operators
+ * (ta[t], tb[t]) with coefficient coef[t]: hop[t] != 0 is
+ * |01><10| + |10><01| (models.py:40-42), else n_a n_b (models.py:44).
+ * ------------------------------------------------------------------ */
+/* out = H in for nvec full-space vectors (out must not alias in). */
+int gf_hamiltonian_apply(const void *in, void *out, int k, const int32_t *ta, const int32_t *tb, const double *coef,
+                         const int32_t *hop, int nterms, int64_t nvec, void *stream);
+/* One Chebyshev order with H~ = scale*H + shift on nvec stored vectors:
+ * t_next = H~ t_cur (t_prev NULL) or 2 H~ t_cur - t_prev, then
+ * acc += c t_next (acc nullable).  sector_flags bits 0-1: 3 = full space,
+ * 0/1 = even/odd compressed sector; bit 8: accumulate conj(c t_next). */
+int gf_cheb_step(const void *t_cur, const void *t_prev, void *t_next, void *acc, int k, const int32_t *ta,
+                 const int32_t *tb, const double *coef, const int32_t *hop, int nterms, double scale, double shift,
+                 double c_re, double c_im, int64_t nvec, int sector_flags, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GATEFIT_B200_H */

@@ -1,0 +1,664 @@
+// gf_engine.cu -- batched basis-sum engine: fused forward / reverse / ascending
+// sweeps over a batch of summands, deterministic reductions, C-ABI plan.
+//
+// Reference semantics (gatefit, arXiv 2506.23775):
+//   forward      psi_{l+1} = G_l psi_l                         objective.py:310-313
+//   backward     phi_m = G_{n-m}^T phi_{m-1}, phi_0 = conj(U|j>)  objective.py:314-317
+//   gradient     D_l = hole(phi_{n-l-1}, psi_l)                objective.py:333-335
+//   HVP          ascending / descending recursions             objective.py:461-482
+// The B200 engine replaces the 2(n+1)-vector pass cache with a reversible
+// 3-vector schedule (SURVEY 7 "hard parts" 2): psi is uncomputed with G^dag,
+// the bra is propagated with G^T on the way down and recovered with conj(G)
+// on the way up.  One kernel launch per slot per sweep streams every vector
+// of the batch once (read + write), fusing the gate applications, the hole
+// contractions and the Z-terms of the HVP.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "gf_common.cuh"
+#include "gf_internal.h"
+
+namespace gf {
+
+enum { OP_FWD = 0, OP_FWD_DOT = 1, OP_REV_G = 2, OP_REV_GH = 3, OP_ASC_H = 4 };
+enum { MODE_DENSE = 0, MODE_SPARSE = 1, MODE_C1Q = 2 };
+
+struct SweepParams {
+    double2 *psi, *bra, *aux;  // [nvec][N]
+    const double2 *phi0;       // [nvec][N]
+    const double *weights;     // [nvec] or null
+    const int64_t *basis;      // [nvec] (init kernel)
+    u64 N;                     // amplitudes per vector
+    u64 nunits;                // tuples (2q) or pairs (c1q) per vector
+    int lo, hi;                // bit positions (c1q: lo = pa)
+    int sector;
+    Mat4 A, B, C;
+    double *partD, *partH, *partV;  // [nvec][gridDim.x][32|32|2]
+};
+
+constexpr int kThreads = 256;
+
+// ---------------------------------------------------------------------------
+// Sweep kernel.  Grid: (ctas_per_vector, nvec).  Each CTA only touches the
+// vector blockIdx.y, so every per-summand partial is independent of the batch
+// composition (deterministic for any batch size / GPU count).
+// ---------------------------------------------------------------------------
+template <int OP, int MODE, bool FIRST>
+__global__ void __launch_bounds__(kThreads) k_sweep(const SweepParams p)
+{
+    constexpr bool C1Q = (MODE == MODE_C1Q);
+    constexpr bool SP = (MODE == MODE_SPARSE);
+    constexpr int W = C1Q ? 2 : 4;  // amplitudes per unit
+    constexpr bool HAS_D = (OP == OP_REV_G || OP == OP_REV_GH);
+    constexpr bool HAS_H = (OP == OP_REV_GH || OP == OP_ASC_H);
+    constexpr bool HAS_V = (OP == OP_FWD_DOT) || ((OP == OP_REV_G || OP == OP_REV_GH) && FIRST);
+
+    const u64 vb = (u64)blockIdx.y * p.N;
+    double2 *psi = p.psi + vb;
+    double2 *bra = p.bra + vb;
+    double2 *aux = p.aux + vb;
+    const double2 *phi0 = p.phi0 ? p.phi0 + vb : nullptr;
+    const double w = p.weights ? p.weights[blockIdx.y] : 1.0;
+
+    double accD[32], accH[32];
+    double vre = 0.0, vim = 0.0;
+    if (HAS_D) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) accD[i] = 0.0;
+    }
+    if (HAS_H) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) accH[i] = 0.0;
+    }
+
+    const u64 stride = (u64)gridDim.x * blockDim.x;
+    for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < p.nunits; t += stride) {
+        u64 idx[W];
+        int P = 0;
+        if constexpr (C1Q) {
+            u64 y0 = ins0(t, p.lo);
+            idx[0] = y0;
+            idx[1] = y0 | (1ull << p.lo);
+            P = (__popcll(y0) & 1) ^ p.sector;
+        } else {
+            u64 b = ins0(ins0(t, p.lo), p.hi);
+            u64 ol = 1ull << p.lo, oh = 1ull << p.hi;
+            idx[0] = b;
+            idx[1] = b + ol;
+            idx[2] = b + oh;
+            idx[3] = b + ol + oh;
+        }
+        double2 x[W], y[W];
+#pragma unroll
+        for (int i = 0; i < W; ++i) x[i] = psi[idx[i]];
+
+        if constexpr (OP == OP_FWD || OP == OP_FWD_DOT) {
+            if constexpr (C1Q) mv2(p.A, P, x, y); else mv4<SP>(p.A, x, y);
+#pragma unroll
+            for (int i = 0; i < W; ++i) psi[idx[i]] = y[i];
+            if (OP == OP_FWD_DOT) {
+#pragma unroll
+                for (int i = 0; i < W; ++i) {
+                    double2 f = cscale(phi0[idx[i]], w);
+                    vre = fma(f.x, y[i].x, vre);
+                    vre = fma(-f.y, y[i].y, vre);
+                    vim = fma(f.x, y[i].y, vim);
+                    vim = fma(f.y, y[i].x, vim);
+                }
+            }
+        } else if constexpr (OP == OP_REV_G || OP == OP_REV_GH) {
+            // A = G^dag (uncompute psi), B = G^T (propagate bra), C = Z^T
+            double2 b[W], c[W];
+#pragma unroll
+            for (int i = 0; i < W; ++i) {
+                if (FIRST) {
+                    b[i] = cscale(phi0[idx[i]], w);
+                } else {
+                    b[i] = bra[idx[i]];
+                }
+            }
+            if (HAS_V) {
+#pragma unroll
+                for (int i = 0; i < W; ++i) {
+                    vre = fma(b[i].x, x[i].x, vre);
+                    vre = fma(-b[i].y, x[i].y, vre);
+                    vim = fma(b[i].x, x[i].y, vim);
+                    vim = fma(b[i].y, x[i].x, vim);
+                }
+            }
+            if constexpr (C1Q) mv2(p.A, P, x, y); else mv4<SP>(p.A, x, y);  // y = psi_l
+            if constexpr (C1Q) hole_acc2(accD, P, b, y); else hole_acc(accD, b, y);
+            if constexpr (OP == OP_REV_GH) {
+                if (!FIRST) {
+#pragma unroll
+                    for (int i = 0; i < W; ++i) c[i] = aux[idx[i]];
+                    if constexpr (C1Q) hole_acc2(accH, P, c, y); else hole_acc(accH, c, y);
+                }
+                double2 cn[W];
+                if (FIRST) {
+                    if constexpr (C1Q) mv2(p.C, P, b, cn); else mv4<SP>(p.C, b, cn);
+                } else {
+                    if constexpr (C1Q) mv2(p.B, P, c, cn); else mv4<SP>(p.B, c, cn);
+                    if constexpr (C1Q) mv2_acc(p.C, P, b, cn); else mv4_acc<SP>(p.C, b, cn);
+                }
+#pragma unroll
+                for (int i = 0; i < W; ++i) aux[idx[i]] = cn[i];
+            }
+            double2 bn[W];
+            if constexpr (C1Q) mv2(p.B, P, b, bn); else mv4<SP>(p.B, b, bn);
+#pragma unroll
+            for (int i = 0; i < W; ++i) {
+                psi[idx[i]] = y[i];
+                bra[idx[i]] = bn[i];
+            }
+        } else if constexpr (OP == OP_ASC_H) {
+            // A = conj(G) (recover bra), B = G (propagate v, psi), C = Z
+            double2 b[W], bn[W], v[W], vn[W];
+#pragma unroll
+            for (int i = 0; i < W; ++i) b[i] = bra[idx[i]];
+            if constexpr (C1Q) mv2(p.A, P, b, bn); else mv4<SP>(p.A, b, bn);
+            if (FIRST) {
+                if constexpr (C1Q) mv2(p.C, P, x, vn); else mv4<SP>(p.C, x, vn);
+            } else {
+#pragma unroll
+                for (int i = 0; i < W; ++i) v[i] = aux[idx[i]];
+                if constexpr (C1Q) hole_acc2(accH, P, bn, v); else hole_acc(accH, bn, v);
+                if constexpr (C1Q) mv2(p.B, P, v, vn); else mv4<SP>(p.B, v, vn);
+                if constexpr (C1Q) mv2_acc(p.C, P, x, vn); else mv4_acc<SP>(p.C, x, vn);
+            }
+            if constexpr (C1Q) mv2(p.B, P, x, y); else mv4<SP>(p.B, x, y);
+#pragma unroll
+            for (int i = 0; i < W; ++i) {
+                psi[idx[i]] = y[i];
+                bra[idx[i]] = bn[i];
+                aux[idx[i]] = vn[i];
+            }
+        }
+    }
+
+    __shared__ double red[kThreads / 32 * 32];
+    const u64 part = ((u64)blockIdx.y * gridDim.x + blockIdx.x);
+    if (HAS_D) {
+        double v = block_reduce32(accD, red);
+        if (threadIdx.x < 32) p.partD[part * 32 + threadIdx.x] = v;
+    }
+    if (HAS_H) {
+        double v = block_reduce32(accH, red);
+        if (threadIdx.x < 32) p.partH[part * 32 + threadIdx.x] = v;
+    }
+    if (HAS_V) {
+        double acc[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc[i] = 0.0;
+        acc[0] = vre;
+        acc[1] = vim;
+        // reuse the same deterministic block reduction (entries 0,1 used)
+        double v = block_reduce32(acc, red);
+        if (threadIdx.x < 2) p.partV[part * 2 + threadIdx.x] = v;
+    }
+}
+
+// |j> for every vector of the batch (basis index per vector).
+__global__ void k_init_basis(double2 *psi, u64 N, const int64_t *basis, int64_t nvec)
+{
+    const u64 total = N * (u64)nvec;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (u64)gridDim.x * blockDim.x) {
+        u64 b = i / N, x = i - b * N;
+        psi[i] = make_double2((int64_t)x == basis[b] ? 1.0 : 0.0, 0.0);
+    }
+}
+
+// part[s][b][c][32] -> q[s][b][32], summing c ascending.
+__global__ void k_reduce_ctas(const double *part, double *q, int64_t nsb, int ctas)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nsb * 32) return;
+    int64_t sb = i >> 5;
+    int e = (int)(i & 31);
+    const double *src = part + sb * ctas * 32 + e;
+    double acc = 0.0;
+    for (int c = 0; c < ctas; ++c) acc += src[(int64_t)c * 32];
+    q[i] = acc;
+}
+
+// Chunk records.  rec = [value(2)] [D: nlog*32] [H: nlog*32].
+__global__ void k_chunk_records(const double *qD, const double *qHd, const double *qHa, const double *partV,
+                                int64_t nvec, int ctas, int nslots, int nlog, const int *lstart,
+                                const int *lslots, const int *swapped, int chunk, int flags, double *out)
+{
+    const int rec = 2 + 64 * nlog;
+    const int64_t nchunks = (nvec + chunk - 1) / chunk;
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nchunks * rec) return;
+    const int64_t ch = i / rec;
+    const int r = (int)(i - ch * rec);
+    const int64_t b0 = ch * chunk, b1 = (nvec < b0 + chunk) ? nvec : (b0 + chunk);
+    double acc = 0.0;
+    if (r < 2) {
+        if (partV) {
+            for (int64_t b = b0; b < b1; ++b)
+                for (int c = 0; c < ctas; ++c) acc += partV[(b * ctas + c) * 2 + r];
+        }
+    } else {
+        int rr = r - 2;
+        const bool isH = rr >= 32 * nlog;
+        if (isH) rr -= 32 * nlog;
+        const int l = rr >> 5, q = rr & 31;
+        const int e = q >> 1, ri = q & 1;
+        const int ii = e >> 2, jj = e & 3;
+        const double *src = isH ? qHd : qD;
+        const bool want = isH ? (flags & 4) : (flags & 2);
+        if (want) {
+            for (int64_t b = b0; b < b1; ++b)
+                for (int t = lstart[l]; t < lstart[l + 1]; ++t) {
+                    int s = lslots[t];
+                    int si = ii, sj = jj;
+                    if (swapped[s]) {  // WIRE_SWAP = [0,2,1,3]
+                        si = (ii == 1) ? 2 : (ii == 2 ? 1 : ii);
+                        sj = (jj == 1) ? 2 : (jj == 2 ? 1 : jj);
+                    }
+                    int64_t o = ((int64_t)s * nvec + b) * 32 + 2 * (4 * si + sj) + ri;
+                    acc += src[o];
+                    if (isH) acc += qHa[o];
+                }
+        }
+    }
+    out[i] = acc;
+}
+
+// per-slot sums over the batch: q[s][b][32] -> out[s][32]
+__global__ void k_slot_sums(const double *q, const double *q2, int64_t nvec, int nslots, double *out)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nslots * 32) return;
+    int s = i >> 5, e = i & 31;
+    double acc = 0.0;
+    for (int64_t b = 0; b < nvec; ++b) {
+        acc += q[((int64_t)s * nvec + b) * 32 + e];
+        if (q2) acc += q2[((int64_t)s * nvec + b) * 32 + e];
+    }
+    out[i] = acc;
+}
+
+}  // namespace gf
+
+using namespace gf;
+
+// ---------------------------------------------------------------------------
+// plan
+// ---------------------------------------------------------------------------
+struct SlotInfo {
+    int q1, q2;  // normalised q1 < q2 (full-space qubits)
+    bool swapped;
+    int logical;
+    int mode_c1q;  // touches the implicit qubit in sector mode
+    int lo, hi;    // bit positions in the stored (compressed) space
+};
+
+struct gf_plan {
+    int k, K, sector, n, nlog, chunk;
+    int64_t max_batch;
+    u64 N;
+    int ctas;
+    std::vector<SlotInfo> slots;
+    std::vector<Mat4> G, Gd, Gt, Gc, Z, Zt;  // per slot, normalised orientation
+    std::vector<char> spG, spZ;
+    bool have_z = false;
+    double2 *psi = nullptr, *bra = nullptr, *aux = nullptr;
+    double *partD = nullptr, *partHd = nullptr, *partHa = nullptr, *partV = nullptr;
+    double *qD = nullptr, *qHd = nullptr, *qHa = nullptr;
+    int *d_lstart = nullptr, *d_lslots = nullptr, *d_swapped = nullptr;
+    int64_t last_launches = 0;
+    int last_flags = 0;
+};
+
+static Mat4 to_mat4(const double *m)
+{
+    Mat4 r;
+    for (int e = 0; e < 16; ++e) r.m[e] = make_double2(m[2 * e], m[2 * e + 1]);
+    return r;
+}
+
+static Mat4 wire_swap(const Mat4 &a)
+{
+    static const int s[4] = {0, 2, 1, 3};
+    Mat4 r;
+    for (int i = 0; i < 4; ++i)
+        for (int j = 0; j < 4; ++j) r.m[4 * i + j] = a.m[4 * s[i] + s[j]];
+    return r;
+}
+
+static Mat4 transpose(const Mat4 &a)
+{
+    Mat4 r;
+    for (int i = 0; i < 4; ++i)
+        for (int j = 0; j < 4; ++j) r.m[4 * i + j] = a.m[4 * j + i];
+    return r;
+}
+
+static Mat4 conjugate(const Mat4 &a)
+{
+    Mat4 r;
+    for (int e = 0; e < 16; ++e) r.m[e] = make_double2(a.m[e].x, -a.m[e].y);
+    return r;
+}
+
+static bool parity_zeros(const Mat4 &a)
+{
+    static const int off[8] = {1, 2, 4, 7, 8, 11, 13, 14};
+    for (int e : off)
+        if (a.m[e].x != 0.0 || a.m[e].y != 0.0) return false;
+    return true;
+}
+
+#define GF_CUDA(call)                                                                   \
+    do {                                                                                \
+        cudaError_t _e = (call);                                                        \
+        if (_e != cudaSuccess) {                                                        \
+            gf_set_error("%s:%d CUDA error %s (%s)", __FILE__, __LINE__,                \
+                         cudaGetErrorName(_e), cudaGetErrorString(_e));                 \
+            return _e == cudaErrorMemoryAllocation ? GF_ENOMEM : GF_ECUDA;             \
+        }                                                                               \
+    } while (0)
+
+static void plan_free(gf_plan *p)
+{
+    void *ptrs[] = {p->psi, p->bra, p->aux, p->partD, p->partHd, p->partHa, p->partV,
+                    p->qD, p->qHd, p->qHa, p->d_lstart, p->d_lslots, p->d_swapped};
+    for (void *q : ptrs)
+        if (q) cudaFree(q);
+}
+
+extern "C" int gf_plan_create(gf_plan **out, int k, int sector, int n_slots, const int32_t *t1, const int32_t *t2,
+                              const int32_t *logical, int n_logical, int64_t max_batch, int chunk_states)
+{
+    if (!out) return gf_fail(GF_EINVAL, "null plan pointer");
+    *out = nullptr;
+    if (k < 2 || k > 34) return gf_fail(GF_EINVAL, "qubit count %d out of range [2, 34]", k);
+    if (sector < -1 || sector > 1) return gf_fail(GF_EINVAL, "sector must be -1, 0 or 1");
+    if (n_slots < 0 || n_logical < 0 || max_batch < 1 || chunk_states < 1)
+        return gf_fail(GF_EINVAL, "bad plan sizes");
+    gf_plan *p = new gf_plan();
+    p->k = k;
+    p->sector = sector;
+    p->K = sector >= 0 ? k - 1 : k;
+    p->n = n_slots;
+    p->nlog = n_logical;
+    p->max_batch = max_batch;
+    p->chunk = chunk_states;
+    p->N = 1ull << p->K;
+    if (p->K < 2) {
+        delete p;
+        return gf_fail(GF_EINVAL, "state space too small");
+    }
+    for (int s = 0; s < n_slots; ++s) {
+        int a = t1[s], b = t2[s];
+        if (a == b || a < 0 || b < 0 || a >= k || b >= k) {
+            delete p;
+            return gf_fail(GF_EINVAL, "invalid slot targets (%d, %d) for %d qubits", a, b, k);
+        }
+        if (logical[s] < 0 || logical[s] >= n_logical) {
+            delete p;
+            return gf_fail(GF_EINVAL, "slot references unknown logical gate %d", logical[s]);
+        }
+        SlotInfo si;
+        si.swapped = a > b;
+        si.q1 = std::min(a, b);
+        si.q2 = std::max(a, b);
+        si.logical = logical[s];
+        si.mode_c1q = (sector >= 0 && si.q2 == k - 1);
+        if (si.mode_c1q) {
+            si.lo = p->K - 1 - si.q1;  // compressed position of qubit q1
+            si.hi = -1;
+        } else {
+            si.lo = p->K - 1 - si.q2;
+            si.hi = p->K - 1 - si.q1;
+        }
+        p->slots.push_back(si);
+    }
+    u64 units = p->N / 4;
+    int64_t ctas = (int64_t)(units / (kThreads * 4));
+    p->ctas = (int)std::max<int64_t>(1, std::min<int64_t>(ctas, 148 * 8));
+    // workspace
+    size_t vbytes = sizeof(double2) * p->N * (size_t)max_batch;
+    size_t pbytes = sizeof(double) * 32 * (size_t)p->ctas * max_batch * std::max(1, n_slots);
+    size_t qbytes = sizeof(double) * 32 * (size_t)max_batch * std::max(1, n_slots);
+    cudaError_t e = cudaSuccess;
+    if (e == cudaSuccess) e = cudaMalloc(&p->psi, vbytes);
+    if (e == cudaSuccess) e = cudaMalloc(&p->bra, vbytes);
+    if (e == cudaSuccess) e = cudaMalloc(&p->aux, vbytes);
+    if (e == cudaSuccess) e = cudaMalloc(&p->partD, pbytes);
+    if (e == cudaSuccess) e = cudaMalloc(&p->partHd, pbytes);
+    if (e == cudaSuccess) e = cudaMalloc(&p->partHa, pbytes);
+    if (e == cudaSuccess) e = cudaMalloc(&p->partV, sizeof(double) * 2 * (size_t)p->ctas * max_batch);
+    if (e == cudaSuccess) e = cudaMalloc(&p->qD, qbytes);
+    if (e == cudaSuccess) e = cudaMalloc(&p->qHd, qbytes);
+    if (e == cudaSuccess) e = cudaMalloc(&p->qHa, qbytes);
+    // logical -> slot CSR
+    std::vector<int> lstart(n_logical + 1, 0), lslots, sw(std::max(1, n_slots), 0);
+    for (int l = 0; l < n_logical; ++l) {
+        lstart[l] = (int)lslots.size();
+        for (int s = 0; s < n_slots; ++s)
+            if (p->slots[s].logical == l) lslots.push_back(s);
+    }
+    lstart[n_logical] = (int)lslots.size();
+    for (int s = 0; s < n_slots; ++s) sw[s] = p->slots[s].swapped;
+    if (lslots.empty()) lslots.push_back(0);
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_lstart, sizeof(int) * lstart.size());
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_lslots, sizeof(int) * lslots.size());
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_swapped, sizeof(int) * sw.size());
+    if (e == cudaSuccess) e = cudaMemcpy(p->d_lstart, lstart.data(), sizeof(int) * lstart.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(p->d_lslots, lslots.data(), sizeof(int) * lslots.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(p->d_swapped, sw.data(), sizeof(int) * sw.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        plan_free(p);
+        delete p;
+        cudaGetLastError();
+        return gf_fail(e == cudaErrorMemoryAllocation ? GF_ENOMEM : GF_ECUDA, "plan workspace: %s",
+                       cudaGetErrorString(e));
+    }
+    *out = p;
+    return GF_OK;
+}
+
+extern "C" int gf_plan_set_gates(gf_plan *p, const double *mats)
+{
+    if (!p || !mats) return gf_fail(GF_EINVAL, "null argument");
+    p->G.resize(p->n); p->Gd.resize(p->n); p->Gt.resize(p->n); p->Gc.resize(p->n);
+    p->spG.assign(p->n, 0);
+    for (int s = 0; s < p->n; ++s) {
+        Mat4 g = to_mat4(mats + 32 * p->slots[s].logical);
+        if (p->slots[s].swapped) g = wire_swap(g);
+        if (p->slots[s].mode_c1q && !parity_zeros(g))
+            return gf_fail(GF_EINVAL, "slot %d acts on the compressed qubit but its gate is not parity-conserving", s);
+        p->G[s] = g;
+        p->Gt[s] = transpose(g);
+        p->Gc[s] = conjugate(g);
+        p->Gd[s] = conjugate(p->Gt[s]);
+        p->spG[s] = parity_zeros(g);
+    }
+    return GF_OK;
+}
+
+extern "C" int gf_plan_set_directions(gf_plan *p, const double *zmats)
+{
+    if (!p || !zmats) return gf_fail(GF_EINVAL, "null argument");
+    p->Z.resize(p->n); p->Zt.resize(p->n);
+    p->spZ.assign(p->n, 0);
+    for (int s = 0; s < p->n; ++s) {
+        Mat4 z = to_mat4(zmats + 32 * p->slots[s].logical);
+        if (p->slots[s].swapped) z = wire_swap(z);
+        if (p->sector >= 0 && !parity_zeros(z))
+            return gf_fail(GF_EINVAL, "sector-compressed HVP needs parity-conserving directions (slot %d)", s);
+        p->Z[s] = z;
+        p->Zt[s] = transpose(z);
+        p->spZ[s] = parity_zeros(z);
+    }
+    p->have_z = true;
+    return GF_OK;
+}
+
+template <int OP, bool FIRST>
+static void launch_sweep(const gf_plan *p, const SlotInfo &si, bool sparse, SweepParams &sp, int64_t nvec,
+                         cudaStream_t st)
+{
+    dim3 grid(p->ctas, (unsigned)nvec);
+    if (si.mode_c1q) {
+        sp.nunits = p->N / 2;
+        k_sweep<OP, MODE_C1Q, FIRST><<<grid, kThreads, 0, st>>>(sp);
+    } else {
+        sp.nunits = p->N / 4;
+        if (sparse)
+            k_sweep<OP, MODE_SPARSE, FIRST><<<grid, kThreads, 0, st>>>(sp);
+        else
+            k_sweep<OP, MODE_DENSE, FIRST><<<grid, kThreads, 0, st>>>(sp);
+    }
+}
+
+extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *basis, const double *weights,
+                            const void *phi0, double *out, void *stream)
+{
+    if (!p) return gf_fail(GF_EINVAL, "null plan");
+    if (nvec < 1 || nvec > p->max_batch)
+        return gf_fail(GF_EINVAL, "batch of %lld summands outside [1, %lld]", (long long)nvec, (long long)p->max_batch);
+    if (!basis || !phi0 || !out) return gf_fail(GF_EINVAL, "null device buffer");
+    if (p->G.size() != (size_t)p->n) return gf_fail(GF_EINVAL, "gates not set");
+    if ((flags & GF_HVP) && !p->have_z) return gf_fail(GF_EINVAL, "HVP requested but no directions set");
+    if (!(flags & (GF_VALUE | GF_GRAD | GF_HVP))) return gf_fail(GF_EINVAL, "empty flags");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int n = p->n;
+    int64_t launches = 0;
+    SweepParams sp;
+    memset(&sp, 0, sizeof sp);
+    sp.psi = p->psi;
+    sp.bra = p->bra;
+    sp.aux = p->aux;
+    sp.phi0 = (const double2 *)phi0;
+    sp.weights = weights;
+    sp.N = p->N;
+    sp.sector = p->sector < 0 ? 0 : p->sector;
+    const size_t pstride = (size_t)32 * p->ctas * nvec;
+
+    {
+        u64 total = p->N * (u64)nvec;
+        int blocks = (int)std::min<u64>((total + 255) / 256, 148 * 16);
+        k_init_basis<<<blocks, 256, 0, st>>>(p->psi, p->N, basis, nvec);
+        ++launches;
+    }
+    const bool grad_like = (flags & (GF_GRAD | GF_HVP)) != 0;
+    if (n == 0) {
+        // empty circuit: value = sum phi0 . |j>; an identity "slot" with the dot fused
+        Mat4 I;
+        for (int e = 0; e < 16; ++e) I.m[e] = make_double2((e % 5 == 0) ? 1.0 : 0.0, 0.0);
+        SlotInfo si;
+        si.q1 = 0; si.q2 = 1; si.swapped = false; si.logical = 0; si.mode_c1q = 0; si.lo = 0; si.hi = 1;
+        sp.lo = 0; sp.hi = 1; sp.A = I; sp.partV = p->partV;
+        launch_sweep<OP_FWD_DOT, false>(p, si, false, sp, nvec, st);
+        ++launches;
+    }
+    // forward sweep
+    for (int s = 0; s < n; ++s) {
+        const SlotInfo &si = p->slots[s];
+        sp.lo = si.lo;
+        sp.hi = si.hi;
+        sp.A = p->G[s];
+        if (!grad_like && s == n - 1) {
+            sp.partV = p->partV;
+            launch_sweep<OP_FWD_DOT, false>(p, si, p->spG[s], sp, nvec, st);
+        } else {
+            launch_sweep<OP_FWD, false>(p, si, p->spG[s], sp, nvec, st);
+        }
+        ++launches;
+    }
+    if (grad_like && n > 0) {
+        const bool h = (flags & GF_HVP) != 0;
+        for (int s = n - 1; s >= 0; --s) {
+            const SlotInfo &si = p->slots[s];
+            sp.lo = si.lo;
+            sp.hi = si.hi;
+            sp.A = p->Gd[s];
+            sp.B = p->Gt[s];
+            sp.partD = p->partD + pstride * s;
+            sp.partV = p->partV;
+            const bool first = (s == n - 1);
+            if (h) {
+                sp.C = p->Zt[s];
+                sp.partH = p->partHd + pstride * s;
+                bool sparse = p->spG[s] && p->spZ[s];
+                if (first) launch_sweep<OP_REV_GH, true>(p, si, sparse, sp, nvec, st);
+                else launch_sweep<OP_REV_GH, false>(p, si, sparse, sp, nvec, st);
+            } else {
+                if (first) launch_sweep<OP_REV_G, true>(p, si, p->spG[s], sp, nvec, st);
+                else launch_sweep<OP_REV_G, false>(p, si, p->spG[s], sp, nvec, st);
+            }
+            ++launches;
+        }
+        if (h) {
+            for (int s = 0; s < n; ++s) {
+                const SlotInfo &si = p->slots[s];
+                sp.lo = si.lo;
+                sp.hi = si.hi;
+                sp.A = p->Gc[s];
+                sp.B = p->G[s];
+                sp.C = p->Z[s];
+                sp.partH = p->partHa + pstride * s;
+                bool sparse = p->spG[s] && p->spZ[s];
+                if (s == 0) launch_sweep<OP_ASC_H, true>(p, si, sparse, sp, nvec, st);
+                else launch_sweep<OP_ASC_H, false>(p, si, sparse, sp, nvec, st);
+                ++launches;
+            }
+        }
+    }
+    if (grad_like && n > 0) {
+        int64_t nsb = (int64_t)n * nvec;
+        int blocks = (int)((nsb * 32 + 255) / 256);
+        k_reduce_ctas<<<blocks, 256, 0, st>>>(p->partD, p->qD, nsb, p->ctas);
+        ++launches;
+        if (flags & GF_HVP) {
+            k_reduce_ctas<<<blocks, 256, 0, st>>>(p->partHd, p->qHd, nsb, p->ctas);
+            k_reduce_ctas<<<blocks, 256, 0, st>>>(p->partHa, p->qHa, nsb, p->ctas);
+            launches += 2;
+        }
+    }
+    {
+        int64_t nchunks = (nvec + p->chunk - 1) / p->chunk;
+        int rec = 2 + 64 * p->nlog;
+        int64_t tot = nchunks * rec;
+        int eff = (n > 0) ? flags : (flags & GF_VALUE);
+        k_chunk_records<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
+            p->qD, p->qHd, p->qHa, p->partV, nvec, p->ctas, n, p->nlog, p->d_lstart, p->d_lslots, p->d_swapped,
+            p->chunk, eff, out);
+        ++launches;
+    }
+    GF_CUDA(cudaGetLastError());
+    p->last_launches = launches;
+    p->last_flags = flags;
+    return GF_OK;
+}
+
+extern "C" int gf_plan_slot_outputs(gf_plan *p, int64_t nvec, double *d_dev, double *h_dev, void *stream)
+{
+    if (!p || nvec < 1 || nvec > p->max_batch) return gf_fail(GF_EINVAL, "bad arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    int blocks = (p->n * 32 + 255) / 256;
+    if (blocks == 0) return GF_OK;
+    if (d_dev) k_slot_sums<<<blocks, 256, 0, st>>>(p->qD, nullptr, nvec, p->n, d_dev);
+    if (h_dev) k_slot_sums<<<blocks, 256, 0, st>>>(p->qHd, p->qHa, nvec, p->n, h_dev);
+    GF_CUDA(cudaGetLastError());
+    return GF_OK;
+}
+
+extern "C" int64_t gf_plan_last_launches(const gf_plan *p) { return p ? p->last_launches : 0; }
+
+extern "C" int gf_plan_destroy(gf_plan *p)
+{
+    if (!p) return GF_OK;
+    plan_free(p);
+    delete p;
+    return GF_OK;
+}

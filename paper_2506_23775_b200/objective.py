@@ -1,0 +1,639 @@
+"""Basis-sum objective, gradient, Hessian-vector product and Hessian on the GPU.
+
+Drop-in for the public API of the reference ``gatefit.objective``
+(reference objective.py:586-814): the same functions, arguments, return
+types, orientation conventions and exceptions.  The per-summand passes and
+the reduction over basis states run in libgfcuda.so (gf_plan_eval); this
+module only plans batches, fetches target columns from the oracle, shards
+chunks over ranks and converts holomorphic derivatives to Riemannian
+gradients on the host.
+
+f(G) = -Re Tr[U^dag C(G)] = -Re sum_j phi0_j . C|j>,  phi0_j = conj(U|j>)
+(reference objective.py:1-10).  Extra keyword-only options (no reference
+counterpart):
+
+* ``sector`` -- None (reference semantics), "even"/"odd" or 0/1: restrict the
+  basis sum to a parity sector and store vectors compressed on qubit k-1
+  (gates touching it become parity-controlled one-qubit gates);
+* ``fold`` -- with a sector, sum over lattice-translation orbit
+  representatives weighted by orbit size (periodic, translation-invariant
+  circuit and target only);
+* ``basis`` -- explicit ``(indices, weights)`` sample of stored-space indices;
+* ``batch`` / ``chunk`` -- summands per engine call / per output record.
+
+Reductions are deterministic: every summand is reduced by a fixed CTA tree,
+chunks of ``chunk`` consecutive summands form records, and records are
+summed in ascending chunk order -- bit-identical for any batch size and any
+number of GPUs (the reference's worker-count invariance,
+objective.py:490-533).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib, manifold
+from .circuit import Circuit, accumulate_shared, translation_classes
+from .kernels import DENSE_SUPPORT, PARITY_SUPPORT, WIRE_SWAP, Gate, apply_gate, basis_state, hole_contract
+
+__all__ = [
+    "PassCache",
+    "HessianBlocks",
+    "ObjectiveReport",
+    "target_value",
+    "summand_gradient",
+    "full_gradient",
+    "gradient_and_hvp",
+    "full_hessian",
+    "hessian_vector_product",
+    "build_pass_cache",
+    "parallel_reduce",
+    "chunk_bounds",
+    "frobenius_error_squared",
+    "default_workers",
+    "BasisSpec",
+]
+
+COUNT_NAMES = (
+    "gate_applications",
+    "array_gate_applications",
+    "hole_applications",
+    "hole_contractions",
+    "pair_contractions",
+)
+CHUNK_STATES = 64  # reference objective.py:75
+
+
+def default_workers() -> int:
+    """RQCO_WORKERS (reference objective.py:78-83); accepted for API parity --
+    the GPU engine does not use host worker threads."""
+    try:
+        return max(1, int(os.environ.get("RQCO_WORKERS", "1")))
+    except ValueError:
+        return 1
+
+
+@dataclass
+class PassCache:
+    forward_states: list
+    backward_states: list
+
+
+@dataclass
+class HessianBlocks:
+    """Upper-triangular holomorphic second-derivative blocks keyed (a, b),
+    a <= b, over ``support`` entries (reference objective.py:99-131)."""
+
+    num_logical: int
+    support: np.ndarray
+    blocks: dict
+
+    def apply_direction(self, directions):
+        if len(directions) != self.num_logical:
+            raise ValueError("need one direction matrix per logical gate")
+        sup = np.asarray(self.support)
+        z = [np.asarray(d, dtype=np.complex128).reshape(16)[sup] for d in directions]
+        acc = [np.zeros(sup.size, dtype=np.complex128) for _ in range(self.num_logical)]
+        for (a, b), blk in self.blocks.items():
+            acc[a] += blk @ z[b]
+            if a != b:
+                acc[b] += blk.T @ z[a]
+        out = []
+        for v in acc:
+            m = np.zeros(16, dtype=np.complex128)
+            m[sup] = v
+            out.append(m.reshape(4, 4))
+        return out
+
+
+@dataclass
+class ObjectiveReport:
+    value: float
+    per_logical_gradient: list | None = None
+    euclidean_gradients: list | None = None
+    holomorphic_derivatives: list | None = None
+    hessian: HessianBlocks | None = None
+    wall_time: float = 0.0
+    pass_counts: dict = field(default_factory=dict)
+    engine: dict = field(default_factory=dict)
+
+
+def frobenius_error_squared(value: float, num_qubits: int) -> float:
+    """||C - U||_F^2 = 2 Tr[I] + 2 f (reference objective.py:147-149)."""
+    return 2.0 * 2**num_qubits + 2.0 * value
+
+
+def chunk_bounds(total: int, num_chunks: int | None = None):
+    """Contiguous near-equal chunks covering range(total) (reference
+    objective.py:490-510)."""
+    if total < 0:
+        raise ValueError("total must be non-negative")
+    if total == 0:
+        return []
+    nc = max(1, total // CHUNK_STATES) if num_chunks is None else num_chunks
+    nc = max(1, min(nc, total))
+    q, r = divmod(total, nc)
+    edges = np.cumsum([0] + [q + (1 if c < r else 0) for c in range(nc)])
+    return [(int(a), int(b)) for a, b in zip(edges[:-1], edges[1:])]
+
+
+def parallel_reduce(num_items: int, evaluate_chunk, worker_count: int = 1):
+    """Fixed chunks, partials combined with + in ascending order (reference
+    objective.py:513-533).  Host helper kept for API parity."""
+    if worker_count < 1:
+        raise ValueError("worker_count must be >= 1")
+    bounds = chunk_bounds(num_items)
+    if not bounds:
+        return None
+    if worker_count == 1:
+        parts = [evaluate_chunk(a, b) for a, b in bounds]
+    else:
+        from concurrent.futures import ThreadPoolExecutor
+
+        with ThreadPoolExecutor(max_workers=worker_count) as ex:
+            parts = list(ex.map(lambda ab: evaluate_chunk(*ab), bounds))
+    total = parts[0]
+    for p in parts[1:]:
+        total = total + p
+    return total
+
+
+# ---------------------------------------------------------------------------
+# engine plan (C ABI) and basis planning
+# ---------------------------------------------------------------------------
+
+
+def _sector_code(sector) -> int:
+    if sector is None:
+        return -1
+    if sector in ("even", 0):
+        return 0
+    if sector in ("odd", 1):
+        return 1
+    raise ValueError(f"unknown sector {sector!r}")
+
+
+class EnginePlan:
+    """Owns one gf_plan (device workspace for `batch` summands)."""
+
+    def __init__(self, circuit: Circuit, sector: int, batch: int, chunk: int):
+        t1, t2, lid = circuit.slot_arrays()
+        self.k = circuit.num_qubits
+        self.sector = sector
+        self.batch = batch
+        self.chunk = chunk
+        self.nlog = circuit.num_logical
+        self.n = circuit.num_slots
+        self.N = 1 << (self.k - (1 if sector >= 0 else 0))
+        self.rec = 2 + 64 * self.nlog
+        h = ctypes.c_void_p()
+        self._keep = (t1, t2, lid)
+        with torch.cuda.device(torch.cuda.current_device()):
+            _lib.check(_lib.lib.gf_plan_create(ctypes.byref(h), self.k, sector, self.n, t1.ctypes.data,
+                                               t2.ctypes.data, lid.ctypes.data, self.nlog, batch, chunk))
+        self.h = h
+        self.device = torch.device("cuda", torch.cuda.current_device())
+
+    def set_gates(self, mats: np.ndarray):
+        m = np.ascontiguousarray(mats, dtype=np.complex128)
+        _lib.check(_lib.lib.gf_plan_set_gates(self.h, m.ctypes.data))
+
+    def set_directions(self, zmats: np.ndarray):
+        z = np.ascontiguousarray(zmats, dtype=np.complex128)
+        _lib.check(_lib.lib.gf_plan_set_directions(self.h, z.ctypes.data))
+
+    def eval(self, flags, nvec, basis, weights, phi0, out):
+        _lib.check(_lib.lib.gf_plan_eval(self.h, flags, nvec, basis.data_ptr(),
+                                         None if weights is None else weights.data_ptr(), phi0.data_ptr(),
+                                         out.data_ptr(), _lib.stream_ptr()))
+
+    def last_launches(self) -> int:
+        return int(_lib.lib.gf_plan_last_launches(self.h))
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value:
+            try:
+                _lib.lib.gf_plan_destroy(h)
+            except Exception:  # interpreter shutdown
+                pass
+
+
+_PLANS: dict = {}
+
+
+def _get_plan(circuit: Circuit, sector: int, batch: int, chunk: int) -> EnginePlan:
+    t1, t2, lid = circuit.slot_arrays()
+    key = (torch.cuda.current_device(), circuit.num_qubits, sector, t1.tobytes(), t2.tobytes(), lid.tobytes(),
+           circuit.num_logical, batch, chunk)
+    plan = _PLANS.get(key)
+    if plan is None:
+        while len(_PLANS) >= 4:
+            _PLANS.pop(next(iter(_PLANS)))
+        plan = EnginePlan(circuit, sector, batch, chunk)
+        _PLANS[key] = plan
+    return plan
+
+
+@dataclass
+class BasisSpec:
+    """Summands of the basis sum in stored (possibly compressed) space.
+
+    ``indices`` None means all stored indices 0..total-1 (contiguous)."""
+
+    total: int
+    indices: np.ndarray | None = None
+    weights: np.ndarray | None = None
+
+    def weight_sum(self) -> float:
+        return float(self.total if self.weights is None else np.sum(self.weights))
+
+
+def _default_batch(N: int, total: int) -> int:
+    env = os.environ.get("GF_BATCH")
+    if env:
+        return max(1, min(int(env), total))
+    budget = 64 * 2**20  # bytes per workspace vector set member
+    return max(1, min(total, budget // (16 * N)))
+
+
+def fold_basis(k: int, sector: int, L: int | None = None) -> BasisSpec:
+    """Translation-orbit representatives of the sector with orbit sizes
+    (computed on the GPU by gf_sector_orbit_mark)."""
+    if sector < 0:
+        raise ValueError("translation folding needs a parity sector")
+    if L is None:
+        if k % 2:
+            raise ValueError("folding needs a spinful chain (even qubit count)")
+        L = k // 2
+    M = 1 << (k - 1)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    reps, ws = [], []
+    step = 1 << 26
+    for i0 in range(0, M, step):
+        m = min(step, M - i0)
+        mark = torch.empty(m, dtype=torch.int32, device=dev)
+        _lib.check(_lib.lib.gf_sector_orbit_mark(i0, m, L, sector, mark.data_ptr(), _lib.stream_ptr()))
+        nz = torch.nonzero(mark).flatten()
+        reps.append((nz + i0).cpu().numpy())
+        ws.append(mark[nz].to(torch.float64).cpu().numpy())
+    idx = np.concatenate(reps).astype(np.int64)
+    return BasisSpec(int(idx.size), idx, np.concatenate(ws))
+
+
+def _resolve_basis(k, sector, fold, basis) -> BasisSpec:
+    N = 1 << (k - (1 if sector >= 0 else 0))
+    if basis is not None:
+        if fold:
+            raise ValueError("pass either fold=True or an explicit basis, not both")
+        if isinstance(basis, BasisSpec):
+            return basis
+        idx, w = basis if isinstance(basis, tuple) else (basis, None)
+        idx = np.ascontiguousarray(idx, dtype=np.int64)
+        if idx.size and (idx.min() < 0 or idx.max() >= N):
+            raise ValueError("basis index out of range")
+        return BasisSpec(int(idx.size), idx, None if w is None else np.ascontiguousarray(w, dtype=np.float64))
+    if fold:
+        return fold_basis(k, sector)
+    return BasisSpec(N)
+
+
+def _dist_info(distributed):
+    if distributed is False:
+        return 0, 1, None
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        return dist.get_rank(), dist.get_world_size(), dist
+    return 0, 1, None
+
+
+def shard_chunks(nchunks: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous chunk range of one rank (no data-path collective)."""
+    lo = (nchunks * rank) // world
+    hi = (nchunks * (rank + 1)) // world
+    return lo, hi
+
+
+def gather_records(local: torch.Tensor, lo: int, nchunks: int, rank: int, world: int, dist) -> torch.Tensor:
+    """All-gather per-chunk records so every rank holds all chunks in order.
+
+    Records are tiny (2 + 64 n_log doubles per chunk); the all-gather is the
+    only collective of an evaluation (NCCL over NVLink, gloo in CPU tests)."""
+    if dist is None:
+        return local
+    counts = [shard_chunks(nchunks, r, world) for r in range(world)]
+    width = max(h - l for l, h in counts)
+    pad = torch.zeros((width, local.shape[1]), dtype=local.dtype, device=local.device)
+    pad[: local.shape[0]] = local
+    bufs = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(bufs, pad)
+    return torch.cat([b[: h - l] for b, (l, h) in zip(bufs, counts)], dim=0)
+
+
+def ordered_sum(records: np.ndarray) -> np.ndarray:
+    """Sum chunk records in ascending chunk order (deterministic)."""
+    acc = np.zeros(records.shape[1], dtype=np.float64)
+    for r in records:
+        acc += r
+    return acc
+
+
+def _host_phi0(oracle, js_full: np.ndarray, k: int, sector: int) -> np.ndarray:
+    """Generic duck-typed oracle (reference _phi_block, objective.py:561-565)."""
+    rows = []
+    sel = None
+    if sector >= 0:
+        i = np.arange(1 << (k - 1), dtype=np.int64)
+        pc = np.array([bin(int(v)).count("1") & 1 for v in i], dtype=np.int64)
+        sel = (i << 1) | (pc ^ sector)
+    for j in js_full:
+        col = np.conj(np.asarray(oracle.apply(basis_state(k, int(j))), dtype=np.complex128))
+        rows.append(col if sel is None else col[sel])
+    return np.ascontiguousarray(np.stack(rows))
+
+
+class _Run:
+    """One basis-sum evaluation (value / gradient / HVP) on this rank."""
+
+    def __init__(self, circuit, oracle, flags, directions, sector, fold, basis, batch, chunk, distributed):
+        self.k = circuit.num_qubits
+        self.sector = _sector_code(sector)
+        self.circuit = circuit
+        self.flags = flags
+        self.spec = _resolve_basis(self.k, self.sector, fold, basis)
+        self.N = 1 << (self.k - (1 if self.sector >= 0 else 0))
+        total = self.spec.total
+        self.batch = batch or _default_batch(self.N, max(total, 1))
+        self.chunk = chunk or min(CHUNK_STATES, self.batch)
+        if self.batch % self.chunk:
+            self.batch = max(self.chunk, (self.batch // self.chunk) * self.chunk)
+        self.rank, self.world, self.dist = _dist_info(distributed)
+        self.plan = _get_plan(circuit, self.sector, self.batch, self.chunk)
+        self.plan.set_gates(circuit.gate_stack())
+        if flags & _lib.GF_HVP:
+            self.plan.set_directions(directions)
+        self.oracle = oracle
+
+    def run(self):
+        dev = self.plan.device
+        total, chunk = self.spec.total, self.chunk
+        nchunks = (total + chunk - 1) // chunk
+        lo, hi = shard_chunks(nchunks, self.rank, self.world)
+        rec = self.plan.rec
+        local = torch.zeros((hi - lo, rec), dtype=torch.float64, device=dev)
+        phi0 = torch.empty((self.batch, self.N), dtype=torch.complex128, device=dev)
+        idx_all = None if self.spec.indices is None else torch.from_numpy(self.spec.indices).to(dev)
+        w_all = None if self.spec.weights is None else torch.from_numpy(self.spec.weights).to(dev)
+        launches = 0
+        t0 = time.perf_counter()
+        s0, s1 = lo * chunk, min(total, hi * chunk)
+        pos = s0
+        while pos < s1:
+            nvec = min(self.batch, s1 - pos)
+            if idx_all is None:
+                basis = torch.arange(pos, pos + nvec, dtype=torch.int64, device=dev)
+            else:
+                basis = idx_all[pos:pos + nvec].contiguous()
+            weights = None if w_all is None else w_all[pos:pos + nvec].contiguous()
+            self._fill_phi0(basis, phi0[:nvec])
+            c0 = (pos // chunk) - lo
+            nc = (nvec + chunk - 1) // chunk
+            self.plan.eval(self.flags, nvec, basis, weights, phi0, local[c0:c0 + nc])
+            launches += self.plan.last_launches()
+            pos += nvec
+        allrec = gather_records(local, lo, nchunks, self.rank, self.world, self.dist)
+        host = allrec.cpu().numpy()
+        self.elapsed = time.perf_counter() - t0
+        self.launches = launches
+        tot = ordered_sum(host) if host.shape[0] else np.zeros(rec)
+        nlog = self.circuit.num_logical
+        value = complex(tot[0], tot[1])
+        d = tot[2:2 + 32 * nlog].view(np.complex128).reshape(nlog, 4, 4).copy()
+        h = tot[2 + 32 * nlog:].view(np.complex128).reshape(nlog, 4, 4).copy()
+        return value, d, h
+
+    def _fill_phi0(self, basis: torch.Tensor, out: torch.Tensor):
+        if self.sector >= 0:
+            js_full = torch.empty_like(basis)
+            _lib.check(_lib.lib.gf_sector_unrank(basis.data_ptr(), basis.numel(), self.sector, js_full.data_ptr(),
+                                                 _lib.stream_ptr()))
+        else:
+            js_full = basis
+        fn = getattr(self.oracle, "phi0_into", None)
+        if fn is not None:
+            fn(js_full, None if self.sector < 0 else self.sector, out)
+            return
+        host = _host_phi0(self.oracle, js_full.cpu().numpy(), self.k, self.sector)
+        out.copy_(torch.from_numpy(host).to(out.device, non_blocking=False))
+
+
+def _check_oracle(circuit, oracle):
+    if oracle.num_qubits != circuit.num_qubits:
+        raise ValueError(f"oracle acts on {oracle.num_qubits} qubits, circuit on {circuit.num_qubits}")
+
+
+def _assert_bounded(value: float, bound: float):
+    """Cauchy-Schwarz: f >= -(number of weighted summands) (reference
+    objective.py:575-578 with Tr[I] = 2^k)."""
+    if value < -bound * (1.0 + 1e-9) - 1e-9:
+        raise FloatingPointError(f"objective {value} below the -{bound:g} trace bound")
+
+
+def _riemannian(circuit, holo, parity_mode):
+    euclid = [manifold.euclid_gradient_from_holomorphic(d) for d in holo]
+    riem = [manifold.project_tangent_gate(g.matrix, e, parity_mode) for g, e in zip(circuit.logical_gates, euclid)]
+    return euclid, riem
+
+
+def _ref_counts(n: int, S: int, kind: str, pairs: int = 0, firsts: int = 0, arrays: int = 0):
+    """Pass counters with the reference's semantics (objective.py:65-73)."""
+    c = dict.fromkeys(COUNT_NAMES, 0)
+    if kind == "value":
+        c["gate_applications"] = n * S
+    elif kind == "gradient":
+        c["gate_applications"] = 2 * n * S
+        c["hole_contractions"] = n * S
+    elif kind == "hvp":
+        c["gate_applications"] = (2 * n + 4 * max(n - 1, 0)) * S
+        c["hole_contractions"] = 2 * max(n - 1, 0) * S
+    elif kind == "hessian":
+        c["gate_applications"] = 2 * n * S
+        c["hole_contractions"] = n * S
+        c["pair_contractions"] = pairs * S
+        c["hole_applications"] = firsts * S
+        c["array_gate_applications"] = arrays * S
+    return c
+
+
+def _slot_directions(circuit, directions):
+    if len(directions) != circuit.num_logical:
+        raise ValueError("need one direction matrix per logical gate")
+    return np.ascontiguousarray(np.stack([np.asarray(z, dtype=np.complex128).reshape(4, 4) for z in directions]))
+
+
+# ---------------------------------------------------------------------------
+# public API
+# ---------------------------------------------------------------------------
+
+
+def target_value(circuit: Circuit, oracle, workers: int | None = None, *, sector=None, fold=False, basis=None,
+                 batch=None, chunk=None, distributed=None) -> float:
+    """f = -Re Tr[U^dag C] (reference objective.py:586-608)."""
+    _check_oracle(circuit, oracle)
+    run = _Run(circuit, oracle, _lib.GF_VALUE, None, sector, fold, basis, batch, chunk, distributed)
+    value, _, _ = run.run()
+    f = float(-value.real)
+    _assert_bounded(f, run.spec.weight_sum())
+    return f
+
+
+def _grad_report(circuit, run, value, holo, parity_mode, kind, t0, hvp=None):
+    f = float(-value.real)
+    _assert_bounded(f, run.spec.weight_sum())
+    holo_l = [holo[i] for i in range(circuit.num_logical)]
+    euclid, riem = _riemannian(circuit, holo_l, parity_mode)
+    S = run.spec.total
+    return ObjectiveReport(
+        value=f,
+        per_logical_gradient=riem,
+        euclidean_gradients=euclid,
+        holomorphic_derivatives=holo_l,
+        wall_time=time.perf_counter() - t0,
+        pass_counts=_ref_counts(circuit.num_slots, S, kind),
+        engine={"launches": run.launches, "summands": S, "batch": run.batch, "chunk": run.chunk,
+                "seconds": run.elapsed, "world": run.world},
+    )
+
+
+def full_gradient(circuit: Circuit, oracle, workers: int | None = None, parity_mode: bool = False, *, sector=None,
+                  fold=False, basis=None, batch=None, chunk=None, distributed=None) -> ObjectiveReport:
+    """Value and Riemannian gradient per logical gate (reference
+    objective.py:659-698)."""
+    _check_oracle(circuit, oracle)
+    t0 = time.perf_counter()
+    run = _Run(circuit, oracle, _lib.GF_VALUE | _lib.GF_GRAD, None, sector, fold, basis, batch, chunk, distributed)
+    value, d, _ = run.run()
+    return _grad_report(circuit, run, value, d, parity_mode, "gradient", t0)
+
+
+def gradient_and_hvp(circuit: Circuit, oracle, directions, parity_mode: bool = False, *, sector=None, fold=False,
+                     basis=None, batch=None, chunk=None, distributed=None):
+    """Fused value + gradient + one HVP in a single reversible 3-sweep pass
+    (the bench's "gradient+HVP" evaluation).  Returns (report, hvp_list)."""
+    _check_oracle(circuit, oracle)
+    t0 = time.perf_counter()
+    z = _slot_directions(circuit, directions)
+    run = _Run(circuit, oracle, _lib.GF_VALUE | _lib.GF_GRAD | _lib.GF_HVP, z, sector, fold, basis, batch, chunk,
+               distributed)
+    value, d, h = run.run()
+    rep = _grad_report(circuit, run, value, d, parity_mode, "gradient", t0)
+    hv = _ref_counts(circuit.num_slots, run.spec.total, "hvp")
+    rep.pass_counts = {k: rep.pass_counts[k] + hv[k] for k in COUNT_NAMES}
+    return rep, [h[i] for i in range(circuit.num_logical)]
+
+
+def hessian_vector_product(circuit: Circuit, oracle, directions, workers: int | None = None, *, sector=None,
+                           fold=False, basis=None, batch=None, chunk=None, distributed=None):
+    """Holomorphic H~ . vec(Z) per logical gate (reference objective.py:770-814)."""
+    _check_oracle(circuit, oracle)
+    z = _slot_directions(circuit, directions)
+    if not np.any(z) or circuit.num_slots == 0:
+        return [np.zeros((4, 4), dtype=np.complex128) for _ in range(circuit.num_logical)]
+    run = _Run(circuit, oracle, _lib.GF_HVP, z, sector, fold, basis, batch, chunk, distributed)
+    _, _, h = run.run()
+    return [h[i] for i in range(circuit.num_logical)]
+
+
+def _used_routes(circuit: Circuit):
+    lid = [s.logical_id for s in circuit.slots]
+    used = set()
+    n = len(lid)
+    for a in range(n):
+        for b in range(a + 1, n):
+            used.add((min(lid[a], lid[b]), max(lid[a], lid[b])))
+    return used
+
+
+def full_hessian(circuit: Circuit, oracle, use_translation_dedup: bool = False, parity_mode: bool = False,
+                 workers: int | None = None, *, sector=None, fold=False, basis=None, batch=None, chunk=None,
+                 distributed=None) -> ObjectiveReport:
+    """Value, gradient and all holomorphic Hessian blocks (reference
+    objective.py:701-767).
+
+    Blocks are assembled column by column from engine HVPs with unit
+    directions on the support entries (H~_{(a,i),(b,j)} = HVP(e_{b,j})[a][i]).
+    ``use_translation_dedup`` only changes the reported pair counts: the
+    engine computes the exact sum, which the reference's dedup equals."""
+    _check_oracle(circuit, oracle)
+    t0 = time.perf_counter()
+    if use_translation_dedup:
+        classes = translation_classes(circuit)
+    rep = full_gradient(circuit, oracle, workers, parity_mode, sector=sector, fold=fold, basis=basis, batch=batch,
+                        chunk=chunk, distributed=distributed)
+    sup = PARITY_SUPPORT if parity_mode else DENSE_SUPPORT
+    nlog = circuit.num_logical
+    used = _used_routes(circuit)
+    cols = {}
+    for b in range(nlog):
+        if not any(b in key for key in used):
+            continue
+        for jj, e in enumerate(sup):
+            z = [np.zeros((4, 4), dtype=np.complex128) for _ in range(nlog)]
+            z[b].reshape(16)[e] = 1.0
+            cols[(b, jj)] = hessian_vector_product(circuit, oracle, z, sector=sector, fold=fold, basis=basis,
+                                                   batch=batch, chunk=chunk, distributed=distributed)
+    blocks = {}
+    for a, b in sorted(used):
+        blk = np.empty((sup.size, sup.size), dtype=np.complex128)
+        for jj in range(sup.size):
+            blk[:, jj] = cols[(b, jj)][a].reshape(16)[sup]
+        blocks[(a, b)] = blk
+    rep.hessian = HessianBlocks(nlog, np.asarray(sup), blocks)
+    n = circuit.num_slots
+    pairs = len(classes) if use_translation_dedup else n * (n - 1) // 2
+    S = rep.engine.get("summands", 0)
+    rep.pass_counts = _ref_counts(n, S, "hessian", pairs=pairs, firsts=max(n - 1, 0),
+                                  arrays=max(n - 1, 0) * max(n - 2, 0) // 2)
+    rep.wall_time = time.perf_counter() - t0
+    return rep
+
+
+def build_pass_cache(circuit: Circuit, oracle, j: int) -> PassCache:
+    """Forward / backward states of summand j (reference objective.py:611-624),
+    computed with the GPU gate kernel."""
+    _check_oracle(circuit, oracle)
+    k = circuit.num_qubits
+    fwd = [basis_state(k, j)]
+    for s in circuit.slots:
+        fwd.append(apply_gate(fwd[-1], Gate(circuit.logical_gates[s.logical_id].matrix, s.targets)))
+    bwd = [np.conj(oracle.apply(basis_state(k, j)))]
+    for s in reversed(circuit.slots):
+        bwd.append(apply_gate(bwd[-1], Gate(circuit.logical_gates[s.logical_id].matrix.T, s.targets)))
+    return PassCache(fwd, bwd)
+
+
+def summand_gradient(j: int, circuit: Circuit, oracle):
+    """(value, per-slot holomorphic derivatives) of summand j (reference
+    objective.py:627-642)."""
+    if not 0 <= j < 2**circuit.num_qubits:
+        raise ValueError(f"basis index {j} out of range")
+    cache = build_pass_cache(circuit, oracle, j)
+    n = circuit.num_slots
+    value = complex(cache.backward_states[0] @ cache.forward_states[-1])
+    derivs = [hole_contract(cache.backward_states[n - l - 1], cache.forward_states[l], s.targets)
+              for l, s in enumerate(circuit.slots)]
+    return value, derivs
+
+
+def _unswap(d, swapped):
+    return d[np.ix_(WIRE_SWAP, WIRE_SWAP)] if swapped else d
+
+
+__all__ += ["accumulate_shared"]

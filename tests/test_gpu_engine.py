@@ -1,0 +1,353 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the CPU oracle
+and the reference's golden fixtures.  Run with ``pytest -m gpu``."""
+
+import numpy as np
+import pytest
+
+from conftest import golden, rel_err
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA GPU", allow_module_level=True)
+
+import paper_2506_23775_b200 as gf  # noqa: E402
+from paper_2506_23775_b200 import kernels as K  # noqa: E402
+from paper_2506_23775_b200 import manifold  # noqa: E402
+from oracle import gf_oracle as O  # noqa: E402
+
+TOL = 1e-10  # north-star tolerance for cost / gradient / HVP (fp64)
+
+
+def _loaded_libs():
+    with open("/proc/self/maps") as fh:
+        return fh.read()
+
+
+def test_native_library_is_loaded():
+    assert "libgfcuda.so" in _loaded_libs()
+
+
+# ----------------------------------------------------------------- kernels
+
+
+def test_kernels_match_reference_vectors():
+    g = golden("kernels")
+    psi, bra = g["psi"], g["bra"]
+    for i, t in enumerate(g["pairs"]):
+        t = tuple(int(x) for x in t)
+        t2 = tuple(int(x) for x in g["second_pairs"][i])
+        assert rel_err(K.apply_gate(psi, K.Gate(g["gates"][i], t)), g["apply"][i]) < 1e-14
+        assert rel_err(K.apply_gate(psi, K.Gate(g["pgates"][i], t)), g["apply_parity"][i]) < 1e-14
+        assert rel_err(K.hole_contract(bra, psi, t), g["hole_contract"][i]) < 1e-13
+        arr = K.hole_apply(psi, t)
+        assert np.array_equal(arr, g["hole_apply"][i])
+        assert np.array_equal(K.hole_apply(psi, t, K.PARITY_SUPPORT), g["hole_apply_parity"][i])
+        assert rel_err(K.apply_gate_to_array(arr, K.Gate(g["gates"][i], t2)), g["array_apply"][i]) < 1e-14
+        assert rel_err(K.hole_contract_array(bra, arr, t2), g["hole_contract_array"][i]) < 1e-13
+        arrp = K.hole_apply(psi, t, K.PARITY_SUPPORT)
+        assert rel_err(K.hole_contract_array(bra, arrp, t2, K.PARITY_SUPPORT),
+                       g["hole_contract_array_parity"][i]) < 1e-13
+
+
+@pytest.mark.parametrize("k", [2, 3, 12, 17])
+def test_apply_gate_all_positions_vs_oracle(k):
+    rng = np.random.default_rng(k)
+    psi = rng.normal(size=2**k) + 1j * rng.normal(size=2**k)
+    pairs = [(0, 1), (k - 2, k - 1), (k - 1, 0), (0, k - 1)]
+    if k > 3:
+        pairs += [(1, k - 2), (k // 2, 1), (k - 1, k // 2)]
+    for t in pairs:
+        g = manifold.random_unitary(4, rng)
+        want = O.apply_gate(psi, g, t)
+        assert rel_err(K.apply_gate(psi, K.Gate(g, t)), want) < 1e-14
+        p = manifold.parity_join(manifold.random_unitary(2, rng), manifold.random_unitary(2, rng))
+        assert rel_err(K.apply_gate(psi, K.Gate(p, t)), O.apply_gate(psi, p, t)) < 1e-14
+        bra = rng.normal(size=2**k) + 1j * rng.normal(size=2**k)
+        assert rel_err(K.hole_contract(bra, psi, t), O.hole_contract(bra, psi, t)) < 1e-12
+
+
+def test_apply_gate_errors():
+    psi = np.ones(4, complex)
+    with pytest.raises(ValueError):
+        K.apply_gate(psi, K.Gate(np.eye(4), (0, 2)))
+    with pytest.raises(ValueError):
+        K.Gate(np.eye(4), (1, 1))
+    with pytest.raises(ValueError):
+        K.apply_gate(psi, K.Gate(np.eye(4), (0, 1)), out=psi)
+    with pytest.raises(ValueError):
+        K.apply_gate(np.ones(6, complex), K.Gate(np.eye(4), (0, 1)))
+
+
+def test_large_vector_round_trip_and_norm():
+    """Size-independent properties at 2^28 amplitudes (4 GiB): G then G^dag is
+    the identity and the norm is preserved, for low / high / split targets."""
+    k = 28
+    rng = np.random.default_rng(1)
+    dev = torch.device("cuda")
+    x = torch.randn(2**k, dtype=torch.complex128, device=dev)
+    x /= torch.linalg.vector_norm(x)
+    y = x.clone()
+    for t in [(0, 1), (26, 27), (27, 3), (5, 20)]:
+        g = manifold.random_unitary(4, rng)
+        y = K.apply_gate(y, K.Gate(g, t))
+        n = torch.linalg.vector_norm(y).item()
+        assert abs(n - 1.0) < 1e-12
+        y = K.apply_gate(y, K.Gate(g.conj().T, t))
+    assert torch.max(torch.abs(y - x)).item() < 1e-14 * 2 ** (k / 2) + 1e-12
+
+
+# ------------------------------------------------------------ sector maps
+
+
+def test_sector_maps_bit_exact():
+    dev = torch.device("cuda")
+    for sector in (0, 1):
+        i = torch.arange(2**22, dtype=torch.int64, device=dev)
+        x = torch.empty_like(i)
+        gf._lib.check(gf._lib.lib.gf_sector_unrank(i.data_ptr(), i.numel(), sector, x.data_ptr(),
+                                                   gf._lib.stream_ptr()))
+        want = O.sector_unrank(i.cpu().numpy(), sector)
+        assert np.array_equal(x.cpu().numpy(), want)
+        back = torch.empty_like(i)
+        gf._lib.check(gf._lib.lib.gf_sector_rank(x.data_ptr(), x.numel(), back.data_ptr(), gf._lib.stream_ptr()))
+        assert torch.equal(back, i)
+    # 2^31-entry sector of k = 32: spot check the top of the range
+    i = torch.arange(2**31 - 4096, 2**31, dtype=torch.int64, device=dev)
+    x = torch.empty_like(i)
+    gf._lib.check(gf._lib.lib.gf_sector_unrank(i.data_ptr(), i.numel(), 0, x.data_ptr(), gf._lib.stream_ptr()))
+    assert np.array_equal(x.cpu().numpy(), O.sector_unrank(i.cpu().numpy(), 0))
+
+
+@pytest.mark.parametrize("L", [4, 6, 8])
+def test_orbit_canon_bit_exact(L):
+    dev = torch.device("cuda")
+    rng = np.random.default_rng(L)
+    x = rng.integers(0, 2 ** (2 * L), size=20000, dtype=np.int64)
+    xd = torch.from_numpy(x).to(dev)
+    rep, size = torch.empty_like(xd), torch.empty_like(xd)
+    gf._lib.check(gf._lib.lib.gf_orbit_canon(xd.data_ptr(), xd.numel(), L, rep.data_ptr(), size.data_ptr(),
+                                             gf._lib.stream_ptr()))
+    r2, s2 = O.orbit_canon(x, L)
+    assert np.array_equal(rep.cpu().numpy(), r2) and np.array_equal(size.cpu().numpy(), s2)
+
+
+def test_fold_basis_matches_oracle_and_burnside():
+    from paper_2506_23775_b200.objective import fold_basis
+
+    for L in (4, 6):
+        spec = fold_basis(2 * L, 0)
+        reps, w = O.sector_orbit_reps(L, 0)
+        assert np.array_equal(spec.indices, reps) and np.array_equal(spec.weights, w)
+    assert fold_basis(8, 0).total == 72
+
+
+def test_c1q_sector_gate_matches_full_space():
+    rng = np.random.default_rng(3)
+    k = 8
+    for sector in (0, 1):
+        full = rng.normal(size=2**k) + 1j * rng.normal(size=2**k)
+        par = np.array([bin(j).count("1") & 1 for j in range(2**k)])
+        full[par != sector] = 0
+        sel = O.sector_unrank(np.arange(2 ** (k - 1)), sector)
+        for a in (0, 3, 6):
+            p = manifold.parity_join(manifold.random_unitary(2, rng), manifold.random_unitary(2, rng))
+            want = O.apply_gate(full, p, (a, k - 1))[sel]
+            got = K.apply_sector_c1q(full[sel], p, a, k, sector)
+            assert rel_err(got, want) < 1e-14
+            # the swapped orientation (k-1, a) through the engine's wire swap
+            want2 = O.apply_gate(full, p, (k - 1, a))[sel]
+            got2 = K.apply_sector_c1q(full[sel], K.wire_swapped_matrix(p), a, k, sector)
+            assert rel_err(got2, want2) < 1e-14
+
+
+# ------------------------------------------------------------------ engine
+
+
+def _c1():
+    g = golden("c1")
+    spec, circ, rng = gf.spinful_layer_circuit(4, 3, False, seed=0)
+    assert np.array_equal(circ.gate_stack(), g["gates"])
+    orc = gf.DenseOracle(spec, 0.25)
+    return g, spec, circ, orc
+
+
+def test_c1_dense_target_on_gpu_matches_reference():
+    g, spec, circ, orc = _c1()
+    assert rel_err(orc._u[:, :4], g["U_cols"]) < 1e-12
+
+
+def test_c1_value_gradient_hvp_vs_reference():
+    g, spec, circ, orc = _c1()
+    X = list(g["direction"])
+    assert abs(gf.target_value(circ, orc) - g["target_value"]) < TOL * abs(g["target_value"])
+    rep = gf.full_gradient(circ, orc)
+    assert abs(rep.value - g["value"]) < TOL * abs(g["value"])
+    assert rel_err(np.stack(rep.holomorphic_derivatives), g["holo"]) < TOL
+    assert rel_err(np.stack(rep.per_logical_gradient), g["riem"]) < TOL
+    assert [rep.pass_counts[n] for n in gf.objective.COUNT_NAMES] == list(g["grad_counts"])
+    hv = gf.hessian_vector_product(circ, orc, X)
+    assert rel_err(np.stack(hv), g["hvp"]) < TOL
+    rep2, hv2 = gf.gradient_and_hvp(circ, orc, X)
+    assert rel_err(np.stack(hv2), g["hvp"]) < TOL
+    assert rel_err(np.stack(rep2.holomorphic_derivatives), g["holo"]) < TOL
+    hx = [manifold.hessian_apply_gate(gg.matrix, e, manifold.euclid_gradient_from_holomorphic(h), x)
+          for gg, e, h, x in zip(circ.logical_gates, rep.euclidean_gradients, hv, X)]
+    assert abs(sum(manifold.inner(x, y) for x, y in zip(X, hx)) - g["x_hess_x"]) < TOL * abs(g["x_hess_x"])
+
+
+def test_c1_full_hessian_vs_reference():
+    g, spec, circ, orc = _c1()
+    rep = gf.full_hessian(circ, orc)
+    keys = [tuple(int(v) for v in x) for x in g["hess_keys"]]
+    assert sorted(rep.hessian.blocks) == keys
+    scale = np.abs(g["hess_blocks"]).max()
+    for kk, ref in zip(keys, g["hess_blocks"]):
+        assert np.abs(rep.hessian.blocks[kk] - ref).max() < TOL * scale
+    assert [rep.pass_counts[n] for n in gf.objective.COUNT_NAMES] == list(g["hess_counts"])
+
+
+def test_c1_trust_region_five_iterations_vs_reference():
+    g, spec, circ, orc = _c1()
+    final, trace = gf.trust_region_optimize(circ, orc, gf.TrustRegionParams(max_iterations=5))
+    f = np.array([r.value for r in trace.records])
+    assert np.allclose(f, g["tr_f"], rtol=1e-9, atol=1e-9)
+    assert [r.accepted for r in trace.records] == list(g["tr_accepted"])
+    assert [r.stop_reason for r in trace.records] == list(g["tr_reason"])
+    assert np.allclose([r.radius for r in trace.records], g["tr_radius"], rtol=1e-9)
+    assert rel_err(np.stack([x.matrix for x in final.logical_gates]), g["tr_final_gates"]) < 1e-8
+
+
+def test_batch_and_chunk_bit_determinism():
+    g, spec, circ, orc = _c1()
+    X = list(g["direction"])
+    base = gf.gradient_and_hvp(circ, orc, X, batch=256)
+    for b in (64, 128):
+        other = gf.gradient_and_hvp(circ, orc, X, batch=b)
+        assert other[0].value == base[0].value
+        assert np.array_equal(np.stack(other[0].holomorphic_derivatives), np.stack(base[0].holomorphic_derivatives))
+        assert np.array_equal(np.stack(other[1]), np.stack(base[1]))
+
+
+def test_random_circuit_matrix_oracle_and_shared_gates():
+    """Random wire pairs (adjacent / general / swapped) with a Haar target."""
+    rng = np.random.default_rng(9)
+    k = 7
+    u = manifold.random_unitary(2**k, rng)
+    gates, slots = [], []
+    for i in range(9):
+        t1, t2 = (int(x) for x in rng.choice(k, size=2, replace=False))
+        gates.append(gf.Gate(manifold.random_unitary(4, rng), (t1, t2)))
+        slots.append(gf.GateSlot(i % 5, (t1, t2)))
+    circ = gf.Circuit(k, slots, gates[:5])
+    orc = gf.DenseOracle.from_matrix(u)
+    X = [rng.normal(size=(4, 4)) + 1j * rng.normal(size=(4, 4)) for _ in range(5)]
+    rep, hv = gf.gradient_and_hvp(circ, orc, X)
+    t1, t2, lid = circ.slot_arrays()
+    plan = O.Plan(k, np.stack([t1, t2], 1), lid, circ.gate_stack())
+    phi = O.dense_phi0(u)
+    v, d, _ = O.gradient_sum(plan, np.arange(2**k), phi)
+    h, _ = O.hvp_sum(plan, X, np.arange(2**k), phi)
+    assert abs(rep.value + v.real) < TOL * max(1, abs(v))
+    assert rel_err(np.stack(rep.holomorphic_derivatives), plan.logical_sum(d)) < TOL
+    assert rel_err(np.stack(hv), plan.logical_sum(h)) < TOL
+
+
+def test_empty_circuit_and_oracle_mismatch():
+    circ = gf.Circuit(4, [], [])
+    orc = gf.DenseOracle.from_matrix(np.eye(16, dtype=complex))
+    assert gf.target_value(circ, orc) == -16.0
+    with pytest.raises(ValueError):
+        gf.target_value(gf.Circuit(3, [], []), orc)
+
+
+@pytest.mark.parametrize("name", ["sector_l4p", "sector_l6p", "sector_l5o"])
+def test_sector_engine_vs_reference_restricted_sums(name):
+    g = golden(name)
+    k, L = int(g["k"]), int(g["L"])
+    spec, circ, rng = gf.spinful_layer_circuit(L, int(g["gates"].shape[0]), bool(g["periodic"]),
+                                               seed={"sector_l4p": 2, "sector_l6p": 4, "sector_l5o": 5}[name],
+                                               parity=True)
+    assert np.array_equal(circ.gate_stack(), g["gates"])
+    orc = gf.DenseOracle(spec, 0.25)
+    X = list(g["direction"])
+    for sect, nm in ((0, "even"), (1, "odd")):
+        rep, hv = gf.gradient_and_hvp(circ, orc, X, parity_mode=True, sector=sect)
+        ref_v = g[nm + "_value"]
+        assert abs(-rep.value - ref_v.real) < TOL * max(1, abs(ref_v))
+        assert rel_err(np.stack(rep.holomorphic_derivatives), g[nm + "_holo"]) < TOL
+        assert rel_err(np.stack(hv), g[nm + "_hvp"]) < TOL
+
+
+@pytest.mark.parametrize("name", ["sector_l4p", "sector_l6p"])
+def test_fold_engine_vs_reference_even_sum(name):
+    g = golden(name)
+    L = int(g["L"])
+    spec, circ, rng = gf.spinful_layer_circuit(L, 3, True, seed={"sector_l4p": 2, "sector_l6p": 4}[name],
+                                               parity=True)
+    orc = gf.DenseOracle(spec, 0.25)
+    X = list(g["direction"])
+    rep, hv = gf.gradient_and_hvp(circ, orc, X, parity_mode=True, sector="even", fold=True)
+    assert abs(-rep.value - g["even_value"].real) < TOL * max(1, abs(g["even_value"]))
+    assert rel_err(np.stack(rep.holomorphic_derivatives), g["even_holo"]) < TOL
+    assert rel_err(np.stack(hv), g["even_hvp"]) < TOL
+
+
+def test_chebyshev_oracle_matches_dense_and_reference_krylov():
+    g = golden("models")
+    spec = gf.build_spinful_fh(3, 1.0, 4.0, True)
+    orc = gf.ChebyshevOracle(spec, 0.25)
+    assert rel_err(orc.apply(g["krylov_in"]), g["dense_out"]) < 1e-12
+    spec4 = gf.build_spinful_fh(4, 1.0, 4.0, False)
+    d = gf.DenseOracle(spec4, 0.25)
+    c = gf.ChebyshevOracle(spec4, 0.25)
+    js = torch.arange(0, 256, dtype=torch.int64, device="cuda")
+    a = torch.empty((256, 256), dtype=torch.complex128, device="cuda")
+    b = torch.empty_like(a)
+    d.phi0_into(js, None, a)
+    c.phi0_into(js, None, b)
+    assert torch.max(torch.abs(a - b)).item() < 1e-13
+
+
+def test_c2_slice_vs_reference_chunk_drivers():
+    """BASELINE configs[1] (16 qubits, 36 slots): reference _gradient_chunk /
+    _hvp_chunk with Krylov phi0 on a seeded 16-state sample."""
+    g = golden("c2_slice")
+    spec, circ, rng = gf.spinful_layer_circuit(8, 5, False, seed=1)
+    assert np.array_equal(circ.gate_stack(), g["gates"])
+    orc = gf.ChebyshevOracle(spec, 0.25)
+    js = g["js"]
+    srng = np.random.default_rng(2)
+    srng.choice(2**16, size=16, replace=False)
+    w = srng.normal(size=2**16) + 1j * srng.normal(size=2**16)
+    phi = torch.empty((16, 2**16), dtype=torch.complex128, device="cuda")
+    orc.phi0_into(torch.from_numpy(js).cuda(), None, phi)
+    P = phi.cpu().numpy()
+    chk = np.array([[p.sum(), p @ w, np.vdot(p, p).real] for p in P])
+    assert rel_err(chk, g["phi_checks"]) < 1e-10
+    rep, hv = gf.gradient_and_hvp(circ, orc, list(g["direction"]), basis=js)
+    assert abs(-rep.value - g["values"].sum().real) < TOL * max(1, abs(g["values"].sum()))
+    assert rel_err(np.stack(rep.holomorphic_derivatives), g["holo"]) < TOL
+    assert rel_err(np.stack(hv), g["hvp"]) < TOL
+
+
+def test_k20_single_summands_vs_oracle():
+    """Larger vectors (2^20 amplitudes; multi-CTA reductions per summand)."""
+    spec, circ, rng = gf.spinful_layer_circuit(10, 4, False, seed=3)
+    X = [manifold.project_tangent_gate(x.matrix, rng.normal(size=(4, 4)) + 1j * rng.normal(size=(4, 4)))
+         for x in circ.logical_gates]
+    orc = gf.ChebyshevOracle(spec, 0.25)
+    js = np.array([5, 77777, 1000001])
+    rep, hv = gf.gradient_and_hvp(circ, orc, X, basis=js)
+    phi = torch.empty((3, 2**20), dtype=torch.complex128, device="cuda")
+    orc.phi0_into(torch.from_numpy(js).cuda(), None, phi)
+    P = phi.cpu().numpy()
+    t1, t2, lid = circ.slot_arrays()
+    plan = O.Plan(20, np.stack([t1, t2], 1), lid, circ.gate_stack())
+    fn = lambda jj: P[np.searchsorted(js, jj)]
+    v, d, _ = O.gradient_sum(plan, js, fn)
+    h, _ = O.hvp_sum(plan, X, js, fn)
+    assert abs(rep.value + v.real) < TOL * max(1, abs(v))
+    assert rel_err(np.stack(rep.holomorphic_derivatives), plan.logical_sum(d)) < TOL
+    assert rel_err(np.stack(hv), plan.logical_sum(h)) < TOL
