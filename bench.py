@@ -1,0 +1,457 @@
+#!/usr/bin/env python
+"""Benchmark: full-basis-sum value + gradient + HVP evaluations of BASELINE.json
+configs[1] (L=8 spinful Fermi-Hubbard, 16 qubits, 5 layers / 36 slots, Haar
+gates seed 1, target exp(-iHt) with J=1, U=4, t=0.25).
+
+One step = one evaluation of f, its Riemannian gradient and one Hessian-vector
+product summed over all 2^16 basis states (the reference's full_gradient +
+hessian_vector_product, objective.py:659-698 / 770-814), fused into one
+reversible 3-sweep pass per summand.  With N GPUs (torchrun) the fixed basis
+sum is sharded over ranks in contiguous chunks (strong scaling); the only
+collective is the all-gather of per-chunk records.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Prints one JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "gradient+HVP evals/sec at 16-site Hubbard; gate-apply HBM GB/s vs peak"
+UNIT = "evals/s"
+L_SITES, LAYERS, SEED, T_EVOL = 8, 5, 1, 0.25
+K_QUBITS = 2 * L_SITES
+TOTAL = 1 << K_QUBITS
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def workload():
+    import paper_2506_23775_b200 as gf
+
+    spec, circ, rng = gf.spinful_layer_circuit(L_SITES, LAYERS, False, seed=SEED)
+    X = [gf.manifold.project_tangent_gate(g.matrix, rng.normal(size=(4, 4)) + 1j * rng.normal(size=(4, 4)))
+         for g in circ.logical_gates]
+    return gf, spec, circ, X
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (recipe's clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        self.f.seek(0)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.f.name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _dist():
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return rank, world, local, (dist if world > 1 else None)
+
+
+def _max_over_ranks(x, dist):
+    import torch
+
+    if dist is None:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _sum_over_ranks(x, dist):
+    import torch
+
+    if dist is None:
+        return x
+    t = torch.tensor([float(x)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def gate_apply_sweep(gf, peak):
+    """Standalone K1 bandwidth sweep on one 2^31-amplitude complex128 vector
+    (the c5 compressed 31-qubit space, 32 GiB): 2q adjacent (t, t+1), 2q long
+    range (t, t+15 mod 31), and the parity-controlled 1q gate of the implicit
+    qubit; in place, 32 B per amplitude per application."""
+    import torch
+
+    K = 31
+    N = 1 << K
+    try:
+        x = torch.empty(N, dtype=torch.complex128, device="cuda")
+    except RuntimeError:
+        K, N = 30, 1 << 30
+        x = torch.empty(N, dtype=torch.complex128, device="cuda")
+    x.real.normal_()
+    x.imag.normal_()
+    rng = np.random.default_rng(0)
+    st = gf._lib.stream_ptr()
+    cases = [("adj", t, t + 1) for t in range(K - 1)] + [("long", t, (t + 15) % K) for t in range(0, K, 3)]
+    cases += [("c1q", a, None) for a in (0, 10, 20, 29)]
+    results = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for kind, a, b in cases:
+        g = gf.manifold.random_unitary(4, rng)
+        if kind == "c1q":
+            g = gf.manifold.parity_join(gf.manifold.random_unitary(2, rng), gf.manifold.random_unitary(2, rng))
+        g = np.ascontiguousarray(g)
+
+        def launch():
+            if kind == "c1q":
+                gf._lib.check(gf._lib.lib.gf_apply_gate_sector_c1q(x.data_ptr(), x.data_ptr(), K + 1, a, 0,
+                                                                   g.ctypes.data, 1, st))
+            else:
+                gf._lib.check(gf._lib.lib.gf_apply_gate(x.data_ptr(), x.data_ptr(), K, a, b, g.ctypes.data, 0, 1,
+                                                        st))
+
+        launch()
+        torch.cuda.synchronize()
+        e0.record()
+        reps = 3
+        for _ in range(reps):
+            launch()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        gbs = 32.0 * N / (ms * 1e-3) / 1e9
+        results.append((kind, a, b, ms, gbs))
+    del x
+    torch.cuda.empty_cache()
+    g_all = np.array([r[4] for r in results])
+    worst = min(results, key=lambda r: r[4])
+    return {
+        "vector_amplitudes": N,
+        "bytes_per_application": 32 * N,
+        "launches": len(results) * 4,
+        "gbs_median": round(float(np.median(g_all)), 1),
+        "gbs_min": round(float(g_all.min()), 1),
+        "gbs_max": round(float(g_all.max()), 1),
+        "frac_of_measured_peak_median": round(float(np.median(g_all)) / peak, 4),
+        "frac_of_8TBs_nominal_median": round(float(np.median(g_all)) / 8000.0, 4),
+        "worst_case": f"{worst[0]} ({worst[1]},{worst[2]}) {worst[4]:.0f} GB/s",
+        "per_case_gbs": {f"{r[0]}:{r[1]}-{r[2]}": round(r[4], 1) for r in results},
+    }
+
+
+def cpu_port_rate(circ, X, phi_host, js, workers, with_oracle_terms=None):
+    """Oracle port (oracle/gf_oracle.c, restating the reference drivers) on
+    the host: gradient + HVP per summand, summands spread over `workers`
+    threads.  Returns summands per second."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import gf_oracle as O
+
+    t1, t2, lid = circ.slot_arrays()
+    plan = O.Plan(circ.num_qubits, np.stack([t1, t2], 1), lid, circ.gate_stack())
+    parts = np.array_split(np.arange(len(js)), workers)
+
+    def work(sel):
+        if len(sel) == 0:
+            return 0
+        jj = js[sel]
+        if with_oracle_terms is not None:
+            P = O.lanczos_phi0(circ.num_qubits, with_oracle_terms, T_EVOL)(jj)
+        else:
+            P = phi_host[sel]
+        fn = lambda q: P[np.searchsorted(jj, q)]
+        O.gradient_sum(plan, jj, fn)
+        O.hvp_sum(plan, X, jj, fn)
+        return len(sel)
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=workers) as ex:
+        n = sum(ex.map(work, parts))
+    return n / (time.perf_counter() - t0)
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm's CPU implementation (the
+    oracle port; the reference itself is numba and cannot travel), including
+    its own target oracle (Lanczos, models.py:322-384) per summand, on all host
+    threads; bounded samples of the same c2 workload."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import gf_oracle as O
+
+    gf, spec, circ, X = workload()
+    terms, _ = O.spinful_terms(L_SITES, 1.0, 4.0, False)
+    cores = os.cpu_count() or 1
+    rng = np.random.default_rng(7)
+    sample = max(cores, 16)
+    rates = []
+    for step in range(args.warmup + args.steps):
+        js = np.sort(rng.choice(TOTAL, size=sample, replace=False))
+        r = cpu_port_rate(circ, X, None, js, cores, with_oracle_terms=terms)
+        if step >= args.warmup:
+            rates.append(r)
+    summ_rate = float(np.mean(rates))
+    v = summ_rate / TOTAL
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 / v, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "c128", "data": "synthetic (BASELINE configs[1] recipe)",
+        "config": {"workload": "c2 full 2^16 basis sum, value+gradient+HVP (extrapolated from per-step samples)",
+                   "summands_per_step_sample": sample},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{sample} random c2 summands per step: Lanczos phi0 + gradient + HVP "
+                                   f"(oracle/gf_oracle.c restating reference objective.py:291-482), "
+                                   f"extrapolated x{TOTAL}/{sample}"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_b200(args):
+    import torch
+
+    rank, world, local, dist = _dist()
+    gf, spec, circ, X = workload()
+    from paper_2506_23775_b200 import objective as obj
+
+    peak, peak_src = _peaks()
+    chunk = obj.CHUNK_STATES
+    N = TOTAL
+    nchunks = TOTAL // chunk
+    lo, hi = obj.shard_chunks(nchunks, rank, world)
+    p0, p1 = lo * chunk, hi * chunk
+    batch = args.batch or obj._default_batch(N, TOTAL)
+    oracle = gf.ChebyshevOracle(spec, T_EVOL)
+    t_or = time.perf_counter()
+    cache = gf.models.CachedTargetColumns(oracle, K_QUBITS, p0, p1, batch=batch)
+    torch.cuda.synchronize()
+    oracle_setup_s = time.perf_counter() - t_or
+    kw = dict(batch=batch, distributed=(dist is not None))
+    if args.summands:
+        kw["basis"] = np.arange(min(args.summands, TOTAL), dtype=np.int64)
+    for _ in range(args.warmup):
+        rep, hv = gf.gradient_and_hvp(circ, cache, X, **kw)
+    torch.cuda.synchronize()
+    plan = next(iter(obj._PLANS.values()))
+    gf._lib.check(gf._lib.lib.gf_plan_set_profiling(plan.h, 1))
+
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clk = Clocks(local)
+    clk.start()
+    launches = 0
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.steps):
+        rep, hv = gf.gradient_and_hvp(circ, cache, X, **kw)
+        launches += rep.engine["launches"]
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1)
+    ms_max = _max_over_ranks(ms, dist)
+    launches_all = int(_sum_over_ranks(launches, dist))
+    value = args.steps / (ms_max * 1e-3)
+
+    ms4 = np.zeros(4)
+    l4 = np.zeros(4, dtype=np.int64)
+    gf._lib.check(gf._lib.lib.gf_plan_phase_times(plan.h, ms4.ctypes.data, l4.ctypes.data))
+    gf._lib.check(gf._lib.lib.gf_plan_set_profiling(plan.h, 0))
+    n = circ.num_slots
+    my_summands = (p1 - p0) * args.steps
+    # algorithmic bytes: forward 32 B, reverse (psi, bra, chi) 96 B,
+    # ascending (psi, bra, v) 96 B per amplitude per slot
+    bytes_phase = {"forward": 32.0 * N * n * my_summands, "reverse": 96.0 * N * n * my_summands,
+                   "ascending": 96.0 * N * n * my_summands}
+    phases = {}
+    for i, nm in enumerate(("forward", "reverse", "ascending", "reduce")):
+        phases[nm] = {"ms": round(float(ms4[i]), 3), "launches": int(l4[i]),
+                      "share": round(float(ms4[i] / ms4.sum()), 4) if ms4.sum() else None}
+        if nm in bytes_phase and ms4[i] > 0:
+            phases[nm]["achieved_gbs"] = round(bytes_phase[nm] / (ms4[i] * 1e-3) / 1e9, 1)
+    dom = max(("forward", "reverse", "ascending"), key=lambda k: ms4[("forward", "reverse", "ascending").index(k)])
+    achieved = phases[dom]["achieved_gbs"]
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(dom)
+        except Exception:
+            traffic = None
+
+    # e2e: the public API call a user makes, target columns regenerated on
+    # the device by the matrix-free oracle for every summand of every
+    # evaluation (as the reference's _phi_block does, objective.py:561-565);
+    # host inputs: gate matrices + directions (+ nothing else); host output:
+    # the reduced records.
+    e2e_steps = max(1, args.steps if args.e2e_steps is None else args.e2e_steps)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        gates_host = np.ascontiguousarray(circ.gate_stack())
+        dirs_host = np.ascontiguousarray(np.stack(X))
+        rep_e, hv_e = gf.gradient_and_hvp(circ.with_gates(list(gates_host)), oracle, list(dirs_host), **kw)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = _max_over_ranks(e0.elapsed_time(e1), dist)
+    e2e_val = e2e_steps / (e2e_ms * 1e-3)
+    rec_bytes = (2 + 64 * circ.num_logical) * 8 * nchunks
+    h2d = gates_host.nbytes + dirs_host.nbytes
+    # consistency: same objective from both paths
+    assert abs(rep_e.value - rep.value) <= 1e-10 * max(1.0, abs(rep.value)), (rep_e.value, rep.value)
+
+    gate_sweep = None
+    cpu = None
+    if rank == 0 and world == 1:
+        if not args.no_sweep:
+            gate_sweep = gate_apply_sweep(gf, peak)
+        if not args.no_cpu:
+            cores = os.cpu_count() or 1
+            srng = np.random.default_rng(11)
+            sample = max(cores, 64)
+            js = np.sort(srng.choice(TOTAL, size=sample, replace=False))
+            phi = torch.empty((sample, N), dtype=torch.complex128, device="cuda")
+            oracle.phi0_into(torch.from_numpy(js).cuda(), None, phi)
+            ph = phi.cpu().numpy()
+            del phi
+            r = cpu_port_rate(circ, X, ph, js, cores)
+            cpu = {"value": r / TOTAL, "unit": UNIT, "cores": cores, "kind": "port",
+                   "sample": f"{sample} random c2 summands, gradient + HVP per summand (oracle/gf_oracle.c, "
+                             f"restating reference objective.py:322-337, 432-482) on {cores} threads, phi0 "
+                             f"precomputed; extrapolated to the full 2^16 sum"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": value,
+            "unit": UNIT,
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "c128",
+            "data": "synthetic: BASELINE configs[1] circuit (spinful FH L=8 open, 5 layers, Haar seed 1); target "
+                    "columns conj(exp(-iHt)|j>) (J=1, U=4, t=0.25) computed on device by the Chebyshev oracle",
+            "config": {
+                "workload": "c2: L=8 spinful Fermi-Hubbard, 16 qubits, 36 slots / 5 logical gates; one step = value"
+                            " + Riemannian gradient + one HVP summed over all 65536 basis states",
+                "summands": TOTAL, "batch": batch, "chunk": chunk, "parallelism": f"basis-sum dp{world}",
+                "l2": "inputs larger than L2 (phi0 cache %d MiB per GPU; workspace 3 x batch x 1 MiB)" %
+                      ((p1 - p0) * N * 16 >> 20),
+                "oracle_setup_s": round(oracle_setup_s, 3),
+            },
+            "roofline": {"bound": "hbm", "kernel": f"k_sweep ({dom} sweep)", "achieved": achieved, "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "peak_source": peak_src,
+                         "algorithmic_bytes": "forward 32 B, reverse 96 B, ascending 96 B per amplitude per slot "
+                                              "(SURVEY 8(d)); x 2^16 amplitudes x 36 slots x summands"},
+            "phases": phases,
+            "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(rec_bytes),
+                    "path": "gf.gradient_and_hvp(circuit, ChebyshevOracle, directions): phi0 regenerated per summand"},
+            "gpu_launches": launches_all,
+            "clocks": clocks,
+            "gate_apply": gate_sweep,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--summands", type=int, default=None,
+                    help="profiling only: restrict each step to the first S basis states")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

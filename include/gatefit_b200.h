@@ -141,6 +141,12 @@ int gf_plan_eval(gf_plan *plan, int flags, int64_t nvec, const int64_t *basis_de
 int gf_plan_slot_outputs(gf_plan *plan, int64_t nvec, double *d_dev, double *h_dev, void *stream);
 /* Number of this library's kernels launched by the last gf_plan_eval. */
 int64_t gf_plan_last_launches(const gf_plan *plan);
+/* Phase timing with CUDA events on the eval stream (off by default).
+ * Turning it on resets the accumulators; gf_plan_phase_times waits for the
+ * last eval and returns accumulated milliseconds and kernel launches of
+ * [forward sweep, reverse sweep, ascending sweep, reductions]. */
+int gf_plan_set_profiling(gf_plan *plan, int on);
+int gf_plan_phase_times(gf_plan *plan, double *ms4, int64_t *launches4);
 int gf_plan_destroy(gf_plan *plan);
 
 /* ------------------------------------------------------------------ *

@@ -229,7 +229,8 @@ __global__ void k_reduce_ctas(const double *part, double *q, int64_t nsb, int ct
 // Chunk records.  rec = [value(2)] [D: nlog*32] [H: nlog*32].
 __global__ void k_chunk_records(const double *qD, const double *qHd, const double *qHa, const double *partV,
                                 int64_t nvec, int ctas, int nslots, int nlog, const int *lstart,
-                                const int *lslots, const int *swapped, int chunk, int flags, double *out)
+                                const int *lslots, const int *swapped, int chunk, int flags, int parity_only,
+                                double *out)
 {
     const int rec = 2 + 64 * nlog;
     const int64_t nchunks = (nvec + chunk - 1) / chunk;
@@ -252,7 +253,11 @@ __global__ void k_chunk_records(const double *qD, const double *qHd, const doubl
         const int e = q >> 1, ri = q & 1;
         const int ii = e >> 2, jj = e & 3;
         const double *src = isH ? qHd : qD;
-        const bool want = isH ? (flags & 4) : (flags & 2);
+        // compressed-sector hole entries pairing opposite-parity rows/cols
+        // would pair different implicit-qubit values: exactly zero in the
+        // full-space sum (both vectors live in the sector)
+        const bool offpat = parity_only && (((ii ^ (ii >> 1)) & 1) != ((jj ^ (jj >> 1)) & 1));
+        const bool want = (isH ? (flags & 4) : (flags & 2)) && !offpat;
         if (want) {
             for (int64_t b = b0; b < b1; ++b)
                 for (int t = lstart[l]; t < lstart[l + 1]; ++t) {
@@ -272,12 +277,18 @@ __global__ void k_chunk_records(const double *qD, const double *qHd, const doubl
 }
 
 // per-slot sums over the batch: q[s][b][32] -> out[s][32]
-__global__ void k_slot_sums(const double *q, const double *q2, int64_t nvec, int nslots, double *out)
+__global__ void k_slot_sums(const double *q, const double *q2, int64_t nvec, int nslots, int parity_only,
+                            double *out)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nslots * 32) return;
     int s = i >> 5, e = i & 31;
+    int ii = (e >> 1) >> 2, jj = (e >> 1) & 3;
     double acc = 0.0;
+    if (parity_only && (((ii ^ (ii >> 1)) & 1) != ((jj ^ (jj >> 1)) & 1))) {
+        out[i] = 0.0;
+        return;
+    }
     for (int64_t b = 0; b < nvec; ++b) {
         acc += q[((int64_t)s * nvec + b) * 32 + e];
         if (q2) acc += q2[((int64_t)s * nvec + b) * 32 + e];
@@ -315,6 +326,12 @@ struct gf_plan {
     int *d_lstart = nullptr, *d_lslots = nullptr, *d_swapped = nullptr;
     int64_t last_launches = 0;
     int last_flags = 0;
+    // optional phase timing (CUDA events on the eval stream)
+    bool profiling = false;
+    cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    double phase_ms[4] = {0, 0, 0, 0};  // accumulated: forward, reverse, ascending, reduce
+    int64_t phase_launches[4] = {0, 0, 0, 0};
+    int pending = 0;
 };
 
 static Mat4 to_mat4(const double *m)
@@ -368,6 +385,8 @@ static bool parity_zeros(const Mat4 &a)
 
 static void plan_free(gf_plan *p)
 {
+    for (auto &e : p->ev)
+        if (e) cudaEventDestroy(e);
     void *ptrs[] = {p->psi, p->bra, p->aux, p->partD, p->partHd, p->partHa, p->partV,
                     p->qD, p->qHd, p->qHa, p->d_lstart, p->d_lslots, p->d_swapped};
     for (void *q : ptrs)
@@ -474,8 +493,9 @@ extern "C" int gf_plan_set_gates(gf_plan *p, const double *mats)
     for (int s = 0; s < p->n; ++s) {
         Mat4 g = to_mat4(mats + 32 * p->slots[s].logical);
         if (p->slots[s].swapped) g = wire_swap(g);
-        if (p->slots[s].mode_c1q && !parity_zeros(g))
-            return gf_fail(GF_EINVAL, "slot %d acts on the compressed qubit but its gate is not parity-conserving", s);
+        if (p->sector >= 0 && !parity_zeros(g))
+            return gf_fail(GF_EINVAL,
+                           "parity-sector evaluation needs parity-conserving gates (slot %d has off-pattern entries)", s);
         p->G[s] = g;
         p->Gt[s] = transpose(g);
         p->Gc[s] = conjugate(g);
@@ -502,6 +522,8 @@ extern "C" int gf_plan_set_directions(gf_plan *p, const double *zmats)
     p->have_z = true;
     return GF_OK;
 }
+
+static int collect_phases(gf_plan *p);
 
 template <int OP, bool FIRST>
 static void launch_sweep(const gf_plan *p, const SlotInfo &si, bool sparse, SweepParams &sp, int64_t nvec,
@@ -544,12 +566,17 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
     sp.sector = p->sector < 0 ? 0 : p->sector;
     const size_t pstride = (size_t)32 * p->ctas * nvec;
 
+    if (p->profiling) {
+        if (p->pending) collect_phases(p);
+        GF_CUDA(cudaEventRecord(p->ev[0], st));
+    }
     {
         u64 total = p->N * (u64)nvec;
         int blocks = (int)std::min<u64>((total + 255) / 256, 148 * 16);
         k_init_basis<<<blocks, 256, 0, st>>>(p->psi, p->N, basis, nvec);
         ++launches;
     }
+    int64_t l_fwd = 0, l_rev = 0, l_asc = 0;
     const bool grad_like = (flags & (GF_GRAD | GF_HVP)) != 0;
     if (n == 0) {
         // empty circuit: value = sum phi0 . |j>; an identity "slot" with the dot fused
@@ -575,6 +602,8 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
         }
         ++launches;
     }
+    l_fwd = launches;
+    if (p->profiling) GF_CUDA(cudaEventRecord(p->ev[1], st));
     if (grad_like && n > 0) {
         const bool h = (flags & GF_HVP) != 0;
         for (int s = n - 1; s >= 0; --s) {
@@ -598,6 +627,8 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
             }
             ++launches;
         }
+        l_rev = launches - l_fwd;
+        if (p->profiling) GF_CUDA(cudaEventRecord(p->ev[2], st));
         if (h) {
             for (int s = 0; s < n; ++s) {
                 const SlotInfo &si = p->slots[s];
@@ -614,6 +645,9 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
             }
         }
     }
+    if (!(grad_like && n > 0) && p->profiling) GF_CUDA(cudaEventRecord(p->ev[2], st));
+    l_asc = launches - l_fwd - l_rev;
+    if (p->profiling) GF_CUDA(cudaEventRecord(p->ev[3], st));
     if (grad_like && n > 0) {
         int64_t nsb = (int64_t)n * nvec;
         int blocks = (int)((nsb * 32 + 255) / 256);
@@ -632,12 +666,59 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
         int eff = (n > 0) ? flags : (flags & GF_VALUE);
         k_chunk_records<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
             p->qD, p->qHd, p->qHa, p->partV, nvec, p->ctas, n, p->nlog, p->d_lstart, p->d_lslots, p->d_swapped,
-            p->chunk, eff, out);
+            p->chunk, eff, p->sector >= 0, out);
         ++launches;
+    }
+    if (p->profiling) {
+        GF_CUDA(cudaEventRecord(p->ev[4], st));
+        p->pending = 1;
+        p->phase_launches[0] += l_fwd;
+        p->phase_launches[1] += l_rev;
+        p->phase_launches[2] += l_asc;
+        p->phase_launches[3] += launches - l_fwd - l_rev - l_asc;
     }
     GF_CUDA(cudaGetLastError());
     p->last_launches = launches;
     p->last_flags = flags;
+    return GF_OK;
+}
+
+static int collect_phases(gf_plan *p)
+{
+    if (!p->pending) return GF_OK;
+    GF_CUDA(cudaEventSynchronize(p->ev[4]));
+    for (int i = 0; i < 4; ++i) {
+        float ms = 0.f;
+        GF_CUDA(cudaEventElapsedTime(&ms, p->ev[i], p->ev[i + 1]));
+        p->phase_ms[i] += ms;
+    }
+    p->pending = 0;
+    return GF_OK;
+}
+
+extern "C" int gf_plan_set_profiling(gf_plan *p, int on)
+{
+    if (!p) return gf_fail(GF_EINVAL, "null plan");
+    if (on && !p->ev[0])
+        for (auto &e : p->ev) GF_CUDA(cudaEventCreate(&e));
+    p->profiling = on != 0;
+    p->pending = 0;
+    for (int i = 0; i < 4; ++i) {
+        p->phase_ms[i] = 0.0;
+        p->phase_launches[i] = 0;
+    }
+    return GF_OK;
+}
+
+extern "C" int gf_plan_phase_times(gf_plan *p, double *ms4, int64_t *launches4)
+{
+    if (!p || !ms4) return gf_fail(GF_EINVAL, "null argument");
+    int rc = collect_phases(p);
+    if (rc) return rc;
+    for (int i = 0; i < 4; ++i) {
+        ms4[i] = p->phase_ms[i];
+        if (launches4) launches4[i] = p->phase_launches[i];
+    }
     return GF_OK;
 }
 
@@ -647,8 +728,8 @@ extern "C" int gf_plan_slot_outputs(gf_plan *p, int64_t nvec, double *d_dev, dou
     cudaStream_t st = (cudaStream_t)stream;
     int blocks = (p->n * 32 + 255) / 256;
     if (blocks == 0) return GF_OK;
-    if (d_dev) k_slot_sums<<<blocks, 256, 0, st>>>(p->qD, nullptr, nvec, p->n, d_dev);
-    if (h_dev) k_slot_sums<<<blocks, 256, 0, st>>>(p->qHd, p->qHa, nvec, p->n, h_dev);
+    if (d_dev) k_slot_sums<<<blocks, 256, 0, st>>>(p->qD, nullptr, nvec, p->n, p->sector >= 0, d_dev);
+    if (h_dev) k_slot_sums<<<blocks, 256, 0, st>>>(p->qHd, p->qHa, nvec, p->n, p->sector >= 0, h_dev);
     GF_CUDA(cudaGetLastError());
     return GF_OK;
 }

@@ -48,6 +48,7 @@ __all__ = [
     "KrylovOracle",
     "KrylovConvergenceError",
     "spinful_layer_circuit",
+    "CachedTargetColumns",
 ]
 
 _HOP = np.array([[0, 0, 0, 0], [0, 0, 1, 0], [0, 1, 0, 0], [0, 0, 0, 0]], dtype=np.complex128)
@@ -430,6 +431,57 @@ class ChebyshevOracle:
         idx = js_full if sector is None else (js_full >> 1)
         v0[torch.arange(B, device=out.device), idx] = 1.0
         self._series(v0, sector, out=out)
+
+
+class CachedTargetColumns:
+    """phi0 rows for basis positions [p0, p1) of one basis-sum layout,
+    computed once by an inner oracle and kept resident in HBM (the target
+    does not change across trust-region iterations).  ``phi0_at`` hands the
+    engine zero-copy views; positions outside the cached range fall back to
+    the inner oracle."""
+
+    def __init__(self, oracle, k: int, p0: int, p1: int, sector=None, indices=None, batch: int = 256):
+        self.num_qubits = oracle.num_qubits
+        self.inner = oracle
+        self.p0, self.p1 = p0, p1
+        self.sector = sector
+        self.indices = None if indices is None else np.asarray(indices, np.int64).copy()
+        dev = torch.device("cuda", torch.cuda.current_device())
+        N = 1 << (k - (0 if sector is None else 1))
+        self.rows = torch.empty((p1 - p0, N), dtype=torch.complex128, device=dev)
+        for s in range(p0, p1, batch):
+            e = min(p1, s + batch)
+            if indices is None:
+                st = torch.arange(s, e, dtype=torch.int64, device=dev)
+            else:
+                st = torch.from_numpy(np.ascontiguousarray(indices[s:e])).to(dev)
+            if sector is None:
+                js = st
+            else:
+                js = torch.empty_like(st)
+                _lib.check(_lib.lib.gf_sector_unrank(st.data_ptr(), st.numel(), int(sector), js.data_ptr(),
+                                                     _lib.stream_ptr()))
+            oracle.phi0_into(js, sector, self.rows[s - p0:e - p0])
+
+    def apply(self, state):
+        return self.inner.apply(state)
+
+    def apply_adjoint(self, state):
+        return self.inner.apply_adjoint(state)
+
+    def phi0_into(self, js_full, sector, out):
+        self.inner.phi0_into(js_full, sector, out)
+
+    def phi0_at(self, pos: int, nvec: int, sector_code: int, indices=None):
+        want = None if sector_code < 0 else sector_code
+        if want != self.sector or pos < self.p0 or pos + nvec > self.p1:
+            return None
+        if (indices is None) != (self.indices is None):
+            return None
+        if indices is not None and not np.array_equal(indices[pos:pos + nvec],
+                                                      self.indices[pos:pos + nvec]):
+            return None
+        return self.rows[pos - self.p0:pos - self.p0 + nvec]
 
 
 #: drop-in name for the reference's matrix-free oracle (models.py:322)

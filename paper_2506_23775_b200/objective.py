@@ -402,10 +402,14 @@ class _Run:
             else:
                 basis = idx_all[pos:pos + nvec].contiguous()
             weights = None if w_all is None else w_all[pos:pos + nvec].contiguous()
-            self._fill_phi0(basis, phi0[:nvec])
+            rows = getattr(self.oracle, "phi0_at", None)
+            cur = rows(pos, nvec, self.sector, self.spec.indices) if rows is not None else None
+            if cur is None:
+                self._fill_phi0(basis, phi0[:nvec])
+                cur = phi0
             c0 = (pos // chunk) - lo
             nc = (nvec + chunk - 1) // chunk
-            self.plan.eval(self.flags, nvec, basis, weights, phi0, local[c0:c0 + nc])
+            self.plan.eval(self.flags, nvec, basis, weights, cur, local[c0:c0 + nc])
             launches += self.plan.last_launches()
             pos += nvec
         allrec = gather_records(local, lo, nchunks, self.rank, self.world, self.dist)
