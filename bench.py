@@ -285,6 +285,8 @@ def run_b200(args):
     nchunks = TOTAL // chunk
     lo, hi = obj.shard_chunks(nchunks, rank, world)
     p0, p1 = lo * chunk, hi * chunk
+    if args.summands:
+        p1 = min(p1, p0 + args.summands)
     batch = args.batch or obj._default_batch(N, TOTAL)
     oracle = gf.ChebyshevOracle(spec, T_EVOL)
     t_or = time.perf_counter()
