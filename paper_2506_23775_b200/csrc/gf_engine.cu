@@ -16,11 +16,13 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
 
 #include "gf_common.cuh"
+#include "gf_fused.cuh"
 #include "gf_internal.h"
 
 namespace gf {
@@ -203,6 +205,292 @@ __global__ void __launch_bounds__(kThreads) k_sweep(const SweepParams p)
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Fused tile pass (see gf_fused.cuh).  Grid: (ctas, nvec); each CTA walks the
+// tiles blockIdx.x, blockIdx.x + ctas, ... of vector blockIdx.y.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
+{
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ unsigned ins0u(unsigned t, int b)
+{
+    unsigned low = t & ((1u << b) - 1u);
+    return ((t >> b) << (b + 1)) | low;
+}
+
+template <int OP, bool FIRST>
+__global__ void __launch_bounds__(FT, 2) k_fused(const FusedParams p)
+{
+    constexpr int NV = (OP == OP_FWD || OP == OP_FWD_DOT) ? 1 : (OP == OP_REV_G ? 2 : 3);
+    constexpr bool HD = (OP == OP_REV_G || OP == OP_REV_GH);
+    constexpr bool HH = (OP == OP_REV_GH || OP == OP_ASC_H);
+    constexpr bool HV = (OP == OP_FWD_DOT) || (HD && FIRST);
+    constexpr bool REV = (OP == OP_REV_G || OP == OP_REV_GH);
+    extern __shared__ __align__(16) unsigned char fsm[];
+    const int m = p.m, c = p.c;
+    const unsigned T = 1u << m;
+    double2 *t0 = reinterpret_cast<double2 *>(fsm);  // psi
+    double2 *t1 = t0 + T;                            // bra
+    double2 *t2 = t0 + 2 * T;                        // chi (REV) / v (ASC)
+    double *scratch = reinterpret_cast<double *>(t0 + NV * T);  // [2][8][64]
+    double *sacc = scratch + 2 * 8 * 64;                        // [FMAXSLOTS][2][32]
+    u64 *hiofs = reinterpret_cast<u64 *>(sacc + FMAXSLOTS * 2 * 32);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const u64 vb = (u64)blockIdx.y * p.N;
+    double2 *psi = p.psi + vb;
+    double2 *bra = p.bra + vb;
+    double2 *aux = p.aux + vb;
+    const double2 *phi0 = p.phi0 ? p.phi0 + vb : nullptr;
+    const double w = p.weights ? p.weights[blockIdx.y] : 1.0;
+
+    const int nh = 1 << (m - c);
+    for (int h = tid; h < nh; h += FT) {
+        u64 o = 0;
+        for (int i = 0; i < m - c; ++i)
+            if ((h >> i) & 1) o |= 1ull << p.lpos[c + i];
+        hiofs[h] = o;
+    }
+    for (int i = tid; i < FMAXSLOTS * 2 * 32; i += FT) sacc[i] = 0.0;
+    __syncthreads();
+    double vre = 0.0, vim = 0.0;
+    const unsigned cmask = (1u << c) - 1u;
+    const int g = lane >> 2, tq = lane & 3;
+    const int gi = g & 3, gpart = g >> 2;
+
+    for (u64 tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+        u64 base = 0;
+        for (int i = 0; i < p.nglob; ++i)
+            if ((tile >> i) & 1ull) base |= 1ull << p.gpos[i];
+        const int tpop = __popcll(tile);
+        for (unsigned l = tid; l < T; l += FT) {
+            const u64 a = base + (l & cmask) + hiofs[l >> c];
+            const double2 x = psi[a];
+            t0[l] = x;
+            if constexpr (NV >= 2) {
+                double2 b;
+                if constexpr (REV && FIRST) {
+                    b = cscale(phi0[a], w);
+                    vre = fma(b.x, x.x, vre);
+                    vre = fma(-b.y, x.y, vre);
+                    vim = fma(b.x, x.y, vim);
+                    vim = fma(b.y, x.x, vim);
+                } else {
+                    b = bra[a];
+                }
+                t1[l] = b;
+            }
+            if constexpr (NV >= 3) t2[l] = FIRST ? czero() : aux[a];
+        }
+        __syncthreads();
+
+        for (int si = 0; si < p.nslots; ++si) {
+            const int mode = p.ps[si].mode;
+            const int llo = p.ps[si].llo, lhi = p.ps[si].lhi;
+            const Mat4 &MA = p.mat[si][0];
+            const Mat4 &MB = p.mat[si][1];
+            const Mat4 &MC = p.mat[si][2];
+            double cD0 = 0.0, cD1 = 0.0, cH0 = 0.0, cH1 = 0.0;
+            const bool c1q = (mode == PM_C1Q);
+            const unsigned nunit = c1q ? (T >> 1) : (T >> 2);
+            const unsigned TW = max(nunit / 8u, 4u);
+            const unsigned nwa = nunit / TW;
+            const unsigned olo = 1u << llo, ohi = 1u << lhi;
+            if ((unsigned)warp < nwa) {
+                // ---- step 1: psi <- G^dag psi (REV) | bra <- conj(G) bra (ASC) | psi <- G psi (FWD)
+                for (unsigned j = lane; j < TW; j += 32) {
+                    const unsigned tau = warp * TW + j;
+                    double2 *V = (OP == OP_ASC_H) ? t1 : t0;
+                    if (c1q) {
+                        const unsigned l0 = ins0u(tau, llo);
+                        const int P = (tpop + __popc(l0)) & 1 ^ p.sector;
+                        double2 x[2] = {V[l0], V[l0 | olo]}, y[2];
+                        mv2(MA, P, x, y);
+                        V[l0] = y[0];
+                        V[l0 | olo] = y[1];
+                    } else {
+                        const unsigned b = ins0u(ins0u(tau, llo), lhi);
+                        double2 x[4] = {V[b], V[b + olo], V[b + ohi], V[b + olo + ohi]}, y[4];
+                        if (mode == PM_SPARSE) mv4<true>(MA, x, y); else mv4<false>(MA, x, y);
+                        V[b] = y[0];
+                        V[b + olo] = y[1];
+                        V[b + ohi] = y[2];
+                        V[b + olo + ohi] = y[3];
+                    }
+                }
+                if constexpr (HD || HH) {
+                    __syncwarp();
+                    // ---- holes on the tensor cores: env samples = this warp's units
+                    const double *d0 = reinterpret_cast<const double *>(t0);
+                    const double *d1 = reinterpret_cast<const double *>(t1);
+                    const double *d2 = reinterpret_cast<const double *>(t2);
+                    for (unsigned q = 0; q < TW / 4; ++q) {
+                        const unsigned tau = warp * TW + 4 * q + tq;
+                        int li;
+                        if (c1q) {
+                            const unsigned l0 = ins0u(tau, llo);
+                            const int P = (tpop + __popc(l0)) & 1 ^ p.sector;
+                            const int i0 = P ? 1 : 0, i1 = P ? 2 : 3;
+                            li = (gi == i0) ? (int)l0 : ((gi == i1) ? (int)(l0 | olo) : -1);
+                        } else {
+                            const unsigned b = ins0u(ins0u(tau, llo), lhi);
+                            li = (int)(b + ((gi & 2) ? ohi : 0u) + ((gi & 1) ? olo : 0u));
+                        }
+                        const int o = 2 * li + gpart;
+                        if constexpr (REV) {
+                            const double k = li >= 0 ? d0[o] : 0.0;  // ket = psi_l
+                            dmma(cD0, cD1, li >= 0 ? d1[o] : 0.0, k);
+                            if constexpr (HH) dmma(cH0, cH1, li >= 0 ? d2[o] : 0.0, k);
+                        } else {
+                            // ASC: bra = new bra, ket = v
+                            dmma(cH0, cH1, li >= 0 ? d1[o] : 0.0, li >= 0 ? d2[o] : 0.0);
+                        }
+                    }
+                    __syncwarp();
+                }
+                // ---- step 3
+                if constexpr (OP != OP_FWD && OP != OP_FWD_DOT) {
+                    for (unsigned j = lane; j < TW; j += 32) {
+                        const unsigned tau = warp * TW + j;
+                        if (c1q) {
+                            const unsigned l0 = ins0u(tau, llo), l1 = l0 | olo;
+                            const int P = (tpop + __popc(l0)) & 1 ^ p.sector;
+                            if constexpr (REV) {
+                                double2 b[2] = {t1[l0], t1[l1]}, bn[2];
+                                if constexpr (OP == OP_REV_GH) {
+                                    double2 cc[2] = {t2[l0], t2[l1]}, cn[2];
+                                    mv2(MB, P, cc, cn);
+                                    mv2_acc(MC, P, b, cn);
+                                    t2[l0] = cn[0];
+                                    t2[l1] = cn[1];
+                                }
+                                mv2(MB, P, b, bn);
+                                t1[l0] = bn[0];
+                                t1[l1] = bn[1];
+                            } else {
+                                double2 x[2] = {t0[l0], t0[l1]}, v[2] = {t2[l0], t2[l1]}, vn[2], y[2];
+                                mv2(MB, P, v, vn);
+                                mv2_acc(MC, P, x, vn);
+                                mv2(MB, P, x, y);
+                                t2[l0] = vn[0];
+                                t2[l1] = vn[1];
+                                t0[l0] = y[0];
+                                t0[l1] = y[1];
+                            }
+                        } else {
+                            const unsigned b0 = ins0u(ins0u(tau, llo), lhi);
+                            const unsigned L[4] = {b0, b0 + olo, b0 + ohi, b0 + olo + ohi};
+                            const bool sp = (mode == PM_SPARSE);
+                            if constexpr (REV) {
+                                double2 b[4], bn[4];
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) b[i] = t1[L[i]];
+                                if constexpr (OP == OP_REV_GH) {
+                                    double2 cc[4], cn[4];
+#pragma unroll
+                                    for (int i = 0; i < 4; ++i) cc[i] = t2[L[i]];
+                                    if (sp) { mv4<true>(MB, cc, cn); mv4_acc<true>(MC, b, cn); }
+                                    else { mv4<false>(MB, cc, cn); mv4_acc<false>(MC, b, cn); }
+#pragma unroll
+                                    for (int i = 0; i < 4; ++i) t2[L[i]] = cn[i];
+                                }
+                                if (sp) mv4<true>(MB, b, bn); else mv4<false>(MB, b, bn);
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) t1[L[i]] = bn[i];
+                            } else {
+                                double2 x[4], v[4], vn[4], y[4];
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) {
+                                    x[i] = t0[L[i]];
+                                    v[i] = t2[L[i]];
+                                }
+                                if (sp) { mv4<true>(MB, v, vn); mv4_acc<true>(MC, x, vn); mv4<true>(MB, x, y); }
+                                else { mv4<false>(MB, v, vn); mv4_acc<false>(MC, x, vn); mv4<false>(MB, x, y); }
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) {
+                                    t2[L[i]] = vn[i];
+                                    t0[L[i]] = y[i];
+                                }
+                            }
+                        }
+                    }
+                }
+            }
+            if constexpr (HD || HH) {
+                if ((unsigned)warp < nwa) {
+                    if (HD) {
+                        scratch[(0 * 8 + warp) * 64 + g * 8 + 2 * tq] = cD0;
+                        scratch[(0 * 8 + warp) * 64 + g * 8 + 2 * tq + 1] = cD1;
+                    }
+                    if (HH) {
+                        scratch[(1 * 8 + warp) * 64 + g * 8 + 2 * tq] = cH0;
+                        scratch[(1 * 8 + warp) * 64 + g * 8 + 2 * tq + 1] = cH1;
+                    }
+                }
+                __syncthreads();
+                if (tid < 64) {
+                    const int hole = tid >> 5;
+                    if ((hole == 0 && HD) || (hole == 1 && HH)) {
+                        const int i = tid & 31, e = i >> 1, part = i & 1, ii = e >> 2, jj = e & 3;
+                        double s = 0.0;
+                        for (unsigned ww = 0; ww < nwa; ++ww) {
+                            const double *C = scratch + (hole * 8 + ww) * 64;
+                            s += part == 0 ? (C[ii * 8 + jj] - C[(4 + ii) * 8 + 4 + jj])
+                                           : (C[ii * 8 + 4 + jj] + C[(4 + ii) * 8 + jj]);
+                        }
+                        sacc[(si * 2 + hole) * 32 + i] += s;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+
+        for (unsigned l = tid; l < T; l += FT) {
+            const u64 a = base + (l & cmask) + hiofs[l >> c];
+            const double2 x = t0[l];
+            psi[a] = x;
+            if constexpr (NV >= 2) bra[a] = t1[l];
+            if constexpr (NV >= 3) aux[a] = t2[l];
+            if constexpr (OP == OP_FWD_DOT) {
+                const double2 f = cscale(phi0[a], w);
+                vre = fma(f.x, x.x, vre);
+                vre = fma(-f.y, x.y, vre);
+                vim = fma(f.x, x.y, vim);
+                vim = fma(f.y, x.x, vim);
+            }
+        }
+        __syncthreads();
+    }
+
+    for (int i = tid; i < p.nslots * 64; i += FT) {
+        const int si = i >> 6, hole = (i >> 5) & 1, e = i & 31;
+        if ((hole == 0 && HD) || (hole == 1 && HH)) {
+            double *dst = hole == 0 ? p.partD : p.partH;
+            const u64 slot = (u64)p.ps[si].slot;
+            dst[((slot * p.nvec + blockIdx.y) * p.ctas + blockIdx.x) * 32 + e] = sacc[(si * 2 + hole) * 32 + e];
+        }
+    }
+    if constexpr (HV) {
+        vre = warp_sum(vre);
+        vim = warp_sum(vim);
+        __syncthreads();
+        if (lane == 0) {
+            scratch[warp * 2] = vre;
+            scratch[warp * 2 + 1] = vim;
+        }
+        __syncthreads();
+        if (tid < 2) {
+            double s = 0.0;
+            for (int ww = 0; ww < FT / 32; ++ww) s += scratch[ww * 2 + tid];
+            p.partV[((u64)blockIdx.y * p.ctas + blockIdx.x) * 2 + tid] = s;
+        }
+    }
+}
+
 // |j> for every vector of the batch (basis index per vector).
 __global__ void k_init_basis(double2 *psi, u64 N, const int64_t *basis, int64_t nvec)
 {
@@ -326,6 +614,10 @@ struct gf_plan {
     int *d_lstart = nullptr, *d_lslots = nullptr, *d_swapped = nullptr;
     int64_t last_launches = 0;
     int last_flags = 0;
+    // fused tile engine
+    bool fused = false;
+    int fm = 0, fc = 0;
+    std::vector<FusedParams> fwd_passes, rev_passes;  // geometry only (matrices filled per eval)
     // optional phase timing (CUDA events on the eval stream)
     bool profiling = false;
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -393,6 +685,8 @@ static void plan_free(gf_plan *p)
         if (q) cudaFree(q);
 }
 
+static std::vector<FusedParams> plan_passes(const gf_plan *p, bool reverse);
+
 extern "C" int gf_plan_create(gf_plan **out, int k, int sector, int n_slots, const int32_t *t1, const int32_t *t2,
                               const int32_t *logical, int n_logical, int64_t max_batch, int chunk_states)
 {
@@ -443,6 +737,20 @@ extern "C" int gf_plan_create(gf_plan **out, int k, int sector, int n_slots, con
     u64 units = p->N / 4;
     int64_t ctas = (int64_t)(units / (kThreads * 4));
     p->ctas = (int)std::max<int64_t>(1, std::min<int64_t>(ctas, 148 * 8));
+    {
+        const char *eng = getenv("GF_ENGINE");
+        p->fused = p->K >= 6 && !(eng && strcmp(eng, "stream") == 0);
+        const char *fmenv = getenv("GF_FUSED_M");
+        int fm = fmenv ? atoi(fmenv) : 11;
+        p->fm = std::max(4, std::min(std::min(fm, FMAXM), p->K));
+        p->fc = std::min(4, p->fm);
+        if (p->fused) {
+            p->fwd_passes = plan_passes(p, false);
+            p->rev_passes = plan_passes(p, true);
+            u64 ntiles = 1ull << (p->K - p->fm);
+            p->ctas = (int)std::max<u64>(1, std::min<u64>((u64)p->ctas, ntiles));
+        }
+    }
     // workspace
     size_t vbytes = sizeof(double2) * p->N * (size_t)max_batch;
     size_t pbytes = sizeof(double) * 32 * (size_t)p->ctas * max_batch * std::max(1, n_slots);
@@ -523,6 +831,96 @@ extern "C" int gf_plan_set_directions(gf_plan *p, const double *zmats)
     return GF_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// Fused pass planning: greedy over the sweep order.  A slot joins the current
+// pass if its bits fit in the local set (<= m bits) and it commutes with every
+// earlier slot that was skipped (no shared qubit).  Slots acting on the
+// sector's implicit qubit share a virtual qubit so they never reorder among
+// themselves.
+// ---------------------------------------------------------------------------
+static std::vector<FusedParams> plan_passes(const gf_plan *p, bool reverse)
+{
+    std::vector<FusedParams> out;
+    const int n = p->n, K = p->K, m = p->fm, c = p->fc;
+    std::vector<int> remaining;
+    for (int i = 0; i < n; ++i) remaining.push_back(reverse ? n - 1 - i : i);
+    const int VIRT = 63;
+    while (!remaining.empty()) {
+        unsigned long long S = (1ull << c) - 1ull, blocked = 0ull;
+        std::vector<int> taken, rest;
+        for (int s : remaining) {
+            const SlotInfo &si = p->slots[s];
+            unsigned long long bits = si.mode_c1q ? (1ull << si.lo) : ((1ull << si.lo) | (1ull << si.hi));
+            unsigned long long dep = bits | (si.mode_c1q ? (1ull << VIRT) : 0ull);
+            if (dep & blocked) {
+                blocked |= dep;
+                rest.push_back(s);
+                continue;
+            }
+            unsigned long long S2 = S | bits;
+            if (__builtin_popcountll(S2) <= m && (int)taken.size() < FMAXSLOTS) {
+                S = S2;
+                taken.push_back(s);
+            } else {
+                blocked |= dep;
+                rest.push_back(s);
+            }
+        }
+        for (int b = 0; __builtin_popcountll(S) < m && b < K; ++b) S |= 1ull << b;  // pad with low bits
+        FusedParams fp;
+        memset(&fp, 0, sizeof fp);
+        fp.m = m;
+        fp.c = c;
+        int li = 0, gi = 0;
+        int lidx[64];
+        for (int b = 0; b < K; ++b) {
+            if ((S >> b) & 1ull) {
+                lidx[b] = li;
+                fp.lpos[li++] = b;
+            } else {
+                fp.gpos[gi++] = b;
+            }
+        }
+        fp.nglob = gi;
+        fp.ntiles = 1ull << gi;
+        fp.nslots = (int)taken.size();
+        for (int t = 0; t < fp.nslots; ++t) {
+            const SlotInfo &si = p->slots[taken[t]];
+            PassSlot ps;
+            ps.slot = taken[t];
+            ps.mode = si.mode_c1q ? PM_C1Q : PM_DENSE;  // sparse decided per eval
+            ps.llo = lidx[si.lo];
+            ps.lhi = si.mode_c1q ? 0 : lidx[si.hi];
+            fp.ps[t] = ps;
+        }
+        out.push_back(fp);
+        remaining = rest;
+    }
+    return out;
+}
+
+static size_t fused_smem(int nv, int m, int c)
+{
+    return sizeof(double2) * ((size_t)nv << m) + sizeof(double) * (2 * 8 * 64 + FMAXSLOTS * 2 * 32) +
+           sizeof(unsigned long long) * ((size_t)1 << (m - c));
+}
+
+template <int OP, bool FIRST>
+static int launch_fused(const gf_plan *p, FusedParams &fp, int64_t nvec, cudaStream_t st)
+{
+    const int nv = (OP == OP_FWD || OP == OP_FWD_DOT) ? 1 : (OP == OP_REV_G ? 2 : 3);
+    const size_t smem = fused_smem(nv, fp.m, fp.c);
+    static bool attr_done = false;
+    if (!attr_done) {
+        cudaFuncSetAttribute(k_fused<OP, FIRST>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr_done = true;
+    }
+    dim3 grid(p->ctas, (unsigned)nvec);
+    k_fused<OP, FIRST><<<grid, FT, smem, st>>>(fp);
+    return GF_OK;
+}
+
 static int collect_phases(gf_plan *p);
 
 template <int OP, bool FIRST>
@@ -588,60 +986,136 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
         launch_sweep<OP_FWD_DOT, false>(p, si, false, sp, nvec, st);
         ++launches;
     }
-    // forward sweep
-    for (int s = 0; s < n; ++s) {
-        const SlotInfo &si = p->slots[s];
-        sp.lo = si.lo;
-        sp.hi = si.hi;
-        sp.A = p->G[s];
-        if (!grad_like && s == n - 1) {
-            sp.partV = p->partV;
-            launch_sweep<OP_FWD_DOT, false>(p, si, p->spG[s], sp, nvec, st);
-        } else {
-            launch_sweep<OP_FWD, false>(p, si, p->spG[s], sp, nvec, st);
+    if (p->fused && n > 0) {
+        FusedParams fp;
+        auto setup = [&](FusedParams &f) {
+            f.psi = p->psi;
+            f.bra = p->bra;
+            f.aux = p->aux;
+            f.phi0 = (const double2 *)phi0;
+            f.weights = weights;
+            f.N = p->N;
+            f.nvec = (int)nvec;
+            f.ctas = p->ctas;
+            f.sector = p->sector < 0 ? 0 : p->sector;
+            f.partV = p->partV;
+        };
+        const int nf = (int)p->fwd_passes.size(), nr = (int)p->rev_passes.size();
+        for (int pi = 0; pi < nf; ++pi) {
+            fp = p->fwd_passes[pi];
+            setup(fp);
+            for (int t = 0; t < fp.nslots; ++t) {
+                const int s = fp.ps[t].slot;
+                fp.mat[t][0] = p->G[s];
+                if (fp.ps[t].mode != PM_C1Q) fp.ps[t].mode = p->spG[s] ? PM_SPARSE : PM_DENSE;
+            }
+            if (!grad_like && pi == nf - 1) launch_fused<OP_FWD_DOT, false>(p, fp, nvec, st);
+            else launch_fused<OP_FWD, false>(p, fp, nvec, st);
+            ++launches;
         }
-        ++launches;
-    }
-    l_fwd = launches;
-    if (p->profiling) GF_CUDA(cudaEventRecord(p->ev[1], st));
-    if (grad_like && n > 0) {
-        const bool h = (flags & GF_HVP) != 0;
-        for (int s = n - 1; s >= 0; --s) {
+        l_fwd = launches;
+        if (p->profiling) GF_CUDA(cudaEventRecord(p->ev[1], st));
+        if (grad_like) {
+            const bool h = (flags & GF_HVP) != 0;
+            for (int pi = 0; pi < nr; ++pi) {
+                fp = p->rev_passes[pi];
+                setup(fp);
+                fp.partD = p->partD;
+                fp.partH = p->partHd;
+                for (int t = 0; t < fp.nslots; ++t) {
+                    const int s = fp.ps[t].slot;
+                    fp.mat[t][0] = p->Gd[s];
+                    fp.mat[t][1] = p->Gt[s];
+                    if (h) fp.mat[t][2] = p->Zt[s];
+                    bool sp = p->spG[s] && (!h || p->spZ[s]);
+                    if (fp.ps[t].mode != PM_C1Q) fp.ps[t].mode = sp ? PM_SPARSE : PM_DENSE;
+                }
+                if (h) {
+                    if (pi == 0) launch_fused<OP_REV_GH, true>(p, fp, nvec, st);
+                    else launch_fused<OP_REV_GH, false>(p, fp, nvec, st);
+                } else {
+                    if (pi == 0) launch_fused<OP_REV_G, true>(p, fp, nvec, st);
+                    else launch_fused<OP_REV_G, false>(p, fp, nvec, st);
+                }
+                ++launches;
+            }
+            l_rev = launches - l_fwd;
+            if (p->profiling) GF_CUDA(cudaEventRecord(p->ev[2], st));
+            if (h) {
+                for (int pi = 0; pi < nf; ++pi) {
+                    fp = p->fwd_passes[pi];
+                    setup(fp);
+                    fp.partH = p->partHa;
+                    for (int t = 0; t < fp.nslots; ++t) {
+                        const int s = fp.ps[t].slot;
+                        fp.mat[t][0] = p->Gc[s];
+                        fp.mat[t][1] = p->G[s];
+                        fp.mat[t][2] = p->Z[s];
+                        bool sp = p->spG[s] && p->spZ[s];
+                        if (fp.ps[t].mode != PM_C1Q) fp.ps[t].mode = sp ? PM_SPARSE : PM_DENSE;
+                    }
+                    if (pi == 0) launch_fused<OP_ASC_H, true>(p, fp, nvec, st);
+                    else launch_fused<OP_ASC_H, false>(p, fp, nvec, st);
+                    ++launches;
+                }
+            }
+        }
+    } else {
+    // forward sweep
+        for (int s = 0; s < n; ++s) {
             const SlotInfo &si = p->slots[s];
             sp.lo = si.lo;
             sp.hi = si.hi;
-            sp.A = p->Gd[s];
-            sp.B = p->Gt[s];
-            sp.partD = p->partD + pstride * s;
-            sp.partV = p->partV;
-            const bool first = (s == n - 1);
-            if (h) {
-                sp.C = p->Zt[s];
-                sp.partH = p->partHd + pstride * s;
-                bool sparse = p->spG[s] && p->spZ[s];
-                if (first) launch_sweep<OP_REV_GH, true>(p, si, sparse, sp, nvec, st);
-                else launch_sweep<OP_REV_GH, false>(p, si, sparse, sp, nvec, st);
+            sp.A = p->G[s];
+            if (!grad_like && s == n - 1) {
+                sp.partV = p->partV;
+                launch_sweep<OP_FWD_DOT, false>(p, si, p->spG[s], sp, nvec, st);
             } else {
-                if (first) launch_sweep<OP_REV_G, true>(p, si, p->spG[s], sp, nvec, st);
-                else launch_sweep<OP_REV_G, false>(p, si, p->spG[s], sp, nvec, st);
+                launch_sweep<OP_FWD, false>(p, si, p->spG[s], sp, nvec, st);
             }
             ++launches;
         }
-        l_rev = launches - l_fwd;
-        if (p->profiling) GF_CUDA(cudaEventRecord(p->ev[2], st));
-        if (h) {
-            for (int s = 0; s < n; ++s) {
+        l_fwd = launches;
+        if (p->profiling) GF_CUDA(cudaEventRecord(p->ev[1], st));
+        if (grad_like && n > 0) {
+            const bool h = (flags & GF_HVP) != 0;
+            for (int s = n - 1; s >= 0; --s) {
                 const SlotInfo &si = p->slots[s];
                 sp.lo = si.lo;
                 sp.hi = si.hi;
-                sp.A = p->Gc[s];
-                sp.B = p->G[s];
-                sp.C = p->Z[s];
-                sp.partH = p->partHa + pstride * s;
-                bool sparse = p->spG[s] && p->spZ[s];
-                if (s == 0) launch_sweep<OP_ASC_H, true>(p, si, sparse, sp, nvec, st);
-                else launch_sweep<OP_ASC_H, false>(p, si, sparse, sp, nvec, st);
+                sp.A = p->Gd[s];
+                sp.B = p->Gt[s];
+                sp.partD = p->partD + pstride * s;
+                sp.partV = p->partV;
+                const bool first = (s == n - 1);
+                if (h) {
+                    sp.C = p->Zt[s];
+                    sp.partH = p->partHd + pstride * s;
+                    bool sparse = p->spG[s] && p->spZ[s];
+                    if (first) launch_sweep<OP_REV_GH, true>(p, si, sparse, sp, nvec, st);
+                    else launch_sweep<OP_REV_GH, false>(p, si, sparse, sp, nvec, st);
+                } else {
+                    if (first) launch_sweep<OP_REV_G, true>(p, si, p->spG[s], sp, nvec, st);
+                    else launch_sweep<OP_REV_G, false>(p, si, p->spG[s], sp, nvec, st);
+                }
                 ++launches;
+            }
+            l_rev = launches - l_fwd;
+            if (p->profiling) GF_CUDA(cudaEventRecord(p->ev[2], st));
+            if (h) {
+                for (int s = 0; s < n; ++s) {
+                    const SlotInfo &si = p->slots[s];
+                    sp.lo = si.lo;
+                    sp.hi = si.hi;
+                    sp.A = p->Gc[s];
+                    sp.B = p->G[s];
+                    sp.C = p->Z[s];
+                    sp.partH = p->partHa + pstride * s;
+                    bool sparse = p->spG[s] && p->spZ[s];
+                    if (s == 0) launch_sweep<OP_ASC_H, true>(p, si, sparse, sp, nvec, st);
+                    else launch_sweep<OP_ASC_H, false>(p, si, sparse, sp, nvec, st);
+                    ++launches;
+                }
             }
         }
     }

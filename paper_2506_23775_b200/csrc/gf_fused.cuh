@@ -1,0 +1,50 @@
+// gf_fused.cuh -- fused k-qubit tile passes (north-star item 1).
+//
+// A pass applies a run of slots whose target bits all lie in a set S of m
+// "local" bit positions (always including the c lowest bits, so every HBM
+// access is a >= 256 B contiguous run).  One CTA stages a tile -- the 2^m
+// amplitudes sharing one assignment of the K-m global bits -- of every vector
+// the sweep touches (psi, bra, chi/v) in shared memory, runs all slots of the
+// pass on it, and writes it back: one HBM round trip per pass instead of one
+// per slot.  Gate applications are FP64 FMAs on 4-amplitude tuples; the 4x4
+// hole contractions (reference kernels.py:208-242) are FP64 tensor-core
+// MMAs (DMMA m8n8k4): with the complex 4-vectors split into 8 real
+// components, C[r][s] = sum_env bra_r ket_s is an 8x8 GEMM with the
+// environment as the K dimension, accumulated in 2 registers per lane; the
+// 8 warps' fragments are summed in a fixed order in shared memory, so the
+// result is deterministic.
+#pragma once
+#include "gf_common.cuh"
+
+namespace gf {
+
+constexpr int FT = 256;         // threads per fused CTA (8 warps)
+constexpr int FMAXM = 12;       // max local bits
+constexpr int FMAXSLOTS = 12;   // max slots per pass
+constexpr int FMAXGLOB = 40;
+
+enum { PM_DENSE = 0, PM_SPARSE = 1, PM_C1Q = 2 };
+
+struct PassSlot {
+    int slot;  // circuit slot index (for the partial layout)
+    int mode;  // PM_*
+    int llo;   // local bit index of the low target bit (c1q: the explicit qubit)
+    int lhi;   // local bit index of the high target bit (unused for c1q)
+};
+
+struct FusedParams {
+    double2 *psi, *bra, *aux;  // [nvec][N]
+    const double2 *phi0;       // [nvec][N]
+    const double *weights;     // [nvec] or null
+    double *partD, *partH, *partV;
+    unsigned long long N;
+    unsigned long long ntiles;  // 2^(K-m)
+    int nvec, ctas, sector;
+    int m, c, nglob, nslots;
+    int lpos[FMAXM];
+    int gpos[FMAXGLOB];
+    PassSlot ps[FMAXSLOTS];
+    Mat4 mat[FMAXSLOTS][3];  // per op: FWD {G}; REV {G^dag, G^T, Z^T}; ASC {conj G, G, Z}
+};
+
+}  // namespace gf
