@@ -617,7 +617,11 @@ struct gf_plan {
     // fused tile engine
     bool fused = false;
     int fm = 0, fc = 0;
-    std::vector<FusedParams> fwd_passes, rev_passes;  // geometry only (matrices filled per eval)
+    // geometry only (matrices filled per eval).  The ascending HVP sweep must
+    // replay exactly the reverse slot order of the reverse sweep (the two HVP
+    // half-sums are only order-invariant together), so asc_passes is
+    // rev_passes reversed with each pass's slot list reversed.
+    std::vector<FusedParams> fwd_passes, rev_passes, asc_passes;
     // optional phase timing (CUDA events on the eval stream)
     bool profiling = false;
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -747,6 +751,8 @@ extern "C" int gf_plan_create(gf_plan **out, int k, int sector, int n_slots, con
         if (p->fused) {
             p->fwd_passes = plan_passes(p, false);
             p->rev_passes = plan_passes(p, true);
+            p->asc_passes.assign(p->rev_passes.rbegin(), p->rev_passes.rend());
+            for (auto &f : p->asc_passes) std::reverse(f.ps, f.ps + f.nslots);
             u64 ntiles = 1ull << (p->K - p->fm);
             p->ctas = (int)std::max<u64>(1, std::min<u64>((u64)p->ctas, ntiles));
         }
@@ -1042,8 +1048,8 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
             l_rev = launches - l_fwd;
             if (p->profiling) GF_CUDA(cudaEventRecord(p->ev[2], st));
             if (h) {
-                for (int pi = 0; pi < nf; ++pi) {
-                    fp = p->fwd_passes[pi];
+                for (int pi = 0; pi < nr; ++pi) {
+                    fp = p->asc_passes[pi];
                     setup(fp);
                     fp.partH = p->partHa;
                     for (int t = 0; t < fp.nslots; ++t) {

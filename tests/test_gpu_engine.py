@@ -351,3 +351,31 @@ def test_k20_single_summands_vs_oracle():
     assert abs(rep.value + v.real) < TOL * max(1, abs(v))
     assert rel_err(np.stack(rep.holomorphic_derivatives), plan.logical_sum(d)) < TOL
     assert rel_err(np.stack(hv), plan.logical_sum(h)) < TOL
+
+
+@pytest.mark.parametrize("engine,m", [("fused", "6"), ("fused", "7"), ("stream", None)])
+def test_multi_tile_multi_pass_engine_vs_oracle(monkeypatch, engine, m):
+    """Force tiny fused tiles (2^6 amplitudes) on a 12-qubit circuit: many
+    tiles per vector and many passes per sweep, both sector and full space."""
+    monkeypatch.setenv("GF_ENGINE", engine)
+    if m:
+        monkeypatch.setenv("GF_FUSED_M", m)
+    for sector, parity in ((None, False), (0, True)):
+        spec, circ, rng = gf.spinful_layer_circuit(6, 5, True, seed=12, parity=parity)
+        X = [manifold.project_tangent_gate(x.matrix, rng.normal(size=(4, 4)) + 1j * rng.normal(size=(4, 4)), parity)
+             for x in circ.logical_gates]
+        orc = gf.DenseOracle(spec, 0.25)
+        rep, hv = gf.gradient_and_hvp(circ, orc, X, parity_mode=parity, sector=sector, batch=64)
+        t1, t2, lid = circ.slot_arrays()
+        plan = O.Plan(12, np.stack([t1, t2], 1), lid, circ.gate_stack())
+        js = np.arange(4096) if sector is None else np.sort(O.sector_unrank(np.arange(2048), 0))
+        phi = O.dense_phi0(orc._u)
+        v, d, _ = O.gradient_sum(plan, js, phi, workers=8)
+        h, _ = O.hvp_sum(plan, X, js, phi, workers=8)
+        hol, hvo = plan.logical_sum(d), plan.logical_sum(h)
+        if sector is not None:
+            mask = np.array([[(i ^ (i >> 1)) & 1 == (j ^ (j >> 1)) & 1 for j in range(4)] for i in range(4)])
+            hol, hvo = hol * mask, hvo * mask
+        assert abs(rep.value + v.real) < TOL * max(1, abs(v))
+        assert rel_err(np.stack(rep.holomorphic_derivatives), hol) < TOL
+        assert rel_err(np.stack(hv), hvo) < TOL
