@@ -223,6 +223,14 @@ __device__ __forceinline__ unsigned ins0u(unsigned t, int b)
     return ((t >> b) << (b + 1)) | low;
 }
 
+// XOR swizzle of the tile index (double2 granularity): folds the bits above
+// the 128-byte bank group into it so that tuple members 2^llo / 2^lhi apart
+// land in different banks (ncu: half the smem wavefronts were conflicts).
+__device__ __forceinline__ unsigned swz(unsigned l)
+{
+    return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7u);
+}
+
 template <int OP, bool FIRST>
 __global__ void __launch_bounds__(FT, 2) k_fused(const FusedParams p)
 {
@@ -270,7 +278,7 @@ __global__ void __launch_bounds__(FT, 2) k_fused(const FusedParams p)
         for (unsigned l = tid; l < T; l += FT) {
             const u64 a = base + (l & cmask) + hiofs[l >> c];
             const double2 x = psi[a];
-            t0[l] = x;
+            t0[swz(l)] = x;
             if constexpr (NV >= 2) {
                 double2 b;
                 if constexpr (REV && FIRST) {
@@ -282,9 +290,9 @@ __global__ void __launch_bounds__(FT, 2) k_fused(const FusedParams p)
                 } else {
                     b = bra[a];
                 }
-                t1[l] = b;
+                t1[swz(l)] = b;
             }
-            if constexpr (NV >= 3) t2[l] = FIRST ? czero() : aux[a];
+            if constexpr (NV >= 3) t2[swz(l)] = FIRST ? czero() : aux[a];
         }
         __syncthreads();
 
@@ -308,18 +316,20 @@ __global__ void __launch_bounds__(FT, 2) k_fused(const FusedParams p)
                     if (c1q) {
                         const unsigned l0 = ins0u(tau, llo);
                         const int P = (tpop + __popc(l0)) & 1 ^ p.sector;
-                        double2 x[2] = {V[l0], V[l0 | olo]}, y[2];
+                        const unsigned s0 = swz(l0), s1 = swz(l0 | olo);
+                        double2 x[2] = {V[s0], V[s1]}, y[2];
                         mv2(MA, P, x, y);
-                        V[l0] = y[0];
-                        V[l0 | olo] = y[1];
+                        V[s0] = y[0];
+                        V[s1] = y[1];
                     } else {
                         const unsigned b = ins0u(ins0u(tau, llo), lhi);
-                        double2 x[4] = {V[b], V[b + olo], V[b + ohi], V[b + olo + ohi]}, y[4];
+                        const unsigned q0 = swz(b), q1 = swz(b + olo), q2 = swz(b + ohi), q3 = swz(b + olo + ohi);
+                        double2 x[4] = {V[q0], V[q1], V[q2], V[q3]}, y[4];
                         if (mode == PM_SPARSE) mv4<true>(MA, x, y); else mv4<false>(MA, x, y);
-                        V[b] = y[0];
-                        V[b + olo] = y[1];
-                        V[b + ohi] = y[2];
-                        V[b + olo + ohi] = y[3];
+                        V[q0] = y[0];
+                        V[q1] = y[1];
+                        V[q2] = y[2];
+                        V[q3] = y[3];
                     }
                 }
                 if constexpr (HD || HH) {
@@ -340,7 +350,7 @@ __global__ void __launch_bounds__(FT, 2) k_fused(const FusedParams p)
                             const unsigned b = ins0u(ins0u(tau, llo), lhi);
                             li = (int)(b + ((gi & 2) ? ohi : 0u) + ((gi & 1) ? olo : 0u));
                         }
-                        const int o = 2 * li + gpart;
+                        const int o = li >= 0 ? 2 * (int)swz((unsigned)li) + gpart : 0;
                         if constexpr (REV) {
                             const double k = li >= 0 ? d0[o] : 0.0;  // ket = psi_l
                             dmma(cD0, cD1, li >= 0 ? d1[o] : 0.0, k);
@@ -357,8 +367,8 @@ __global__ void __launch_bounds__(FT, 2) k_fused(const FusedParams p)
                     for (unsigned j = lane; j < TW; j += 32) {
                         const unsigned tau = warp * TW + j;
                         if (c1q) {
-                            const unsigned l0 = ins0u(tau, llo), l1 = l0 | olo;
-                            const int P = (tpop + __popc(l0)) & 1 ^ p.sector;
+                            const unsigned l0r = ins0u(tau, llo), l0 = swz(l0r), l1 = swz(l0r | olo);
+                            const int P = (tpop + __popc(l0r)) & 1 ^ p.sector;
                             if constexpr (REV) {
                                 double2 b[2] = {t1[l0], t1[l1]}, bn[2];
                                 if constexpr (OP == OP_REV_GH) {
@@ -383,7 +393,7 @@ __global__ void __launch_bounds__(FT, 2) k_fused(const FusedParams p)
                             }
                         } else {
                             const unsigned b0 = ins0u(ins0u(tau, llo), lhi);
-                            const unsigned L[4] = {b0, b0 + olo, b0 + ohi, b0 + olo + ohi};
+                            const unsigned L[4] = {swz(b0), swz(b0 + olo), swz(b0 + ohi), swz(b0 + olo + ohi)};
                             const bool sp = (mode == PM_SPARSE);
                             if constexpr (REV) {
                                 double2 b[4], bn[4];
@@ -451,10 +461,10 @@ __global__ void __launch_bounds__(FT, 2) k_fused(const FusedParams p)
 
         for (unsigned l = tid; l < T; l += FT) {
             const u64 a = base + (l & cmask) + hiofs[l >> c];
-            const double2 x = t0[l];
+            const double2 x = t0[swz(l)];
             psi[a] = x;
-            if constexpr (NV >= 2) bra[a] = t1[l];
-            if constexpr (NV >= 3) aux[a] = t2[l];
+            if constexpr (NV >= 2) bra[a] = t1[swz(l)];
+            if constexpr (NV >= 3) aux[a] = t2[swz(l)];
             if constexpr (OP == OP_FWD_DOT) {
                 const double2 f = cscale(phi0[a], w);
                 vre = fma(f.x, x.x, vre);
