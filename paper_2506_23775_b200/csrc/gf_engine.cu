@@ -231,6 +231,37 @@ __device__ __forceinline__ unsigned swz(unsigned l)
     return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7u);
 }
 
+// B fragment (two k-steps) of the real 8x8 form of a complex 4x4 gate for
+// the transposed product Y^T = X^T G^T on 8-tuple groups: lane (g, t) holds
+// amplitude t (re, im) of tuple g; k-step h feeds part h of that amplitude.
+// G_real[(i,pi)][(j,pj)]: (0,0)=re (0,1)=-im (1,0)=im (1,1)=re.
+__device__ __forceinline__ void gate_frag(const Mat4 &M, int g, int t, double &b0, double &b1)
+{
+    const double2 e = M.m[4 * (g >> 1) + t];
+    const bool pi = g & 1;
+    b0 = pi ? e.y : e.x;
+    b1 = pi ? e.x : -e.y;
+}
+
+// y (this lane's amplitude) = sum of DMMA products over (x, fragment) pairs
+__device__ __forceinline__ double2 dmma_mv(double2 x, double b0, double b1)
+{
+    double c0 = 0.0, c1 = 0.0;
+    dmma(c0, c1, x.x, b0);
+    dmma(c0, c1, x.y, b1);
+    return make_double2(c0, c1);
+}
+
+__device__ __forceinline__ double2 dmma_mv2(double2 x, double b0, double b1, double2 z, double e0, double e1)
+{
+    double c0 = 0.0, c1 = 0.0;
+    dmma(c0, c1, x.x, b0);
+    dmma(c0, c1, x.y, b1);
+    dmma(c0, c1, z.x, e0);
+    dmma(c0, c1, z.y, e1);
+    return make_double2(c0, c1);
+}
+
 template <int OP, bool FIRST>
 __global__ void __launch_bounds__(FT, 2) k_fused(const FusedParams p)
 {
@@ -310,10 +341,10 @@ __global__ void __launch_bounds__(FT, 2) k_fused(const FusedParams p)
             const unsigned olo = 1u << llo, ohi = 1u << lhi;
             if ((unsigned)warp < nwa) {
                 // ---- step 1: psi <- G^dag psi (REV) | bra <- conj(G) bra (ASC) | psi <- G psi (FWD)
-                for (unsigned j = lane; j < TW; j += 32) {
-                    const unsigned tau = warp * TW + j;
-                    double2 *V = (OP == OP_ASC_H) ? t1 : t0;
-                    if (c1q) {
+                double2 *V = (OP == OP_ASC_H) ? t1 : t0;
+                if (c1q) {
+                    for (unsigned j = lane; j < TW; j += 32) {
+                        const unsigned tau = warp * TW + j;
                         const unsigned l0 = ins0u(tau, llo);
                         const int P = (tpop + __popc(l0)) & 1 ^ p.sector;
                         const unsigned s0 = swz(l0), s1 = swz(l0 | olo);
@@ -321,15 +352,19 @@ __global__ void __launch_bounds__(FT, 2) k_fused(const FusedParams p)
                         mv2(MA, P, x, y);
                         V[s0] = y[0];
                         V[s1] = y[1];
-                    } else {
-                        const unsigned b = ins0u(ins0u(tau, llo), lhi);
-                        const unsigned q0 = swz(b), q1 = swz(b + olo), q2 = swz(b + ohi), q3 = swz(b + olo + ohi);
-                        double2 x[4] = {V[q0], V[q1], V[q2], V[q3]}, y[4];
-                        if (mode == PM_SPARSE) mv4<true>(MA, x, y); else mv4<false>(MA, x, y);
-                        V[q0] = y[0];
-                        V[q1] = y[1];
-                        V[q2] = y[2];
-                        V[q3] = y[3];
+                    }
+                } else {
+                    // tensor-core gate application: 8 tuples per group, lane (g, tq) owns amplitude tq of tuple g
+                    double fa0, fa1;
+                    gate_frag(MA, g, tq, fa0, fa1);
+                    const unsigned offt = ((tq & 2) ? ohi : 0u) + ((tq & 1) ? olo : 0u);
+                    for (unsigned grp = 0; grp < (TW + 7) / 8; ++grp) {
+                        const unsigned j = grp * 8 + g;
+                        const bool ok = j < TW;
+                        const unsigned addr = swz(ins0u(ins0u(warp * TW + (ok ? j : 0), llo), lhi) + offt);
+                        const double2 x = ok ? V[addr] : czero();
+                        const double2 y = dmma_mv(x, fa0, fa1);
+                        if (ok) V[addr] = y;
                     }
                 }
                 if constexpr (HD || HH) {
@@ -364,9 +399,9 @@ __global__ void __launch_bounds__(FT, 2) k_fused(const FusedParams p)
                 }
                 // ---- step 3
                 if constexpr (OP != OP_FWD && OP != OP_FWD_DOT) {
-                    for (unsigned j = lane; j < TW; j += 32) {
+                    for (unsigned j = lane; c1q && j < TW; j += 32) {
                         const unsigned tau = warp * TW + j;
-                        if (c1q) {
+                        {
                             const unsigned l0r = ins0u(tau, llo), l0 = swz(l0r), l1 = swz(l0r | olo);
                             const int P = (tpop + __popc(l0r)) & 1 ^ p.sector;
                             if constexpr (REV) {
@@ -391,39 +426,34 @@ __global__ void __launch_bounds__(FT, 2) k_fused(const FusedParams p)
                                 t0[l0] = y[0];
                                 t0[l1] = y[1];
                             }
-                        } else {
-                            const unsigned b0 = ins0u(ins0u(tau, llo), lhi);
-                            const unsigned L[4] = {swz(b0), swz(b0 + olo), swz(b0 + ohi), swz(b0 + olo + ohi)};
-                            const bool sp = (mode == PM_SPARSE);
+                        }
+                    }
+                    if (!c1q) {
+                        double fb0, fb1, fc0 = 0.0, fc1 = 0.0;
+                        gate_frag(MB, g, tq, fb0, fb1);
+                        if constexpr (OP == OP_REV_GH || OP == OP_ASC_H) gate_frag(MC, g, tq, fc0, fc1);
+                        const unsigned offt = ((tq & 2) ? ohi : 0u) + ((tq & 1) ? olo : 0u);
+                        for (unsigned grp = 0; grp < (TW + 7) / 8; ++grp) {
+                            const unsigned j = grp * 8 + g;
+                            const bool ok = j < TW;
+                            const unsigned addr = swz(ins0u(ins0u(warp * TW + (ok ? j : 0), llo), lhi) + offt);
                             if constexpr (REV) {
-                                double2 b[4], bn[4];
-#pragma unroll
-                                for (int i = 0; i < 4; ++i) b[i] = t1[L[i]];
+                                const double2 bb = ok ? t1[addr] : czero();
                                 if constexpr (OP == OP_REV_GH) {
-                                    double2 cc[4], cn[4];
-#pragma unroll
-                                    for (int i = 0; i < 4; ++i) cc[i] = t2[L[i]];
-                                    if (sp) { mv4<true>(MB, cc, cn); mv4_acc<true>(MC, b, cn); }
-                                    else { mv4<false>(MB, cc, cn); mv4_acc<false>(MC, b, cn); }
-#pragma unroll
-                                    for (int i = 0; i < 4; ++i) t2[L[i]] = cn[i];
+                                    const double2 cc = ok ? t2[addr] : czero();
+                                    const double2 cn = dmma_mv2(cc, fb0, fb1, bb, fc0, fc1);
+                                    if (ok) t2[addr] = cn;
                                 }
-                                if (sp) mv4<true>(MB, b, bn); else mv4<false>(MB, b, bn);
-#pragma unroll
-                                for (int i = 0; i < 4; ++i) t1[L[i]] = bn[i];
+                                const double2 bn = dmma_mv(bb, fb0, fb1);
+                                if (ok) t1[addr] = bn;
                             } else {
-                                double2 x[4], v[4], vn[4], y[4];
-#pragma unroll
-                                for (int i = 0; i < 4; ++i) {
-                                    x[i] = t0[L[i]];
-                                    v[i] = t2[L[i]];
-                                }
-                                if (sp) { mv4<true>(MB, v, vn); mv4_acc<true>(MC, x, vn); mv4<true>(MB, x, y); }
-                                else { mv4<false>(MB, v, vn); mv4_acc<false>(MC, x, vn); mv4<false>(MB, x, y); }
-#pragma unroll
-                                for (int i = 0; i < 4; ++i) {
-                                    t2[L[i]] = vn[i];
-                                    t0[L[i]] = y[i];
+                                const double2 x = ok ? t0[addr] : czero();
+                                const double2 v = ok ? t2[addr] : czero();
+                                const double2 vn = dmma_mv2(v, fb0, fb1, x, fc0, fc1);
+                                const double2 y = dmma_mv(x, fb0, fb1);
+                                if (ok) {
+                                    t2[addr] = vn;
+                                    t0[addr] = y;
                                 }
                             }
                         }
