@@ -333,76 +333,52 @@ __global__ void __launch_bounds__(FT, 2) k_fused(const FusedParams p)
             const Mat4 &MA = p.mat[si][0];
             const Mat4 &MB = p.mat[si][1];
             const Mat4 &MC = p.mat[si][2];
-            double cD0 = 0.0, cD1 = 0.0, cH0 = 0.0, cH1 = 0.0;
             const bool c1q = (mode == PM_C1Q);
             const unsigned nunit = c1q ? (T >> 1) : (T >> 2);
-            const unsigned TW = max(nunit / 8u, 4u);
+            // units per active warp: multiple of 4 (hole MMA K) -- and of 8 for the
+            // 2q tensor path (8-tuple groups, paired hole MMAs)
+            const unsigned TW = max(nunit / 8u, c1q ? 4u : 8u);
             const unsigned nwa = nunit / TW;
             const unsigned olo = 1u << llo, ohi = 1u << lhi;
+            double cD0 = 0.0, cD1 = 0.0, cH0 = 0.0, cH1 = 0.0;
             if ((unsigned)warp < nwa) {
-                // ---- step 1: psi <- G^dag psi (REV) | bra <- conj(G) bra (ASC) | psi <- G psi (FWD)
-                double2 *V = (OP == OP_ASC_H) ? t1 : t0;
+                const unsigned wbase = warp * TW;
                 if (c1q) {
+                    // ---- parity-controlled 1q slot (sector implicit qubit): FMA on pairs
                     for (unsigned j = lane; j < TW; j += 32) {
-                        const unsigned tau = warp * TW + j;
-                        const unsigned l0 = ins0u(tau, llo);
-                        const int P = (tpop + __popc(l0)) & 1 ^ p.sector;
-                        const unsigned s0 = swz(l0), s1 = swz(l0 | olo);
+                        const unsigned l0r = ins0u(wbase + j, llo);
+                        const int P = (tpop + __popc(l0r)) & 1 ^ p.sector;
+                        const unsigned s0 = swz(l0r), s1 = swz(l0r | olo);
+                        double2 *V = (OP == OP_ASC_H) ? t1 : t0;
                         double2 x[2] = {V[s0], V[s1]}, y[2];
                         mv2(MA, P, x, y);
                         V[s0] = y[0];
                         V[s1] = y[1];
                     }
-                } else {
-                    // tensor-core gate application: 8 tuples per group, lane (g, tq) owns amplitude tq of tuple g
-                    double fa0, fa1;
-                    gate_frag(MA, g, tq, fa0, fa1);
-                    const unsigned offt = ((tq & 2) ? ohi : 0u) + ((tq & 1) ? olo : 0u);
-                    for (unsigned grp = 0; grp < (TW + 7) / 8; ++grp) {
-                        const unsigned j = grp * 8 + g;
-                        const bool ok = j < TW;
-                        const unsigned addr = swz(ins0u(ins0u(warp * TW + (ok ? j : 0), llo), lhi) + offt);
-                        const double2 x = ok ? V[addr] : czero();
-                        const double2 y = dmma_mv(x, fa0, fa1);
-                        if (ok) V[addr] = y;
-                    }
-                }
-                if constexpr (HD || HH) {
-                    __syncwarp();
-                    // ---- holes on the tensor cores: env samples = this warp's units
-                    const double *d0 = reinterpret_cast<const double *>(t0);
-                    const double *d1 = reinterpret_cast<const double *>(t1);
-                    const double *d2 = reinterpret_cast<const double *>(t2);
-                    for (unsigned q = 0; q < TW / 4; ++q) {
-                        const unsigned tau = warp * TW + 4 * q + tq;
-                        int li;
-                        if (c1q) {
-                            const unsigned l0 = ins0u(tau, llo);
+                    if constexpr (HD || HH) {
+                        __syncwarp();
+                        const double *d0 = reinterpret_cast<const double *>(t0);
+                        const double *d1 = reinterpret_cast<const double *>(t1);
+                        const double *d2 = reinterpret_cast<const double *>(t2);
+                        for (unsigned q = 0; q < TW / 4; ++q) {
+                            const unsigned l0 = ins0u(wbase + 4 * q + tq, llo);
                             const int P = (tpop + __popc(l0)) & 1 ^ p.sector;
                             const int i0 = P ? 1 : 0, i1 = P ? 2 : 3;
-                            li = (gi == i0) ? (int)l0 : ((gi == i1) ? (int)(l0 | olo) : -1);
-                        } else {
-                            const unsigned b = ins0u(ins0u(tau, llo), lhi);
-                            li = (int)(b + ((gi & 2) ? ohi : 0u) + ((gi & 1) ? olo : 0u));
+                            const int li = (gi == i0) ? (int)l0 : ((gi == i1) ? (int)(l0 | olo) : -1);
+                            const int o = li >= 0 ? 2 * (int)swz((unsigned)li) + gpart : 0;
+                            if constexpr (REV) {
+                                const double k = li >= 0 ? d0[o] : 0.0;
+                                dmma(cD0, cD1, li >= 0 ? d1[o] : 0.0, k);
+                                if constexpr (HH) dmma(cH0, cH1, li >= 0 ? d2[o] : 0.0, k);
+                            } else {
+                                dmma(cH0, cH1, li >= 0 ? d1[o] : 0.0, li >= 0 ? d2[o] : 0.0);
+                            }
                         }
-                        const int o = li >= 0 ? 2 * (int)swz((unsigned)li) + gpart : 0;
-                        if constexpr (REV) {
-                            const double k = li >= 0 ? d0[o] : 0.0;  // ket = psi_l
-                            dmma(cD0, cD1, li >= 0 ? d1[o] : 0.0, k);
-                            if constexpr (HH) dmma(cH0, cH1, li >= 0 ? d2[o] : 0.0, k);
-                        } else {
-                            // ASC: bra = new bra, ket = v
-                            dmma(cH0, cH1, li >= 0 ? d1[o] : 0.0, li >= 0 ? d2[o] : 0.0);
-                        }
+                        __syncwarp();
                     }
-                    __syncwarp();
-                }
-                // ---- step 3
-                if constexpr (OP != OP_FWD && OP != OP_FWD_DOT) {
-                    for (unsigned j = lane; c1q && j < TW; j += 32) {
-                        const unsigned tau = warp * TW + j;
-                        {
-                            const unsigned l0r = ins0u(tau, llo), l0 = swz(l0r), l1 = swz(l0r | olo);
+                    if constexpr (OP != OP_FWD && OP != OP_FWD_DOT) {
+                        for (unsigned j = lane; j < TW; j += 32) {
+                            const unsigned l0r = ins0u(wbase + j, llo), l0 = swz(l0r), l1 = swz(l0r | olo);
                             const int P = (tpop + __popc(l0r)) & 1 ^ p.sector;
                             if constexpr (REV) {
                                 double2 b[2] = {t1[l0], t1[l1]}, bn[2];
@@ -428,33 +404,89 @@ __global__ void __launch_bounds__(FT, 2) k_fused(const FusedParams p)
                             }
                         }
                     }
-                    if (!c1q) {
+                } else {
+                    // ---- two-qubit slot, all FP64 math on the tensor cores (DMMA m8n8k4).
+                    // Tuple -> swizzled tile index is GF(2)-linear (bit insertion +
+                    // XOR swizzle), so every address is an XOR of precomputed columns.
+                    auto F = [&](unsigned x) { return swz(ins0u(ins0u(x, llo), lhi)); };
+                    const unsigned offA = swz(((tq & 2) ? ohi : 0u) | ((tq & 1) ? olo : 0u));
+                    const unsigned baseA = F(wbase + g) ^ offA;  // gate layout: lane (g, tq) = amp tq of tuple g
+                    const unsigned ngrp = TW >> 3;                // groups of 8 tuples (TW >= 8 here when m >= 7)
+                    unsigned colA[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) colA[i] = F(8u << i);
+                    auto addrA = [&](unsigned grp) {
+                        unsigned a = baseA;
+#pragma unroll
+                        for (int i = 0; i < 4; ++i)
+                            if ((grp >> i) & 1u) a ^= colA[i];
+                        return a;
+                    };
+                    double2 *V = (OP == OP_ASC_H) ? t1 : t0;
+                    {
+                        double fa0, fa1;
+                        gate_frag(MA, g, tq, fa0, fa1);
+#pragma unroll 4
+                        for (unsigned grp = 0; grp < ngrp; ++grp) {
+                            const unsigned ad = addrA(grp);
+                            V[ad] = dmma_mv(V[ad], fa0, fa1);
+                        }
+                    }
+                    if constexpr (HD || HH) {
+                        __syncwarp();
+                        // hole layout: lane (g, tq) = component g (amp g&3, part g>>2) of tuple tq
+                        const unsigned offH = swz(((gi & 2) ? ohi : 0u) | ((gi & 1) ? olo : 0u));
+                        const unsigned baseH = F(wbase + tq) ^ offH;
+                        unsigned colH[5];
+#pragma unroll
+                        for (int i = 0; i < 5; ++i) colH[i] = F(4u << i);
+                        const double *d0 = reinterpret_cast<const double *>(t0) + gpart;
+                        const double *d1 = reinterpret_cast<const double *>(t1) + gpart;
+                        const double *d2 = reinterpret_cast<const double *>(t2) + gpart;
+                        double eD0 = 0.0, eD1 = 0.0, eH0 = 0.0, eH1 = 0.0;  // second accumulators (ILP)
+                        const unsigned nq = TW >> 2;
+#pragma unroll 2
+                        for (unsigned q = 0; q < nq; q += 2) {
+                            unsigned a0 = baseH;
+#pragma unroll
+                            for (int i = 1; i < 5; ++i)
+                                if ((q >> i) & 1u) a0 ^= colH[i];
+                            const unsigned a1 = a0 ^ colH[0];
+                            const unsigned o0 = 2 * a0, o1 = 2 * a1;
+                            if constexpr (REV) {
+                                const double k0 = d0[o0], k1 = d0[o1];
+                                dmma(cD0, cD1, d1[o0], k0);
+                                dmma(eD0, eD1, d1[o1], k1);
+                                if constexpr (HH) {
+                                    dmma(cH0, cH1, d2[o0], k0);
+                                    dmma(eH0, eH1, d2[o1], k1);
+                                }
+                            } else {
+                                dmma(cH0, cH1, d1[o0], d2[o0]);
+                                dmma(eH0, eH1, d1[o1], d2[o1]);
+                            }
+                        }
+                        cD0 += eD0;
+                        cD1 += eD1;
+                        cH0 += eH0;
+                        cH1 += eH1;
+                        __syncwarp();
+                    }
+                    if constexpr (OP != OP_FWD && OP != OP_FWD_DOT) {
                         double fb0, fb1, fc0 = 0.0, fc1 = 0.0;
                         gate_frag(MB, g, tq, fb0, fb1);
                         if constexpr (OP == OP_REV_GH || OP == OP_ASC_H) gate_frag(MC, g, tq, fc0, fc1);
-                        const unsigned offt = ((tq & 2) ? ohi : 0u) + ((tq & 1) ? olo : 0u);
-                        for (unsigned grp = 0; grp < (TW + 7) / 8; ++grp) {
-                            const unsigned j = grp * 8 + g;
-                            const bool ok = j < TW;
-                            const unsigned addr = swz(ins0u(ins0u(warp * TW + (ok ? j : 0), llo), lhi) + offt);
+#pragma unroll 4
+                        for (unsigned grp = 0; grp < ngrp; ++grp) {
+                            const unsigned ad = addrA(grp);
                             if constexpr (REV) {
-                                const double2 bb = ok ? t1[addr] : czero();
-                                if constexpr (OP == OP_REV_GH) {
-                                    const double2 cc = ok ? t2[addr] : czero();
-                                    const double2 cn = dmma_mv2(cc, fb0, fb1, bb, fc0, fc1);
-                                    if (ok) t2[addr] = cn;
-                                }
-                                const double2 bn = dmma_mv(bb, fb0, fb1);
-                                if (ok) t1[addr] = bn;
+                                const double2 bb = t1[ad];
+                                if constexpr (OP == OP_REV_GH) t2[ad] = dmma_mv2(t2[ad], fb0, fb1, bb, fc0, fc1);
+                                t1[ad] = dmma_mv(bb, fb0, fb1);
                             } else {
-                                const double2 x = ok ? t0[addr] : czero();
-                                const double2 v = ok ? t2[addr] : czero();
-                                const double2 vn = dmma_mv2(v, fb0, fb1, x, fc0, fc1);
-                                const double2 y = dmma_mv(x, fb0, fb1);
-                                if (ok) {
-                                    t2[addr] = vn;
-                                    t0[addr] = y;
-                                }
+                                const double2 x = t0[ad];
+                                t2[ad] = dmma_mv2(t2[ad], fb0, fb1, x, fc0, fc1);
+                                t0[ad] = dmma_mv(x, fb0, fb1);
                             }
                         }
                     }
@@ -476,13 +508,13 @@ __global__ void __launch_bounds__(FT, 2) k_fused(const FusedParams p)
                     const int hole = tid >> 5;
                     if ((hole == 0 && HD) || (hole == 1 && HH)) {
                         const int i = tid & 31, e = i >> 1, part = i & 1, ii = e >> 2, jj = e & 3;
-                        double s = 0.0;
+                        double sum = 0.0;
                         for (unsigned ww = 0; ww < nwa; ++ww) {
                             const double *C = scratch + (hole * 8 + ww) * 64;
-                            s += part == 0 ? (C[ii * 8 + jj] - C[(4 + ii) * 8 + 4 + jj])
-                                           : (C[ii * 8 + 4 + jj] + C[(4 + ii) * 8 + jj]);
+                            sum += part == 0 ? (C[ii * 8 + jj] - C[(4 + ii) * 8 + 4 + jj])
+                                             : (C[ii * 8 + 4 + jj] + C[(4 + ii) * 8 + jj]);
                         }
-                        sacc[(si * 2 + hole) * 32 + i] += s;
+                        sacc[(si * 2 + hole) * 32 + i] += sum;
                     }
                 }
             }
@@ -786,7 +818,7 @@ extern "C" int gf_plan_create(gf_plan **out, int k, int sector, int n_slots, con
         p->fused = p->K >= 6 && !(eng && strcmp(eng, "stream") == 0);
         const char *fmenv = getenv("GF_FUSED_M");
         int fm = fmenv ? atoi(fmenv) : 11;
-        p->fm = std::max(4, std::min(std::min(fm, FMAXM), p->K));
+        p->fm = std::max(5, std::min(std::min(fm, FMAXM), p->K));
         p->fc = std::min(4, p->fm);
         if (p->fused) {
             p->fwd_passes = plan_passes(p, false);
