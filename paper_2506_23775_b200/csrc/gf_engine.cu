@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(kThreads) k_sweep(const SweepParams p)
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
 {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                  : "+d"(c0), "+d"(c1)
                  : "d"(a), "d"(b));
 }
