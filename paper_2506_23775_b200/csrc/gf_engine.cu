@@ -228,7 +228,7 @@ __device__ __forceinline__ unsigned ins0u(unsigned t, int b)
 // land in different banks (ncu: half the smem wavefronts were conflicts).
 __device__ __forceinline__ unsigned swz(unsigned l)
 {
-    return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7u);
+    return l ^ (((l >> 3) ^ (l >> 5) ^ (l >> 7) ^ (l >> 9)) & 7u);
 }
 
 // B fragment (two k-steps) of the real 8x8 form of a complex 4x4 gate for
@@ -299,7 +299,8 @@ __global__ void __launch_bounds__(FT, 2) k_fused(const FusedParams p)
     double vre = 0.0, vim = 0.0;
     const unsigned cmask = (1u << c) - 1u;
     const int g = lane >> 2, tq = lane & 3;
-    const int gi = g & 3, gpart = g >> 2;
+    // hole operand rows: component g = 2*amp + part (re/im of one amplitude adjacent)
+    const int gi = g >> 1, gpart = g & 1;
 
     for (u64 tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
         u64 base = 0;
@@ -511,8 +512,8 @@ __global__ void __launch_bounds__(FT, 2) k_fused(const FusedParams p)
                         double sum = 0.0;
                         for (unsigned ww = 0; ww < nwa; ++ww) {
                             const double *C = scratch + (hole * 8 + ww) * 64;
-                            sum += part == 0 ? (C[ii * 8 + jj] - C[(4 + ii) * 8 + 4 + jj])
-                                             : (C[ii * 8 + 4 + jj] + C[(4 + ii) * 8 + jj]);
+                            sum += part == 0 ? (C[(2 * ii) * 8 + 2 * jj] - C[(2 * ii + 1) * 8 + 2 * jj + 1])
+                                             : (C[(2 * ii) * 8 + 2 * jj + 1] + C[(2 * ii + 1) * 8 + 2 * jj]);
                         }
                         sacc[(si * 2 + hole) * 32 + i] += sum;
                     }
