@@ -167,6 +167,11 @@ int gf_cheb_step(const void *t_cur, const void *t_prev, void *t_next, void *acc,
                  const int32_t *tb, const double *coef, const int32_t *hop, int nterms, double scale, double shift,
                  double c_re, double c_im, int64_t nvec, int sector_flags, void *stream);
 
+/* Measurement helper (bench.py roofline): back-to-back FP64 work on all SMs.
+ * which = 0: DMMA m8n8k4 (FP64 tensor cores), 1: DFMA.  *flops receives the
+ * flop count of the launch; time it with events on `stream`. */
+int gf_peak_fp64(int which, int blocks, int iters, double *sink_dev, double *flops, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

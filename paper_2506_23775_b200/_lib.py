@@ -40,6 +40,7 @@ EXPORTS = (
     "gf_plan_destroy",
     "gf_cheb_step",
     "gf_hamiltonian_apply",
+    "gf_peak_fp64",
 )
 
 if not os.path.exists(LIB_PATH):
@@ -79,6 +80,7 @@ for _name, _args in {
     "gf_cheb_step": [_vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _i, ctypes.c_double, ctypes.c_double,
                      ctypes.c_double, ctypes.c_double, _i64, _i, _vp],
     "gf_hamiltonian_apply": [_vp, _vp, _i, _vp, _vp, _vp, _vp, _i, _i64, _vp],
+    "gf_peak_fp64": [_i, _i, _i, _vp, _vp, _vp],
 }.items():
     getattr(lib, _name).argtypes = _args
     getattr(lib, _name).restype = _i

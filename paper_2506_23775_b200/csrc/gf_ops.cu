@@ -551,3 +551,62 @@ extern "C" int gf_sector_orbit_mark(int64_t i0, int64_t m, int L, int sector, in
     GF_CUDA(cudaGetLastError());
     return GF_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Peak microbenchmarks (measurement helpers for bench.py's roofline: neither
+// MEASURED_PEAKS.json nor the profiling recipe states an FP64 peak).
+// 8 independent accumulator chains per thread, back to back.
+// ---------------------------------------------------------------------------
+namespace gf {
+__global__ void __launch_bounds__(256) k_peak_dmma(double *sink, int iters)
+{
+    double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - blockIdx.x * 1e-9;
+    double c[8][2];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) c[j][0] = c[j][1] = 0.0;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                : "+d"(c[j][0]), "+d"(c[j][1])
+                : "d"(a), "d"(b));
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += c[j][0] + c[j][1];
+    if (s == -1.0) sink[0] = s;
+}
+
+__global__ void __launch_bounds__(256) k_peak_dfma(double *sink, int iters)
+{
+    double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - blockIdx.x * 1e-9;
+    double c[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) c[j] = j;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) c[j] = fma(c[j], a, b);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += c[j];
+    if (s == -1.0) sink[0] = s;
+}
+}  // namespace gf
+
+// which: 0 = DMMA m8n8k4 (512 flop per warp instruction), 1 = DFMA (2 flop
+// per thread instruction).  Returns the flop count of the launch in *flops.
+extern "C" int gf_peak_fp64(int which, int blocks, int iters, double *sink_dev, double *flops, void *stream)
+{
+    if (!sink_dev || !flops || blocks < 1 || iters < 1) return gf_fail(GF_EINVAL, "bad arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (which == 0) {
+        k_peak_dmma<<<blocks, 256, 0, st>>>(sink_dev, iters);
+        *flops = (double)blocks * 8 /*warps*/ * iters * 8 * 512.0;
+    } else {
+        k_peak_dfma<<<blocks, 256, 0, st>>>(sink_dev, iters);
+        *flops = (double)blocks * 256 * iters * 8 * 2.0;
+    }
+    GF_CUDA(cudaGetLastError());
+    return GF_OK;
+}
