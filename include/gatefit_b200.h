@@ -167,6 +167,15 @@ int gf_cheb_step(const void *t_cur, const void *t_prev, void *t_next, void *acc,
                  const int32_t *tb, const double *coef, const int32_t *hop, int nterms, double scale, double shift,
                  double c_re, double c_im, int64_t nvec, int sector_flags, void *stream);
 
+/* Device-memory helpers for bindings without a tensor library (the ctypes
+ * stub of INTEGRATION.md).  gf_memcpy kind: 0 = H2D, 1 = D2H, 2 = D2D
+ * (asynchronous on `stream`; pair with gf_stream_sync). */
+int gf_set_device(int device);
+int gf_malloc(void **ptr, int64_t bytes);
+int gf_free(void *ptr);
+int gf_memcpy(void *dst, const void *src, int64_t bytes, int kind, void *stream);
+int gf_stream_sync(void *stream);
+
 /* Measurement helper (bench.py roofline): back-to-back FP64 work on all SMs.
  * which = 0: DMMA m8n8k4 (FP64 tensor cores), 1: DFMA.  *flops receives the
  * flop count of the launch; time it with events on `stream`. */

@@ -41,6 +41,11 @@ EXPORTS = (
     "gf_cheb_step",
     "gf_hamiltonian_apply",
     "gf_peak_fp64",
+    "gf_set_device",
+    "gf_malloc",
+    "gf_free",
+    "gf_memcpy",
+    "gf_stream_sync",
 )
 
 if not os.path.exists(LIB_PATH):
@@ -81,6 +86,11 @@ for _name, _args in {
                      ctypes.c_double, ctypes.c_double, _i64, _i, _vp],
     "gf_hamiltonian_apply": [_vp, _vp, _i, _vp, _vp, _vp, _vp, _i, _i64, _vp],
     "gf_peak_fp64": [_i, _i, _i, _vp, _vp, _vp],
+    "gf_set_device": [_i],
+    "gf_malloc": [ctypes.POINTER(_vp), _i64],
+    "gf_free": [_vp],
+    "gf_memcpy": [_vp, _vp, _i64, _i, _vp],
+    "gf_stream_sync": [_vp],
 }.items():
     getattr(lib, _name).argtypes = _args
     getattr(lib, _name).restype = _i

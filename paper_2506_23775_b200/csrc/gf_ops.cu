@@ -610,3 +610,45 @@ extern "C" int gf_peak_fp64(int which, int blocks, int iters, double *sink_dev, 
     GF_CUDA(cudaGetLastError());
     return GF_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Minimal device-memory helpers so a binding without a tensor library (e.g.
+// a ctypes stub inside the reference's objective.py) can drive the ABI.
+// ---------------------------------------------------------------------------
+extern "C" int gf_set_device(int device)
+{
+    GF_CUDA(cudaSetDevice(device));
+    return GF_OK;
+}
+
+extern "C" int gf_malloc(void **ptr, int64_t bytes)
+{
+    if (!ptr || bytes < 0) return gf_fail(GF_EINVAL, "bad arguments");
+    *ptr = nullptr;
+    if (bytes == 0) return GF_OK;
+    GF_CUDA(cudaMalloc(ptr, (size_t)bytes));
+    return GF_OK;
+}
+
+extern "C" int gf_free(void *ptr)
+{
+    if (ptr) GF_CUDA(cudaFree(ptr));
+    return GF_OK;
+}
+
+extern "C" int gf_memcpy(void *dst, const void *src, int64_t bytes, int kind, void *stream)
+{
+    // kind: 0 host->device, 1 device->host, 2 device->device
+    if (bytes < 0 || kind < 0 || kind > 2) return gf_fail(GF_EINVAL, "bad arguments");
+    if (bytes == 0) return GF_OK;
+    const cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice
+                                       : (kind == 1 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice);
+    GF_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, k, (cudaStream_t)stream));
+    return GF_OK;
+}
+
+extern "C" int gf_stream_sync(void *stream)
+{
+    GF_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    return GF_OK;
+}

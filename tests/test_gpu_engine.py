@@ -379,3 +379,32 @@ def test_multi_tile_multi_pass_engine_vs_oracle(monkeypatch, engine, m):
         assert abs(rep.value + v.real) < TOL * max(1, abs(v))
         assert rel_err(np.stack(rep.holomorphic_derivatives), hol) < TOL
         assert rel_err(np.stack(hv), hvo) < TOL
+
+
+def test_integration_stub_matches_reference_chunk_drivers():
+    """pure-ctypes stub (gf_malloc / gf_memcpy /
+    gf_plan_eval / gf_plan_slot_outputs) returns the reference drivers'
+    per-slot dacc / oacc for a chunk."""
+    import integration_stub as S
+
+    g = golden("c1")
+    spec, circ, rng = gf.spinful_layer_circuit(4, 3, False, seed=0)
+    orc = gf.DenseOracle(spec, 0.25)
+    ev = S.GpuChunkEvaluator(circ, max_chunk=64)
+    ev.set_directions(g["direction"])
+    t1, t2, lid = circ.slot_arrays()
+    plan = O.Plan(8, np.stack([t1, t2], 1), lid, circ.gate_stack())
+    phi = O.dense_phi0(orc._u)
+    vals, dsum, hsum = 0j, 0, 0
+    for j0 in range(0, 256, 64):
+        phi0s = phi(np.arange(j0, j0 + 64))
+        v, dacc, oacc = ev(S.GF_VALUE | S.GF_GRAD | S.GF_HVP, j0, j0 + 64, phi0s)
+        ov, od, _ = O.gradient_sum(plan, np.arange(j0, j0 + 64), phi)
+        oh, _ = O.hvp_sum(plan, list(g["direction"]), np.arange(j0, j0 + 64), phi)
+        assert abs(v - ov) < TOL * max(1, abs(ov))
+        assert rel_err(dacc.reshape(-1, 16), od) < TOL
+        assert rel_err(oacc.reshape(-1, 16), oh) < TOL
+        vals += v
+        dsum = dsum + dacc
+    assert abs(-vals.real - g["value"]) < TOL * abs(g["value"])
+    assert rel_err(plan.logical_sum(dsum.reshape(-1, 16)), g["holo"]) < TOL
