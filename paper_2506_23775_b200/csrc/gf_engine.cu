@@ -827,7 +827,9 @@ extern "C" int gf_plan_create(gf_plan **out, int k, int sector, int n_slots, con
             p->asc_passes.assign(p->rev_passes.rbegin(), p->rev_passes.rend());
             for (auto &f : p->asc_passes) std::reverse(f.ps, f.ps + f.nslots);
             u64 ntiles = 1ull << (p->K - p->fm);
-            p->ctas = (int)std::max<u64>(1, std::min<u64>((u64)p->ctas, ntiles));
+            const char *cenv = getenv("GF_FUSED_CTAS");
+            u64 want = cenv ? (u64)atoll(cenv) : (u64)p->ctas;
+            p->ctas = (int)std::max<u64>(1, std::min<u64>(want, ntiles));
         }
     }
     // workspace
@@ -992,7 +994,7 @@ static int launch_fused(const gf_plan *p, FusedParams &fp, int64_t nvec, cudaStr
     const size_t smem = fused_smem(nv, fp.m, fp.c);
     static bool attr_done = false;
     if (!attr_done) {
-        cudaFuncSetAttribute(k_fused<OP, FIRST>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_fused<OP, FIRST>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         attr_done = true;
     }
     dim3 grid(p->ctas, (unsigned)nvec);
