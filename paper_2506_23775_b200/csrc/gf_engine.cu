@@ -307,9 +307,14 @@ __global__ void __launch_bounds__(FT, 2) k_fused(const FusedParams p)
         for (int i = 0; i < p.nglob; ++i)
             if ((tile >> i) & 1ull) base |= 1ull << p.gpos[i];
         const int tpop = __popcll(tile);
+        const u64 jb = (OP == OP_FWD || OP == OP_FWD_DOT) && FIRST ? (u64)p.basis[blockIdx.y] : 0ull;
         for (unsigned l = tid; l < T; l += FT) {
             const u64 a = base + (l & cmask) + hiofs[l >> c];
-            const double2 x = psi[a];
+            double2 x;
+            if constexpr ((OP == OP_FWD || OP == OP_FWD_DOT) && FIRST)
+                x = make_double2(a == jb ? 1.0 : 0.0, 0.0);  // psi_0 = |j>, no HBM read
+            else
+                x = psi[a];
             t0[swz(l)] = x;
             if constexpr (NV >= 2) {
                 double2 b;
@@ -562,6 +567,38 @@ __global__ void __launch_bounds__(FT, 2) k_fused(const FusedParams p)
             p.partV[((u64)blockIdx.y * p.ctas + blockIdx.x) * 2 + tid] = s;
         }
     }
+    // The last CTA of this vector sums the per-CTA partials in ascending CTA
+    // order (deterministic whichever CTA arrives last) -- no separate
+    // reduction launch.
+    __threadfence();
+    __syncthreads();
+    __shared__ unsigned s_last;
+    if (tid == 0) s_last = (atomicAdd(&p.tickets[blockIdx.y], 1u) == (unsigned)p.ctas - 1u);
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
+        const u64 b = blockIdx.y;
+        for (int i = tid; i < p.nslots * 64; i += FT) {
+            const int si = i >> 6, hole = (i >> 5) & 1, e = i & 31;
+            if ((hole == 0 && HD) || (hole == 1 && HH)) {
+                const double *src = hole == 0 ? p.partD : p.partH;
+                double *dst = hole == 0 ? p.qD : p.qH;
+                const u64 slot = (u64)p.ps[si].slot;
+                const double *q = src + ((slot * p.nvec + b) * p.ctas) * 32 + e;
+                double sum = 0.0;
+                for (int cc = 0; cc < p.ctas; ++cc) sum += __ldcg(q + (u64)cc * 32);
+                dst[(slot * p.nvec + b) * 32 + e] = sum;
+            }
+        }
+        if constexpr (HV) {
+            if (tid < 2) {
+                double sum = 0.0;
+                for (int cc = 0; cc < p.ctas; ++cc) sum += __ldcg(p.partV + (b * p.ctas + cc) * 2 + tid);
+                p.qV[b * 2 + tid] = sum;
+            }
+        }
+        if (tid == 0) p.tickets[blockIdx.y] = 0u;
+    }
 }
 
 // |j> for every vector of the batch (basis index per vector).
@@ -587,7 +624,9 @@ __global__ void k_reduce_ctas(const double *part, double *q, int64_t nsb, int ct
     q[i] = acc;
 }
 
-// Chunk records.  rec = [value(2)] [D: nlog*32] [H: nlog*32].
+// Chunk records.  rec = [value(2)] [D: nlog*32] [H: nlog*32].  One warp per
+// record entry: lanes stride over the chunk's summands, then a fixed xor tree
+// (deterministic, independent of batch boundaries since chunks are aligned).
 __global__ void k_chunk_records(const double *qD, const double *qHd, const double *qHa, const double *partV,
                                 int64_t nvec, int ctas, int nslots, int nlog, const int *lstart,
                                 const int *lslots, const int *swapped, int chunk, int flags, int parity_only,
@@ -595,15 +634,16 @@ __global__ void k_chunk_records(const double *qD, const double *qHd, const doubl
 {
     const int rec = 2 + 64 * nlog;
     const int64_t nchunks = (nvec + chunk - 1) / chunk;
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= nchunks * rec) return;
-    const int64_t ch = i / rec;
-    const int r = (int)(i - ch * rec);
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= nchunks * rec) return;
+    const int64_t ch = w / rec;
+    const int r = (int)(w - ch * rec);
     const int64_t b0 = ch * chunk, b1 = (nvec < b0 + chunk) ? nvec : (b0 + chunk);
     double acc = 0.0;
     if (r < 2) {
         if (partV) {
-            for (int64_t b = b0; b < b1; ++b)
+            for (int64_t b = b0 + lane; b < b1; b += 32)
                 for (int c = 0; c < ctas; ++c) acc += partV[(b * ctas + c) * 2 + r];
         }
     } else {
@@ -620,7 +660,7 @@ __global__ void k_chunk_records(const double *qD, const double *qHd, const doubl
         const bool offpat = parity_only && (((ii ^ (ii >> 1)) & 1) != ((jj ^ (jj >> 1)) & 1));
         const bool want = (isH ? (flags & 4) : (flags & 2)) && !offpat;
         if (want) {
-            for (int64_t b = b0; b < b1; ++b)
+            for (int64_t b = b0 + lane; b < b1; b += 32)
                 for (int t = lstart[l]; t < lstart[l + 1]; ++t) {
                     int s = lslots[t];
                     int si = ii, sj = jj;
@@ -634,7 +674,8 @@ __global__ void k_chunk_records(const double *qD, const double *qHd, const doubl
                 }
         }
     }
-    out[i] = acc;
+    acc = warp_sum(acc);
+    if (lane == 0) out[w] = acc;
 }
 
 // per-slot sums over the batch: q[s][b][32] -> out[s][32]
@@ -683,7 +724,8 @@ struct gf_plan {
     bool have_z = false;
     double2 *psi = nullptr, *bra = nullptr, *aux = nullptr;
     double *partD = nullptr, *partHd = nullptr, *partHa = nullptr, *partV = nullptr;
-    double *qD = nullptr, *qHd = nullptr, *qHa = nullptr;
+    double *qD = nullptr, *qHd = nullptr, *qHa = nullptr, *qV = nullptr;
+    unsigned int *tickets = nullptr;
     int *d_lstart = nullptr, *d_lslots = nullptr, *d_swapped = nullptr;
     int64_t last_launches = 0;
     int last_flags = 0;
@@ -757,7 +799,7 @@ static void plan_free(gf_plan *p)
     for (auto &e : p->ev)
         if (e) cudaEventDestroy(e);
     void *ptrs[] = {p->psi, p->bra, p->aux, p->partD, p->partHd, p->partHa, p->partV,
-                    p->qD, p->qHd, p->qHa, p->d_lstart, p->d_lslots, p->d_swapped};
+                    p->qD, p->qHd, p->qHa, p->qV, p->tickets, p->d_lstart, p->d_lslots, p->d_swapped};
     for (void *q : ptrs)
         if (q) cudaFree(q);
 }
@@ -828,7 +870,7 @@ extern "C" int gf_plan_create(gf_plan **out, int k, int sector, int n_slots, con
             for (auto &f : p->asc_passes) std::reverse(f.ps, f.ps + f.nslots);
             u64 ntiles = 1ull << (p->K - p->fm);
             const char *cenv = getenv("GF_FUSED_CTAS");
-            u64 want = cenv ? (u64)atoll(cenv) : (u64)p->ctas;
+            u64 want = cenv ? (u64)atoll(cenv) : (u64)(148 * 8);  // all tiles, up to 8 per SM
             p->ctas = (int)std::max<u64>(1, std::min<u64>(want, ntiles));
         }
     }
@@ -847,6 +889,9 @@ extern "C" int gf_plan_create(gf_plan **out, int k, int sector, int n_slots, con
     if (e == cudaSuccess) e = cudaMalloc(&p->qD, qbytes);
     if (e == cudaSuccess) e = cudaMalloc(&p->qHd, qbytes);
     if (e == cudaSuccess) e = cudaMalloc(&p->qHa, qbytes);
+    if (e == cudaSuccess) e = cudaMalloc(&p->qV, sizeof(double) * 2 * (size_t)max_batch);
+    if (e == cudaSuccess) e = cudaMalloc(&p->tickets, sizeof(unsigned int) * (size_t)max_batch);
+    if (e == cudaSuccess) e = cudaMemset(p->tickets, 0, sizeof(unsigned int) * (size_t)max_batch);
     // logical -> slot CSR
     std::vector<int> lstart(n_logical + 1, 0), lslots, sw(std::max(1, n_slots), 0);
     for (int l = 0; l < n_logical; ++l) {
@@ -1049,7 +1094,7 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
         if (p->pending) collect_phases(p);
         GF_CUDA(cudaEventRecord(p->ev[0], st));
     }
-    {
+    if (!(p->fused && n > 0)) {
         u64 total = p->N * (u64)nvec;
         int blocks = (int)std::min<u64>((total + 255) / 256, 148 * 16);
         k_init_basis<<<blocks, 256, 0, st>>>(p->psi, p->N, basis, nvec);
@@ -1080,6 +1125,9 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
             f.ctas = p->ctas;
             f.sector = p->sector < 0 ? 0 : p->sector;
             f.partV = p->partV;
+            f.qV = p->qV;
+            f.tickets = p->tickets;
+            f.basis = basis;
         };
         const int nf = (int)p->fwd_passes.size(), nr = (int)p->rev_passes.size();
         for (int pi = 0; pi < nf; ++pi) {
@@ -1090,8 +1138,14 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
                 fp.mat[t][0] = p->G[s];
                 if (fp.ps[t].mode != PM_C1Q) fp.ps[t].mode = p->spG[s] ? PM_SPARSE : PM_DENSE;
             }
-            if (!grad_like && pi == nf - 1) launch_fused<OP_FWD_DOT, false>(p, fp, nvec, st);
-            else launch_fused<OP_FWD, false>(p, fp, nvec, st);
+            const bool last = !grad_like && pi == nf - 1;
+            if (pi == 0) {
+                if (last) launch_fused<OP_FWD_DOT, true>(p, fp, nvec, st);
+                else launch_fused<OP_FWD, true>(p, fp, nvec, st);
+            } else {
+                if (last) launch_fused<OP_FWD_DOT, false>(p, fp, nvec, st);
+                else launch_fused<OP_FWD, false>(p, fp, nvec, st);
+            }
             ++launches;
         }
         l_fwd = launches;
@@ -1103,6 +1157,8 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
                 setup(fp);
                 fp.partD = p->partD;
                 fp.partH = p->partHd;
+                fp.qD = p->qD;
+                fp.qH = p->qHd;
                 for (int t = 0; t < fp.nslots; ++t) {
                     const int s = fp.ps[t].slot;
                     fp.mat[t][0] = p->Gd[s];
@@ -1127,6 +1183,7 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
                     fp = p->asc_passes[pi];
                     setup(fp);
                     fp.partH = p->partHa;
+                    fp.qH = p->qHa;
                     for (int t = 0; t < fp.nslots; ++t) {
                         const int s = fp.ps[t].slot;
                         fp.mat[t][0] = p->Gc[s];
@@ -1203,7 +1260,7 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
     if (!(grad_like && n > 0) && p->profiling) GF_CUDA(cudaEventRecord(p->ev[2], st));
     l_asc = launches - l_fwd - l_rev;
     if (p->profiling) GF_CUDA(cudaEventRecord(p->ev[3], st));
-    if (grad_like && n > 0) {
+    if (grad_like && n > 0 && !p->fused) {
         int64_t nsb = (int64_t)n * nvec;
         int blocks = (int)((nsb * 32 + 255) / 256);
         k_reduce_ctas<<<blocks, 256, 0, st>>>(p->partD, p->qD, nsb, p->ctas);
@@ -1219,9 +1276,10 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
         int rec = 2 + 64 * p->nlog;
         int64_t tot = nchunks * rec;
         int eff = (n > 0) ? flags : (flags & GF_VALUE);
-        k_chunk_records<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
-            p->qD, p->qHd, p->qHa, p->partV, nvec, p->ctas, n, p->nlog, p->d_lstart, p->d_lslots, p->d_swapped,
-            p->chunk, eff, p->sector >= 0, out);
+        const bool fusedV = p->fused && n > 0;
+        k_chunk_records<<<(unsigned)((tot * 32 + 255) / 256), 256, 0, st>>>(
+            p->qD, p->qHd, p->qHa, fusedV ? p->qV : p->partV, nvec, fusedV ? 1 : p->ctas, n, p->nlog, p->d_lstart,
+            p->d_lslots, p->d_swapped, p->chunk, eff, p->sector >= 0, out);
         ++launches;
     }
     if (p->profiling) {

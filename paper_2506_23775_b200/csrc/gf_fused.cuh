@@ -36,7 +36,10 @@ struct FusedParams {
     double2 *psi, *bra, *aux;  // [nvec][N]
     const double2 *phi0;       // [nvec][N]
     const double *weights;     // [nvec] or null
+    const int64_t *basis;      // [nvec] (first forward pass synthesises |j>)
     double *partD, *partH, *partV;
+    double *qD, *qH, *qV;    // per-(slot, vector) sums written by the last CTA of each vector
+    unsigned int *tickets;   // [nvec] arrival counters, self-resetting
     unsigned long long N;
     unsigned long long ntiles;  // 2^(K-m)
     int nvec, ctas, sector;
