@@ -1039,9 +1039,13 @@ static int launch_fused(const gf_plan *p, FusedParams &fp, int64_t nvec, cudaStr
     const size_t smem = fused_smem(nv, fp.m, fp.c);
     static bool attr_done = false;
     if (!attr_done) {
-        cudaFuncSetAttribute(k_fused<OP, FIRST>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        // 226 KB: the opt-in limit (227 KB) minus the kernel's static shared memory
+        cudaError_t ae = cudaFuncSetAttribute(k_fused<OP, FIRST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              226 * 1024);
+        if (ae != cudaSuccess) return gf_fail(GF_ECUDA, "k_fused smem attribute: %s", cudaGetErrorString(ae));
         attr_done = true;
     }
+    if (smem > 226 * 1024) return gf_fail(GF_EINVAL, "fused tile needs %zu B of shared memory", smem);
     dim3 grid(p->ctas, (unsigned)nvec);
     k_fused<OP, FIRST><<<grid, FT, smem, st>>>(fp);
     return GF_OK;
@@ -1140,11 +1144,11 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
             }
             const bool last = !grad_like && pi == nf - 1;
             if (pi == 0) {
-                if (last) launch_fused<OP_FWD_DOT, true>(p, fp, nvec, st);
-                else launch_fused<OP_FWD, true>(p, fp, nvec, st);
+                if (last) { int rc_ = launch_fused<OP_FWD_DOT, true>(p, fp, nvec, st) if (rc_) return rc_; }
+                else { int rc_ = launch_fused<OP_FWD, true>(p, fp, nvec, st) if (rc_) return rc_; }
             } else {
-                if (last) launch_fused<OP_FWD_DOT, false>(p, fp, nvec, st);
-                else launch_fused<OP_FWD, false>(p, fp, nvec, st);
+                if (last) { int rc_ = launch_fused<OP_FWD_DOT, false>(p, fp, nvec, st) if (rc_) return rc_; }
+                else { int rc_ = launch_fused<OP_FWD, false>(p, fp, nvec, st) if (rc_) return rc_; }
             }
             ++launches;
         }
@@ -1168,11 +1172,11 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
                     if (fp.ps[t].mode != PM_C1Q) fp.ps[t].mode = sp ? PM_SPARSE : PM_DENSE;
                 }
                 if (h) {
-                    if (pi == 0) launch_fused<OP_REV_GH, true>(p, fp, nvec, st);
-                    else launch_fused<OP_REV_GH, false>(p, fp, nvec, st);
+                    if (pi == 0) { int rc_ = launch_fused<OP_REV_GH, true>(p, fp, nvec, st) if (rc_) return rc_; }
+                    else { int rc_ = launch_fused<OP_REV_GH, false>(p, fp, nvec, st) if (rc_) return rc_; }
                 } else {
-                    if (pi == 0) launch_fused<OP_REV_G, true>(p, fp, nvec, st);
-                    else launch_fused<OP_REV_G, false>(p, fp, nvec, st);
+                    if (pi == 0) { int rc_ = launch_fused<OP_REV_G, true>(p, fp, nvec, st) if (rc_) return rc_; }
+                    else { int rc_ = launch_fused<OP_REV_G, false>(p, fp, nvec, st) if (rc_) return rc_; }
                 }
                 ++launches;
             }
@@ -1192,8 +1196,8 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
                         bool sp = p->spG[s] && p->spZ[s];
                         if (fp.ps[t].mode != PM_C1Q) fp.ps[t].mode = sp ? PM_SPARSE : PM_DENSE;
                     }
-                    if (pi == 0) launch_fused<OP_ASC_H, true>(p, fp, nvec, st);
-                    else launch_fused<OP_ASC_H, false>(p, fp, nvec, st);
+                    if (pi == 0) { int rc_ = launch_fused<OP_ASC_H, true>(p, fp, nvec, st) if (rc_) return rc_; }
+                    else { int rc_ = launch_fused<OP_ASC_H, false>(p, fp, nvec, st) if (rc_) return rc_; }
                     ++launches;
                 }
             }
