@@ -1144,11 +1144,11 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
             }
             const bool last = !grad_like && pi == nf - 1;
             if (pi == 0) {
-                if (last) { int rc_ = launch_fused<OP_FWD_DOT, true>(p, fp, nvec, st) if (rc_) return rc_; }
-                else { int rc_ = launch_fused<OP_FWD, true>(p, fp, nvec, st) if (rc_) return rc_; }
+                if (last) { int rc_ = launch_fused<OP_FWD_DOT, true>(p, fp, nvec, st); if (rc_) return rc_; }
+                else { int rc_ = launch_fused<OP_FWD, true>(p, fp, nvec, st); if (rc_) return rc_; }
             } else {
-                if (last) { int rc_ = launch_fused<OP_FWD_DOT, false>(p, fp, nvec, st) if (rc_) return rc_; }
-                else { int rc_ = launch_fused<OP_FWD, false>(p, fp, nvec, st) if (rc_) return rc_; }
+                if (last) { int rc_ = launch_fused<OP_FWD_DOT, false>(p, fp, nvec, st); if (rc_) return rc_; }
+                else { int rc_ = launch_fused<OP_FWD, false>(p, fp, nvec, st); if (rc_) return rc_; }
             }
             ++launches;
         }
@@ -1172,11 +1172,11 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
                     if (fp.ps[t].mode != PM_C1Q) fp.ps[t].mode = sp ? PM_SPARSE : PM_DENSE;
                 }
                 if (h) {
-                    if (pi == 0) { int rc_ = launch_fused<OP_REV_GH, true>(p, fp, nvec, st) if (rc_) return rc_; }
-                    else { int rc_ = launch_fused<OP_REV_GH, false>(p, fp, nvec, st) if (rc_) return rc_; }
+                    if (pi == 0) { int rc_ = launch_fused<OP_REV_GH, true>(p, fp, nvec, st); if (rc_) return rc_; }
+                    else { int rc_ = launch_fused<OP_REV_GH, false>(p, fp, nvec, st); if (rc_) return rc_; }
                 } else {
-                    if (pi == 0) { int rc_ = launch_fused<OP_REV_G, true>(p, fp, nvec, st) if (rc_) return rc_; }
-                    else { int rc_ = launch_fused<OP_REV_G, false>(p, fp, nvec, st) if (rc_) return rc_; }
+                    if (pi == 0) { int rc_ = launch_fused<OP_REV_G, true>(p, fp, nvec, st); if (rc_) return rc_; }
+                    else { int rc_ = launch_fused<OP_REV_G, false>(p, fp, nvec, st); if (rc_) return rc_; }
                 }
                 ++launches;
             }
@@ -1196,8 +1196,8 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
                         bool sp = p->spG[s] && p->spZ[s];
                         if (fp.ps[t].mode != PM_C1Q) fp.ps[t].mode = sp ? PM_SPARSE : PM_DENSE;
                     }
-                    if (pi == 0) { int rc_ = launch_fused<OP_ASC_H, true>(p, fp, nvec, st) if (rc_) return rc_; }
-                    else { int rc_ = launch_fused<OP_ASC_H, false>(p, fp, nvec, st) if (rc_) return rc_; }
+                    if (pi == 0) { int rc_ = launch_fused<OP_ASC_H, true>(p, fp, nvec, st); if (rc_) return rc_; }
+                    else { int rc_ = launch_fused<OP_ASC_H, false>(p, fp, nvec, st); if (rc_) return rc_; }
                     ++launches;
                 }
             }
