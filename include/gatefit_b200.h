@@ -177,7 +177,7 @@ int gf_memcpy(void *dst, const void *src, int64_t bytes, int kind, void *stream)
 int gf_stream_sync(void *stream);
 
 /* Measurement helper (bench.py roofline): back-to-back FP64 work on all SMs.
- * which = 0: DMMA m8n8k4 (FP64 tensor cores), 1: DFMA.  *flops receives the
+ * which = 0: DMMA m8n8k4 (FP64 tensor cores), 1: DFMA, 2: both interleaved.  *flops receives the
  * flop count of the launch; time it with events on `stream`. */
 int gf_peak_fp64(int which, int blocks, int iters, double *sink_dev, double *flops, void *stream);
 

@@ -10,7 +10,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libgfcuda.so")
+LIB_PATH = os.environ.get("GF_LIB_PATH") or os.path.join(HERE, "libgfcuda.so")
 
 GF_OK, GF_EINVAL, GF_ENONFINITE, GF_ECUDA, GF_ENOMEM = range(5)
 GF_VALUE, GF_GRAD, GF_HVP = 1, 2, 4

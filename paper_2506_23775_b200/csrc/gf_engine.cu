@@ -307,11 +307,13 @@ __global__ void __launch_bounds__(FT, 2) k_fused(const FusedParams p)
         for (int i = 0; i < p.nglob; ++i)
             if ((tile >> i) & 1ull) base |= 1ull << p.gpos[i];
         const int tpop = __popcll(tile);
-        const u64 jb = (OP == OP_FWD || OP == OP_FWD_DOT) && FIRST ? (u64)p.basis[blockIdx.y] : 0ull;
+        // the first forward and first ascending passes start from psi_0 = |j>
+        constexpr bool SYNTH = (OP == OP_FWD || OP == OP_FWD_DOT || OP == OP_ASC_H) && FIRST;
+        const u64 jb = SYNTH ? (u64)p.basis[blockIdx.y] : 0ull;
         for (unsigned l = tid; l < T; l += FT) {
             const u64 a = base + (l & cmask) + hiofs[l >> c];
             double2 x;
-            if constexpr ((OP == OP_FWD || OP == OP_FWD_DOT) && FIRST)
+            if constexpr (SYNTH)
                 x = make_double2(a == jb ? 1.0 : 0.0, 0.0);  // psi_0 = |j>, no HBM read
             else
                 x = psi[a];
@@ -432,7 +434,7 @@ __global__ void __launch_bounds__(FT, 2) k_fused(const FusedParams p)
                     {
                         double fa0, fa1;
                         gate_frag(MA, g, tq, fa0, fa1);
-#pragma unroll 4
+#pragma unroll 8
                         for (unsigned grp = 0; grp < ngrp; ++grp) {
                             const unsigned ad = addrA(grp);
                             V[ad] = dmma_mv(V[ad], fa0, fa1);
@@ -451,7 +453,7 @@ __global__ void __launch_bounds__(FT, 2) k_fused(const FusedParams p)
                         const double *d2 = reinterpret_cast<const double *>(t2) + gpart;
                         double eD0 = 0.0, eD1 = 0.0, eH0 = 0.0, eH1 = 0.0;  // second accumulators (ILP)
                         const unsigned nq = TW >> 2;
-#pragma unroll 2
+#pragma unroll 4
                         for (unsigned q = 0; q < nq; q += 2) {
                             unsigned a0 = baseH;
 #pragma unroll
@@ -482,7 +484,7 @@ __global__ void __launch_bounds__(FT, 2) k_fused(const FusedParams p)
                         double fb0, fb1, fc0 = 0.0, fc1 = 0.0;
                         gate_frag(MB, g, tq, fb0, fb1);
                         if constexpr (OP == OP_REV_GH || OP == OP_ASC_H) gate_frag(MC, g, tq, fc0, fc1);
-#pragma unroll 4
+#pragma unroll 8
                         for (unsigned grp = 0; grp < ngrp; ++grp) {
                             const unsigned ad = addrA(grp);
                             if constexpr (REV) {
@@ -527,12 +529,13 @@ __global__ void __launch_bounds__(FT, 2) k_fused(const FusedParams p)
             __syncthreads();
         }
 
+        const int sm = p.store_mask;
         for (unsigned l = tid; l < T; l += FT) {
             const u64 a = base + (l & cmask) + hiofs[l >> c];
             const double2 x = t0[swz(l)];
-            psi[a] = x;
-            if constexpr (NV >= 2) bra[a] = t1[swz(l)];
-            if constexpr (NV >= 3) aux[a] = t2[swz(l)];
+            if (sm & 1) psi[a] = x;
+            if constexpr (NV >= 2) if (sm & 2) bra[a] = t1[swz(l)];
+            if constexpr (NV >= 3) if (sm & 4) aux[a] = t2[swz(l)];
             if constexpr (OP == OP_FWD_DOT) {
                 const double2 f = cscale(phi0[a], w);
                 vre = fma(f.x, x.x, vre);
@@ -1118,6 +1121,7 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
     }
     if (p->fused && n > 0) {
         FusedParams fp;
+        static const bool exp_noslots = getenv("GF_EXP_NOSLOTS") != nullptr;  // timing diagnostic only
         auto setup = [&](FusedParams &f) {
             f.psi = p->psi;
             f.bra = p->bra;
@@ -1132,6 +1136,8 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
             f.qV = p->qV;
             f.tickets = p->tickets;
             f.basis = basis;
+            f.store_mask = 7;
+            if (exp_noslots) f.nslots = 0;
         };
         const int nf = (int)p->fwd_passes.size(), nr = (int)p->rev_passes.size();
         for (int pi = 0; pi < nf; ++pi) {
@@ -1144,6 +1150,7 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
             }
             const bool last = !grad_like && pi == nf - 1;
             if (pi == 0) {
+                if (last) fp.store_mask = 0;  // value only: psi_n is not needed afterwards
                 if (last) { int rc_ = launch_fused<OP_FWD_DOT, true>(p, fp, nvec, st); if (rc_) return rc_; }
                 else { int rc_ = launch_fused<OP_FWD, true>(p, fp, nvec, st); if (rc_) return rc_; }
             } else {
@@ -1171,6 +1178,9 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
                     bool sp = p->spG[s] && (!h || p->spZ[s]);
                     if (fp.ps[t].mode != PM_C1Q) fp.ps[t].mode = sp ? PM_SPARSE : PM_DENSE;
                 }
+                // after the reverse sweep psi_0 = |j> is known exactly and chi is dead:
+                // the last pass writes back only the bra (needed by the ascending sweep)
+                if (pi == nr - 1) fp.store_mask = h ? 2 : 0;
                 if (h) {
                     if (pi == 0) { int rc_ = launch_fused<OP_REV_GH, true>(p, fp, nvec, st); if (rc_) return rc_; }
                     else { int rc_ = launch_fused<OP_REV_GH, false>(p, fp, nvec, st); if (rc_) return rc_; }
@@ -1196,6 +1206,7 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
                         bool sp = p->spG[s] && p->spZ[s];
                         if (fp.ps[t].mode != PM_C1Q) fp.ps[t].mode = sp ? PM_SPARSE : PM_DENSE;
                     }
+                    if (pi == nr - 1) fp.store_mask = 0;  // nothing is read after the ascending sweep
                     if (pi == 0) { int rc_ = launch_fused<OP_ASC_H, true>(p, fp, nvec, st); if (rc_) return rc_; }
                     else { int rc_ = launch_fused<OP_ASC_H, false>(p, fp, nvec, st); if (rc_) return rc_; }
                     ++launches;

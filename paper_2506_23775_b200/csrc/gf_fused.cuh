@@ -44,6 +44,7 @@ struct FusedParams {
     unsigned long long ntiles;  // 2^(K-m)
     int nvec, ctas, sector;
     int m, c, nglob, nslots;
+    int store_mask;  // bit 0 psi, bit 1 bra, bit 2 chi/v: vectors written back after the pass
     int lpos[FMAXM];
     int gpos[FMAXGLOB];
     PassSlot ps[FMAXSLOTS];

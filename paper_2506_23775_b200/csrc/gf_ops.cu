@@ -592,6 +592,27 @@ __global__ void __launch_bounds__(256) k_peak_dfma(double *sink, int iters)
     for (int j = 0; j < 8; ++j) s += c[j];
     if (s == -1.0) sink[0] = s;
 }
+__global__ void __launch_bounds__(256) k_peak_mixed(double *sink, int iters)
+{
+    double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - blockIdx.x * 1e-9;
+    double c[8][2], d[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) c[j][0] = c[j][1] = d[j] = j;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                : "+d"(c[j][0]), "+d"(c[j][1])
+                : "d"(a), "d"(b));
+            d[j] = fma(d[j], a, b);
+            d[j] = fma(d[j], b, a);
+        }
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += c[j][0] + c[j][1] + d[j];
+    if (s == -1.0) sink[0] = s;
+}
 }  // namespace gf
 
 // which: 0 = DMMA m8n8k4 (512 flop per warp instruction), 1 = DFMA (2 flop
@@ -603,9 +624,13 @@ extern "C" int gf_peak_fp64(int which, int blocks, int iters, double *sink_dev, 
     if (which == 0) {
         k_peak_dmma<<<blocks, 256, 0, st>>>(sink_dev, iters);
         *flops = (double)blocks * 8 /*warps*/ * iters * 8 * 512.0;
-    } else {
+    } else if (which == 1) {
         k_peak_dfma<<<blocks, 256, 0, st>>>(sink_dev, iters);
         *flops = (double)blocks * 256 * iters * 8 * 2.0;
+    } else {
+        // 2: DMMA and DFMA interleaved (are the FP64 tensor and FMA pipes independent?)
+        k_peak_mixed<<<blocks, 256, 0, st>>>(sink_dev, iters);
+        *flops = (double)blocks * 8 * iters * 8 * 512.0 + (double)blocks * 256 * iters * 8 * 4.0;
     }
     GF_CUDA(cudaGetLastError());
     return GF_OK;
