@@ -323,6 +323,7 @@ def run_b200(args):
         rep, hv = gf.gradient_and_hvp(circ, cache, X, **kw)
     torch.cuda.synchronize()
     plan = next(iter(obj._PLANS.values()))
+    plan_shape = plan.describe()
     gf._lib.check(gf._lib.lib.gf_plan_set_profiling(plan.h, 1))
 
     stream = torch.cuda.current_stream()
@@ -451,6 +452,7 @@ def run_b200(args):
                 "l2": "inputs larger than L2 (phi0 cache %d MiB per GPU; workspace 3 x batch x 1 MiB)" %
                       ((p1 - p0) * N * 16 >> 20),
                 "oracle_setup_s": round(oracle_setup_s, 3),
+                "engine": plan_shape,
             },
             "roofline": {"bound": "tensor", "kernel": f"k_fused ({dom} sweep: fused tile passes, FP64 DMMA)",
                          "achieved": achieved, "peak": peaks64["dmma_tflops"], "unit": "TFLOP/s",

@@ -975,25 +975,46 @@ static std::vector<FusedParams> plan_passes(const gf_plan *p, bool reverse)
     std::vector<int> remaining;
     for (int i = 0; i < n; ++i) remaining.push_back(reverse ? n - 1 - i : i);
     const int VIRT = 63;
+    // deterministic xorshift for the randomized best-of-N pass search
+    unsigned long long rs = 0x9E3779B97F4A7C15ull;
+    auto rnd = [&]() {
+        rs ^= rs << 13;
+        rs ^= rs >> 7;
+        rs ^= rs << 17;
+        return (double)(rs >> 11) * (1.0 / 9007199254740992.0);
+    };
     while (!remaining.empty()) {
-        unsigned long long S = (1ull << c) - 1ull, blocked = 0ull;
+        unsigned long long S = 0;
         std::vector<int> taken, rest;
-        for (int s : remaining) {
-            const SlotInfo &si = p->slots[s];
-            unsigned long long bits = si.mode_c1q ? (1ull << si.lo) : ((1ull << si.lo) | (1ull << si.hi));
-            unsigned long long dep = bits | (si.mode_c1q ? (1ull << VIRT) : 0ull);
-            if (dep & blocked) {
-                blocked |= dep;
-                rest.push_back(s);
-                continue;
+        // trial 0 is the plain greedy pass; later trials skip eligible slots at
+        // random (keeping their qubits free for later slots) -- keep the trial
+        // that executes the most slots
+        for (int trial = 0; trial < 256; ++trial) {
+            const double skip = trial == 0 ? 0.0 : 0.5 * rnd();
+            unsigned long long S1 = (1ull << c) - 1ull, blocked = 0ull;
+            std::vector<int> t1, r1;
+            for (int s : remaining) {
+                const SlotInfo &si = p->slots[s];
+                unsigned long long bits = si.mode_c1q ? (1ull << si.lo) : ((1ull << si.lo) | (1ull << si.hi));
+                unsigned long long dep = bits | (si.mode_c1q ? (1ull << VIRT) : 0ull);
+                if (dep & blocked) {
+                    blocked |= dep;
+                    r1.push_back(s);
+                    continue;
+                }
+                unsigned long long S2 = S1 | bits;
+                if (__builtin_popcountll(S2) <= m && (int)t1.size() < FMAXSLOTS && !(skip > 0.0 && rnd() < skip)) {
+                    S1 = S2;
+                    t1.push_back(s);
+                } else {
+                    blocked |= dep;
+                    r1.push_back(s);
+                }
             }
-            unsigned long long S2 = S | bits;
-            if (__builtin_popcountll(S2) <= m && (int)taken.size() < FMAXSLOTS) {
-                S = S2;
-                taken.push_back(s);
-            } else {
-                blocked |= dep;
-                rest.push_back(s);
+            if (trial == 0 || t1.size() > taken.size()) {
+                taken = t1;
+                rest = r1;
+                S = S1;
             }
         }
         for (int b = 0; __builtin_popcountll(S) < m && b < K; ++b) S |= 1ull << b;  // pad with low bits
@@ -1369,5 +1390,17 @@ extern "C" int gf_plan_destroy(gf_plan *p)
     if (!p) return GF_OK;
     plan_free(p);
     delete p;
+    return GF_OK;
+}
+
+extern "C" int gf_plan_describe(const gf_plan *p, int *fused, int *tile_bits, int *n_fwd_passes, int *n_rev_passes,
+                                int *ctas)
+{
+    if (!p) return gf_fail(GF_EINVAL, "null plan");
+    if (fused) *fused = p->fused ? 1 : 0;
+    if (tile_bits) *tile_bits = p->fm;
+    if (n_fwd_passes) *n_fwd_passes = (int)p->fwd_passes.size();
+    if (n_rev_passes) *n_rev_passes = (int)p->rev_passes.size();
+    if (ctas) *ctas = p->ctas;
     return GF_OK;
 }

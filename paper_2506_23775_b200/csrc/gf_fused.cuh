@@ -20,7 +20,7 @@ namespace gf {
 
 constexpr int FT = 256;         // threads per fused CTA (8 warps)
 constexpr int FMAXM = 12;       // max local bits
-constexpr int FMAXSLOTS = 12;   // max slots per pass
+constexpr int FMAXSLOTS = 14;   // max slots per pass (2 CTAs/SM of m=11 tiles fit 14)
 constexpr int FMAXGLOB = 40;
 
 enum { PM_DENSE = 0, PM_SPARSE = 1, PM_C1Q = 2 };

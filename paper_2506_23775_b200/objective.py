@@ -213,6 +213,12 @@ class EnginePlan:
                                          None if weights is None else weights.data_ptr(), phi0.data_ptr(),
                                          out.data_ptr(), _lib.stream_ptr()))
 
+    def describe(self) -> dict:
+        v = (ctypes.c_int * 5)()
+        _lib.check(_lib.lib.gf_plan_describe(self.h, ctypes.byref(v, 0), ctypes.byref(v, 4), ctypes.byref(v, 8),
+                                             ctypes.byref(v, 12), ctypes.byref(v, 16)))
+        return {"fused": bool(v[0]), "tile_bits": v[1], "fwd_passes": v[2], "rev_passes": v[3], "ctas": v[4]}
+
     def last_launches(self) -> int:
         return int(_lib.lib.gf_plan_last_launches(self.h))
 
