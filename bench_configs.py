@@ -1,0 +1,147 @@
+#!/usr/bin/env python
+"""Per-config measurements for BASELINE.json configs[0], [2], [3], [4] (the
+driver's bench.py measures configs[1]).  Each config runs its recipe (SURVEY
+Appendix B) on a seeded sample of basis-state summands and reports
+summand-evaluations per second with the extrapolated full-sum time; the target
+oracle is timed separately.  At full size, a size-independent parity property
+is checked: for every slot s, sum_ij G_s[i,j] D_s[i,j] equals the summand sum
+phi0 . C|j> (the reinsertion identity, reference test_kernels.py:114-124 /
+test_objective.py:115-122).
+
+  python bench_configs.py [c1 c3 c4 c5] > profiles/configs_r01.json
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (L, layers, periodic, parity, sector, fold, seed, sample)
+    "c1": (4, 3, False, False, None, False, 0, None),
+    "c3": (12, 7, False, True, 0, False, 2, 64),
+    "c4": (14, 9, True, True, 0, True, 3, 8),
+    "c5": (16, 9, True, True, 0, True, 4, 1),
+}
+
+
+def run(name):
+    import torch
+
+    import paper_2506_23775_b200 as gf
+    from paper_2506_23775_b200 import objective as obj
+
+    L, layers, periodic, parity, sector, fold, seed, sample = CONFIGS[name]
+    torch.cuda.set_device(0)
+    spec, circ, rng = gf.spinful_layer_circuit(L, layers, periodic, seed=seed, parity=parity)
+    X = [gf.manifold.project_tangent_gate(g.matrix, rng.normal(size=(4, 4)) + 1j * rng.normal(size=(4, 4)), parity)
+         for g in circ.logical_gates]
+    k = circ.num_qubits
+    out = {"config": name, "L": L, "qubits": k, "layers": layers, "slots": circ.num_slots,
+           "logical": circ.num_logical, "periodic": periodic, "sector": sector, "fold": fold}
+    if name == "c1":
+        orc = gf.DenseOracle(spec, 0.25)
+        for _ in range(3):
+            gf.gradient_and_hvp(circ, orc, X)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        reps = 20
+        for _ in range(reps):
+            rep, hv = gf.gradient_and_hvp(circ, orc, X)
+        torch.cuda.synchronize()
+        out["full_sum_grad_hvp_s"] = (time.perf_counter() - t0) / reps
+        out["value"] = rep.value
+        t0 = time.perf_counter()
+        final, trace = gf.trust_region_optimize(circ, orc, gf.TrustRegionParams(max_iterations=5))
+        out["trust_region_5_iterations_s"] = time.perf_counter() - t0
+        out["trust_region_f"] = [r.value for r in trace.records]
+        out["reference_cpu_s_survey"] = {"grad": 0.022, "hvp": 0.0317, "tr5": 2.72}
+        return out
+    sect_size = 1 << (k - 1)
+    srng = np.random.default_rng(seed + 1)
+    idx = np.unique(srng.integers(0, sect_size, size=sample))
+    weights = None
+    if fold:
+        # canonicalise the sample to orbit representatives with orbit-size weights
+        x = torch.from_numpy(idx).cuda()
+        full = torch.empty_like(x)
+        gf._lib.check(gf._lib.lib.gf_sector_unrank(x.data_ptr(), x.numel(), 0, full.data_ptr(), gf._lib.stream_ptr()))
+        rep, size = torch.empty_like(full), torch.empty_like(full)
+        gf._lib.check(gf._lib.lib.gf_orbit_canon(full.data_ptr(), full.numel(), L, rep.data_ptr(), size.data_ptr(),
+                                                 gf._lib.stream_ptr()))
+        comp = torch.empty_like(rep)
+        gf._lib.check(gf._lib.lib.gf_sector_rank(rep.data_ptr(), rep.numel(), comp.data_ptr(), gf._lib.stream_ptr()))
+        idx, first = np.unique(comp.cpu().numpy(), return_index=True)
+        weights = size.cpu().numpy()[first].astype(np.float64)
+        out["orbit_reps_total_burnside"] = {14: 19173968, 16: 268443720}.get(L)
+    out["sample_summands"] = int(idx.size)
+    # target columns of the sample: Chebyshev oracle in the compressed sector, timed separately
+    orc = gf.ChebyshevOracle(spec, 0.25)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    cache = gf.models.CachedTargetColumns(orc, k, 0, idx.size, sector=0, indices=idx, batch=1)
+    torch.cuda.synchronize()
+    out["oracle_s_per_summand"] = (time.perf_counter() - t0) / idx.size
+    out["oracle_chebyshev_order"] = orc.order
+    del orc
+    torch.cuda.empty_cache()
+    basis = (idx, weights)
+    rep, hv = gf.gradient_and_hvp(circ, cache, X, parity_mode=True, sector=0, basis=basis)  # warm-up + plan
+    plan = list(obj._PLANS.values())[-1]
+    out["engine"] = plan.describe()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    reps = 2 if k >= 28 else 3
+    for _ in range(reps):
+        rep, hv = gf.gradient_and_hvp(circ, cache, X, parity_mode=True, sector=0, basis=basis)
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / reps
+    out["grad_hvp_s_per_summand"] = dt / idx.size
+    out["summand_evals_per_s"] = idx.size / dt
+    total = out.get("orbit_reps_total_burnside") or sect_size
+    out["full_sum_summands"] = total
+    out["extrapolated_full_sum_grad_hvp_hours_1gpu"] = total * dt / idx.size / 3600
+    # HVP-only (tCG inner step) throughput
+    t0 = time.perf_counter()
+    hv2 = gf.hessian_vector_product(circ, cache, X, sector=0, basis=basis)
+    torch.cuda.synchronize()
+    out["hvp_s_per_summand"] = (time.perf_counter() - t0) / idx.size
+    # size-independent parity: reinsertion identity per slot on the last batch
+    nlast = idx.size - ((idx.size - 1) // plan.batch) * plan.batch
+    gf.full_gradient(circ, cache, parity_mode=True, sector=0, basis=(idx[-nlast:], None if weights is None
+                                                                       else weights[-nlast:]))
+    d, _ = plan.slot_outputs(nlast)
+    run_v = gf.target_value(circ, cache, sector=0, basis=(idx[-nlast:], None if weights is None
+                                                          else weights[-nlast:]))
+    vals = []
+    t1, t2, lid = circ.slot_arrays()
+    for s in range(circ.num_slots):
+        gm = circ.logical_gates[lid[s]].matrix
+        if t1[s] > t2[s]:
+            gm = gf.kernels.wire_swapped_matrix(gm)
+        vals.append(np.sum(gm * d[s]))
+    vals = np.array(vals)
+    out["reinsertion_max_rel_dev"] = float(np.max(np.abs(-vals.real - run_v)) / max(1.0, abs(run_v)))
+    out["value_sample"] = rep.value
+    return out
+
+
+if __name__ == "__main__":
+    import subprocess
+
+    if len(sys.argv) == 3 and sys.argv[1] == "--one":
+        print(json.dumps(run(sys.argv[2])), flush=True)
+        sys.exit(0)
+    names = sys.argv[1:] or ["c1", "c3", "c4", "c5"]
+    for nm in names:  # one process per config: each frees its device memory on exit
+        r = subprocess.run([sys.executable, os.path.abspath(__file__), "--one", nm], capture_output=True, text=True)
+        line = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else json.dumps(
+            {"config": nm, "error": r.stderr.strip().splitlines()[-1] if r.stderr.strip() else "no output"})
+        print(line, flush=True)

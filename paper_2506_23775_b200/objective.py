@@ -213,6 +213,14 @@ class EnginePlan:
                                          None if weights is None else weights.data_ptr(), phi0.data_ptr(),
                                          out.data_ptr(), _lib.stream_ptr()))
 
+    def slot_outputs(self, nvec: int):
+        """Per-slot D and H sums (normalised wire orientation) of the last
+        eval's batch: two complex arrays [n_slots, 4, 4]."""
+        d = torch.empty((max(self.n, 1), 16), dtype=torch.complex128, device=self.device)
+        h = torch.empty_like(d)
+        _lib.check(_lib.lib.gf_plan_slot_outputs(self.h, nvec, d.data_ptr(), h.data_ptr(), _lib.stream_ptr()))
+        return d[: self.n].reshape(-1, 4, 4).cpu().numpy(), h[: self.n].reshape(-1, 4, 4).cpu().numpy()
+
     def describe(self) -> dict:
         v = (ctypes.c_int * 5)()
         _lib.check(_lib.lib.gf_plan_describe(self.h, ctypes.byref(v, 0), ctypes.byref(v, 4), ctypes.byref(v, 8),
