@@ -262,9 +262,10 @@ __device__ __forceinline__ double2 dmma_mv2(double2 x, double b0, double b1, dou
     return make_double2(c0, c1);
 }
 
-template <int OP, bool FIRST>
-__global__ void __launch_bounds__(FT, 2) k_fused(const FusedParams p)
+template <int OP, bool FIRST, int NT>
+__global__ void __launch_bounds__(NT, 512 / NT) k_fused(const FusedParams p)
 {
+    constexpr int NW = NT / 32;  // warps per CTA
     constexpr int NV = (OP == OP_FWD || OP == OP_FWD_DOT) ? 1 : (OP == OP_REV_G ? 2 : 3);
     constexpr bool HD = (OP == OP_REV_G || OP == OP_REV_GH);
     constexpr bool HH = (OP == OP_REV_GH || OP == OP_ASC_H);
@@ -276,8 +277,8 @@ __global__ void __launch_bounds__(FT, 2) k_fused(const FusedParams p)
     double2 *t0 = reinterpret_cast<double2 *>(fsm);  // psi
     double2 *t1 = t0 + T;                            // bra
     double2 *t2 = t0 + 2 * T;                        // chi (REV) / v (ASC)
-    double *scratch = reinterpret_cast<double *>(t0 + NV * T);  // [2][8][64]
-    double *sacc = scratch + 2 * 8 * 64;                        // [FMAXSLOTS][2][32]
+    double *scratch = reinterpret_cast<double *>(t0 + NV * T);  // [2][NW][64]
+    double *sacc = scratch + 2 * NW * 64;                       // [FMAXSLOTS][2][32]
     u64 *hiofs = reinterpret_cast<u64 *>(sacc + FMAXSLOTS * 2 * 32);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const u64 vb = (u64)blockIdx.y * p.N;
@@ -288,13 +289,13 @@ __global__ void __launch_bounds__(FT, 2) k_fused(const FusedParams p)
     const double w = p.weights ? p.weights[blockIdx.y] : 1.0;
 
     const int nh = 1 << (m - c);
-    for (int h = tid; h < nh; h += FT) {
+    for (int h = tid; h < nh; h += NT) {
         u64 o = 0;
         for (int i = 0; i < m - c; ++i)
             if ((h >> i) & 1) o |= 1ull << p.lpos[c + i];
         hiofs[h] = o;
     }
-    for (int i = tid; i < FMAXSLOTS * 2 * 32; i += FT) sacc[i] = 0.0;
+    for (int i = tid; i < FMAXSLOTS * 2 * 32; i += NT) sacc[i] = 0.0;
     __syncthreads();
     double vre = 0.0, vim = 0.0;
     const unsigned cmask = (1u << c) - 1u;
@@ -310,7 +311,7 @@ __global__ void __launch_bounds__(FT, 2) k_fused(const FusedParams p)
         // the first forward and first ascending passes start from psi_0 = |j>
         constexpr bool SYNTH = (OP == OP_FWD || OP == OP_FWD_DOT || OP == OP_ASC_H) && FIRST;
         const u64 jb = SYNTH ? (u64)p.basis[blockIdx.y] : 0ull;
-        for (unsigned l = tid; l < T; l += FT) {
+        for (unsigned l = tid; l < T; l += NT) {
             const u64 a = base + (l & cmask) + hiofs[l >> c];
             double2 x;
             if constexpr (SYNTH)
@@ -345,7 +346,7 @@ __global__ void __launch_bounds__(FT, 2) k_fused(const FusedParams p)
             const unsigned nunit = c1q ? (T >> 1) : (T >> 2);
             // units per active warp: multiple of 4 (hole MMA K) -- and of 8 for the
             // 2q tensor path (8-tuple groups, paired hole MMAs)
-            const unsigned TW = max(nunit / 8u, c1q ? 4u : 8u);
+            const unsigned TW = max(nunit / (unsigned)NW, c1q ? 4u : 8u);
             const unsigned nwa = nunit / TW;
             const unsigned olo = 1u << llo, ohi = 1u << lhi;
             double cD0 = 0.0, cD1 = 0.0, cH0 = 0.0, cH1 = 0.0;
@@ -503,12 +504,12 @@ __global__ void __launch_bounds__(FT, 2) k_fused(const FusedParams p)
             if constexpr (HD || HH) {
                 if ((unsigned)warp < nwa) {
                     if (HD) {
-                        scratch[(0 * 8 + warp) * 64 + g * 8 + 2 * tq] = cD0;
-                        scratch[(0 * 8 + warp) * 64 + g * 8 + 2 * tq + 1] = cD1;
+                        scratch[(0 * NW + warp) * 64 + g * 8 + 2 * tq] = cD0;
+                        scratch[(0 * NW + warp) * 64 + g * 8 + 2 * tq + 1] = cD1;
                     }
                     if (HH) {
-                        scratch[(1 * 8 + warp) * 64 + g * 8 + 2 * tq] = cH0;
-                        scratch[(1 * 8 + warp) * 64 + g * 8 + 2 * tq + 1] = cH1;
+                        scratch[(1 * NW + warp) * 64 + g * 8 + 2 * tq] = cH0;
+                        scratch[(1 * NW + warp) * 64 + g * 8 + 2 * tq + 1] = cH1;
                     }
                 }
                 __syncthreads();
@@ -518,7 +519,7 @@ __global__ void __launch_bounds__(FT, 2) k_fused(const FusedParams p)
                         const int i = tid & 31, e = i >> 1, part = i & 1, ii = e >> 2, jj = e & 3;
                         double sum = 0.0;
                         for (unsigned ww = 0; ww < nwa; ++ww) {
-                            const double *C = scratch + (hole * 8 + ww) * 64;
+                            const double *C = scratch + (hole * NW + ww) * 64;
                             sum += part == 0 ? (C[(2 * ii) * 8 + 2 * jj] - C[(2 * ii + 1) * 8 + 2 * jj + 1])
                                              : (C[(2 * ii) * 8 + 2 * jj + 1] + C[(2 * ii + 1) * 8 + 2 * jj]);
                         }
@@ -530,7 +531,7 @@ __global__ void __launch_bounds__(FT, 2) k_fused(const FusedParams p)
         }
 
         const int sm = p.store_mask;
-        for (unsigned l = tid; l < T; l += FT) {
+        for (unsigned l = tid; l < T; l += NT) {
             const u64 a = base + (l & cmask) + hiofs[l >> c];
             const double2 x = t0[swz(l)];
             if (sm & 1) psi[a] = x;
@@ -547,7 +548,7 @@ __global__ void __launch_bounds__(FT, 2) k_fused(const FusedParams p)
         __syncthreads();
     }
 
-    for (int i = tid; i < p.nslots * 64; i += FT) {
+    for (int i = tid; i < p.nslots * 64; i += NT) {
         const int si = i >> 6, hole = (i >> 5) & 1, e = i & 31;
         if ((hole == 0 && HD) || (hole == 1 && HH)) {
             double *dst = hole == 0 ? p.partD : p.partH;
@@ -566,7 +567,7 @@ __global__ void __launch_bounds__(FT, 2) k_fused(const FusedParams p)
         __syncthreads();
         if (tid < 2) {
             double s = 0.0;
-            for (int ww = 0; ww < FT / 32; ++ww) s += scratch[ww * 2 + tid];
+            for (int ww = 0; ww < NT / 32; ++ww) s += scratch[ww * 2 + tid];
             p.partV[((u64)blockIdx.y * p.ctas + blockIdx.x) * 2 + tid] = s;
         }
     }
@@ -581,7 +582,7 @@ __global__ void __launch_bounds__(FT, 2) k_fused(const FusedParams p)
     if (s_last) {
         __threadfence();
         const u64 b = blockIdx.y;
-        for (int i = tid; i < p.nslots * 64; i += FT) {
+        for (int i = tid; i < p.nslots * 64; i += NT) {
             const int si = i >> 6, hole = (i >> 5) & 1, e = i & 31;
             if ((hole == 0 && HD) || (hole == 1 && HH)) {
                 const double *src = hole == 0 ? p.partD : p.partH;
@@ -1050,29 +1051,38 @@ static std::vector<FusedParams> plan_passes(const gf_plan *p, bool reverse)
     return out;
 }
 
-static size_t fused_smem(int nv, int m, int c)
+static size_t fused_smem(int nv, int m, int c, int nw)
 {
-    return sizeof(double2) * ((size_t)nv << m) + sizeof(double) * (2 * 8 * 64 + FMAXSLOTS * 2 * 32) +
+    return sizeof(double2) * ((size_t)nv << m) + sizeof(double) * (2 * nw * 64 + FMAXSLOTS * 2 * 32) +
            sizeof(unsigned long long) * ((size_t)1 << (m - c));
 }
 
-template <int OP, bool FIRST>
-static int launch_fused(const gf_plan *p, FusedParams &fp, int64_t nvec, cudaStream_t st)
+template <int OP, bool FIRST, int NT>
+static int launch_fused_nt(const gf_plan *p, FusedParams &fp, int64_t nvec, cudaStream_t st)
 {
     const int nv = (OP == OP_FWD || OP == OP_FWD_DOT) ? 1 : (OP == OP_REV_G ? 2 : 3);
-    const size_t smem = fused_smem(nv, fp.m, fp.c);
+    const size_t smem = fused_smem(nv, fp.m, fp.c, NT / 32);
     static bool attr_done = false;
     if (!attr_done) {
         // 226 KB: the opt-in limit (227 KB) minus the kernel's static shared memory
-        cudaError_t ae = cudaFuncSetAttribute(k_fused<OP, FIRST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t ae = cudaFuncSetAttribute(k_fused<OP, FIRST, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               226 * 1024);
         if (ae != cudaSuccess) return gf_fail(GF_ECUDA, "k_fused smem attribute: %s", cudaGetErrorString(ae));
         attr_done = true;
     }
     if (smem > 226 * 1024) return gf_fail(GF_EINVAL, "fused tile needs %zu B of shared memory", smem);
     dim3 grid(p->ctas, (unsigned)nvec);
-    k_fused<OP, FIRST><<<grid, FT, smem, st>>>(fp);
+    k_fused<OP, FIRST, NT><<<grid, NT, smem, st>>>(fp);
     return GF_OK;
+}
+
+// 256 threads (2 CTAs/SM) for tiles up to 2^11; 512 threads (1 CTA/SM, same 16
+// warps per SM) for 2^12 tiles
+template <int OP, bool FIRST>
+static int launch_fused(const gf_plan *p, FusedParams &fp, int64_t nvec, cudaStream_t st)
+{
+    if (fp.m >= 12) return launch_fused_nt<OP, FIRST, 512>(p, fp, nvec, st);
+    return launch_fused_nt<OP, FIRST, 256>(p, fp, nvec, st);
 }
 
 static int collect_phases(gf_plan *p);

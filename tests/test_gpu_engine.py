@@ -353,7 +353,7 @@ def test_k20_single_summands_vs_oracle():
     assert rel_err(np.stack(hv), plan.logical_sum(h)) < TOL
 
 
-@pytest.mark.parametrize("engine,m", [("fused", "6"), ("fused", "7"), ("stream", None)])
+@pytest.mark.parametrize("engine,m", [("fused", "6"), ("fused", "7"), ("fused", "12"), ("stream", None)])
 def test_multi_tile_multi_pass_engine_vs_oracle(monkeypatch, engine, m):
     """Force tiny fused tiles (2^6 amplitudes) on a 12-qubit circuit: many
     tiles per vector and many passes per sweep, both sector and full space."""
