@@ -262,80 +262,19 @@ __device__ __forceinline__ double2 dmma_mv2(double2 x, double b0, double b1, dou
     return make_double2(c0, c1);
 }
 
-template <int OP, bool FIRST, int NT>
-__global__ void __launch_bounds__(NT, 512 / NT) k_fused(const FusedParams p)
+// The slots of one pass applied to a tile staged in shared memory (t0 = psi,
+// t1 = bra, t2 = chi / v); hole partials accumulate into sacc.
+template <int OP, int NT>
+__device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, double2 *t1, double2 *t2, double *scratch,
+                                          double *sacc, const int tpop, const unsigned T)
 {
-    constexpr int NW = NT / 32;  // warps per CTA
-    constexpr int NV = (OP == OP_FWD || OP == OP_FWD_DOT) ? 1 : (OP == OP_REV_G ? 2 : 3);
+    constexpr int NW = NT / 32;
     constexpr bool HD = (OP == OP_REV_G || OP == OP_REV_GH);
     constexpr bool HH = (OP == OP_REV_GH || OP == OP_ASC_H);
-    constexpr bool HV = (OP == OP_FWD_DOT) || (HD && FIRST);
     constexpr bool REV = (OP == OP_REV_G || OP == OP_REV_GH);
-    extern __shared__ __align__(16) unsigned char fsm[];
-    const int m = p.m, c = p.c;
-    const unsigned T = 1u << m;
-    double2 *t0 = reinterpret_cast<double2 *>(fsm);  // psi
-    double2 *t1 = t0 + T;                            // bra
-    double2 *t2 = t0 + 2 * T;                        // chi (REV) / v (ASC)
-    double *scratch = reinterpret_cast<double *>(t0 + NV * T);  // [2][NW][64]
-    double *sacc = scratch + 2 * NW * 64;                       // [FMAXSLOTS][2][32]
-    u64 *hiofs = reinterpret_cast<u64 *>(sacc + FMAXSLOTS * 2 * 32);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const u64 vb = (u64)blockIdx.y * p.N;
-    double2 *psi = p.psi + vb;
-    double2 *bra = p.bra + vb;
-    double2 *aux = p.aux + vb;
-    const double2 *phi0 = p.phi0 ? p.phi0 + vb : nullptr;
-    const double w = p.weights ? p.weights[blockIdx.y] : 1.0;
-
-    const int nh = 1 << (m - c);
-    for (int h = tid; h < nh; h += NT) {
-        u64 o = 0;
-        for (int i = 0; i < m - c; ++i)
-            if ((h >> i) & 1) o |= 1ull << p.lpos[c + i];
-        hiofs[h] = o;
-    }
-    for (int i = tid; i < FMAXSLOTS * 2 * 32; i += NT) sacc[i] = 0.0;
-    __syncthreads();
-    double vre = 0.0, vim = 0.0;
-    const unsigned cmask = (1u << c) - 1u;
     const int g = lane >> 2, tq = lane & 3;
-    // hole operand rows: component g = 2*amp + part (re/im of one amplitude adjacent)
     const int gi = g >> 1, gpart = g & 1;
-
-    for (u64 tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
-        u64 base = 0;
-        for (int i = 0; i < p.nglob; ++i)
-            if ((tile >> i) & 1ull) base |= 1ull << p.gpos[i];
-        const int tpop = __popcll(tile);
-        // the first forward and first ascending passes start from psi_0 = |j>
-        constexpr bool SYNTH = (OP == OP_FWD || OP == OP_FWD_DOT || OP == OP_ASC_H) && FIRST;
-        const u64 jb = SYNTH ? (u64)p.basis[blockIdx.y] : 0ull;
-        for (unsigned l = tid; l < T; l += NT) {
-            const u64 a = base + (l & cmask) + hiofs[l >> c];
-            double2 x;
-            if constexpr (SYNTH)
-                x = make_double2(a == jb ? 1.0 : 0.0, 0.0);  // psi_0 = |j>, no HBM read
-            else
-                x = psi[a];
-            t0[swz(l)] = x;
-            if constexpr (NV >= 2) {
-                double2 b;
-                if constexpr (REV && FIRST) {
-                    b = cscale(phi0[a], w);
-                    vre = fma(b.x, x.x, vre);
-                    vre = fma(-b.y, x.y, vre);
-                    vim = fma(b.x, x.y, vim);
-                    vim = fma(b.y, x.x, vim);
-                } else {
-                    b = bra[a];
-                }
-                t1[swz(l)] = b;
-            }
-            if constexpr (NV >= 3) t2[swz(l)] = FIRST ? czero() : aux[a];
-        }
-        __syncthreads();
-
         for (int si = 0; si < p.nslots; ++si) {
             const int mode = p.ps[si].mode;
             const int llo = p.ps[si].llo, lhi = p.ps[si].lhi;
@@ -530,6 +469,81 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_fused(const FusedParams p)
             __syncthreads();
         }
 
+}
+
+template <int OP, bool FIRST, int NT>
+__global__ void __launch_bounds__(NT, 512 / NT) k_fused(const FusedParams p)
+{
+    constexpr int NW = NT / 32;  // warps per CTA
+    constexpr int NV = (OP == OP_FWD || OP == OP_FWD_DOT) ? 1 : (OP == OP_REV_G ? 2 : 3);
+    constexpr bool HD = (OP == OP_REV_G || OP == OP_REV_GH);
+    constexpr bool HH = (OP == OP_REV_GH || OP == OP_ASC_H);
+    constexpr bool HV = (OP == OP_FWD_DOT) || (HD && FIRST);
+    constexpr bool REV = (OP == OP_REV_G || OP == OP_REV_GH);
+    extern __shared__ __align__(16) unsigned char fsm[];
+    const int m = p.m, c = p.c;
+    const unsigned T = 1u << m;
+    double2 *t0 = reinterpret_cast<double2 *>(fsm);  // psi
+    double2 *t1 = t0 + T;                            // bra
+    double2 *t2 = t0 + 2 * T;                        // chi (REV) / v (ASC)
+    double *scratch = reinterpret_cast<double *>(t0 + NV * T);  // [2][NW][64]
+    double *sacc = scratch + 2 * NW * 64;                       // [FMAXSLOTS][2][32]
+    u64 *hiofs = reinterpret_cast<u64 *>(sacc + FMAXSLOTS * 2 * 32);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const u64 vb = (u64)blockIdx.y * p.N;
+    double2 *psi = p.psi + vb;
+    double2 *bra = p.bra + vb;
+    double2 *aux = p.aux + vb;
+    const double2 *phi0 = p.phi0 ? p.phi0 + vb : nullptr;
+    const double w = p.weights ? p.weights[blockIdx.y] : 1.0;
+
+    const int nh = 1 << (m - c);
+    for (int h = tid; h < nh; h += NT) {
+        u64 o = 0;
+        for (int i = 0; i < m - c; ++i)
+            if ((h >> i) & 1) o |= 1ull << p.lpos[c + i];
+        hiofs[h] = o;
+    }
+    for (int i = tid; i < FMAXSLOTS * 2 * 32; i += NT) sacc[i] = 0.0;
+    __syncthreads();
+    double vre = 0.0, vim = 0.0;
+    const unsigned cmask = (1u << c) - 1u;
+
+    for (u64 tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+        u64 base = 0;
+        for (int i = 0; i < p.nglob; ++i)
+            if ((tile >> i) & 1ull) base |= 1ull << p.gpos[i];
+        const int tpop = __popcll(tile);
+        // the first forward and first ascending passes start from psi_0 = |j>
+        constexpr bool SYNTH = (OP == OP_FWD || OP == OP_FWD_DOT || OP == OP_ASC_H) && FIRST;
+        const u64 jb = SYNTH ? (u64)p.basis[blockIdx.y] : 0ull;
+        for (unsigned l = tid; l < T; l += NT) {
+            const u64 a = base + (l & cmask) + hiofs[l >> c];
+            double2 x;
+            if constexpr (SYNTH)
+                x = make_double2(a == jb ? 1.0 : 0.0, 0.0);  // psi_0 = |j>, no HBM read
+            else
+                x = psi[a];
+            t0[swz(l)] = x;
+            if constexpr (NV >= 2) {
+                double2 b;
+                if constexpr (REV && FIRST) {
+                    b = cscale(phi0[a], w);
+                    vre = fma(b.x, x.x, vre);
+                    vre = fma(-b.y, x.y, vre);
+                    vim = fma(b.x, x.y, vim);
+                    vim = fma(b.y, x.x, vim);
+                } else {
+                    b = bra[a];
+                }
+                t1[swz(l)] = b;
+            }
+            if constexpr (NV >= 3) t2[swz(l)] = FIRST ? czero() : aux[a];
+        }
+        __syncthreads();
+
+        run_slots<OP, NT>(p, t0, t1, t2, scratch, sacc, tpop, T);
+
         const int sm = p.store_mask;
         for (unsigned l = tid; l < T; l += NT) {
             const u64 a = base + (l & cmask) + hiofs[l >> c];
@@ -603,6 +617,203 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_fused(const FusedParams p)
         }
         if (tid == 0) p.tickets[blockIdx.y] = 0u;
     }
+}
+
+
+// ---------------------------------------------------------------------------
+// Pipelined fused pass: persistent CTAs walk fixed-size segments of tiles
+// (segment s of vector b = tiles [s*segt, (s+1)*segt)), round-robin over the
+// grid, with two tile buffers: while the slots run on one buffer, cp.async
+// streams the next tile into the other, so HBM traffic overlaps the tensor-
+// core work.  Partials are per (slot, vector, segment) -- segment geometry
+// depends only on the vector size, so sums stay bit-identical for any batch.
+// All partials are scaled by the summand weight at flush time (the engine is
+// linear in the bra), so raw target columns can be copied asynchronously.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
+{
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
+template <int OP, bool FIRST, int NT>
+__global__ void __launch_bounds__(NT, 512 / NT) k_fused_pipe(const FusedParams p)
+{
+    constexpr int NW = NT / 32;
+    constexpr int NV = (OP == OP_FWD || OP == OP_FWD_DOT) ? 1 : (OP == OP_REV_G ? 2 : 3);
+    constexpr bool HD = (OP == OP_REV_G || OP == OP_REV_GH);
+    constexpr bool HH = (OP == OP_REV_GH || OP == OP_ASC_H);
+    constexpr bool REV = (OP == OP_REV_G || OP == OP_REV_GH);
+    constexpr bool VLOAD = REV && FIRST;          // value = phi0 . psi_n on the first reverse pass
+    constexpr bool VSTORE = (OP == OP_FWD_DOT);    // value = phi0 . psi_n after the last forward pass
+    constexpr bool SYNTH = (OP == OP_FWD || OP == OP_FWD_DOT || OP == OP_ASC_H) && FIRST;
+    constexpr bool ZERO3 = (NV >= 3) && FIRST;     // chi / v start at zero
+    extern __shared__ __align__(16) unsigned char fsm[];
+    const int m = p.m, c = p.c;
+    const unsigned T = 1u << m;
+    double2 *buf = reinterpret_cast<double2 *>(fsm);                 // [2][NV][T]
+    double *scratch = reinterpret_cast<double *>(buf + 2 * NV * T);  // [2][NW][64]
+    double *sacc = scratch + 2 * NW * 64;                            // [FMAXSLOTS][2][32]
+    u64 *hiofs = reinterpret_cast<u64 *>(sacc + FMAXSLOTS * 2 * 32);
+    __shared__ double vsum[2];
+    __shared__ unsigned s_last;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nh = 1 << (m - c);
+    for (int h = tid; h < nh; h += NT) {
+        u64 o = 0;
+        for (int i = 0; i < m - c; ++i)
+            if ((h >> i) & 1) o |= 1ull << p.lpos[c + i];
+        hiofs[h] = o;
+    }
+    const unsigned cmask = (1u << c) - 1u;
+    const u64 segt = p.seg_tiles, nseg = p.ntiles / p.seg_tiles;
+    const u64 nsegall = nseg * (u64)p.nvec;
+
+    // flat per-CTA tile sequence: segments blockIdx.x, blockIdx.x + gridDim.x, ...
+    auto tile_of = [&](u64 k, u64 &vec, u64 &seg, u64 &tile) -> bool {
+        const u64 sidx = blockIdx.x + (k / segt) * gridDim.x;
+        if (sidx >= nsegall) return false;
+        vec = sidx / nseg;
+        seg = sidx - vec * nseg;
+        tile = seg * segt + (k % segt);
+        return true;
+    };
+    auto tile_base = [&](u64 tile) {
+        u64 base = 0;
+        for (int i = 0; i < p.nglob; ++i)
+            if ((tile >> i) & 1ull) base |= 1ull << p.gpos[i];
+        return base;
+    };
+    auto issue = [&](u64 k, int sel) {
+        u64 vec, seg, tile;
+        if (tile_of(k, vec, seg, tile)) {
+            const u64 base = tile_base(tile) + vec * p.N;
+            double2 *dst = buf + (u64)sel * NV * T;
+            for (unsigned l = tid; l < T; l += NT) {
+                const u64 a = base + (l & cmask) + hiofs[l >> c];
+                const unsigned s = swz(l);
+                if constexpr (!SYNTH) cp_async16(dst + s, p.psi + a);
+                if constexpr (NV >= 2) cp_async16(dst + T + s, (REV && FIRST) ? (p.phi0 + a) : (p.bra + a));
+                if constexpr (NV >= 3 && !FIRST) cp_async16(dst + 2 * T + s, p.aux + a);
+            }
+        }
+        cp_async_commit();
+    };
+
+    for (int i = tid; i < FMAXSLOTS * 2 * 32; i += NT) sacc[i] = 0.0;
+    __syncthreads();
+    issue(0, 0);
+    double vre = 0.0, vim = 0.0;
+    int cur = 0;
+    for (u64 k = 0;; ++k) {
+        u64 vec, seg, tile;
+        if (!tile_of(k, vec, seg, tile)) break;
+        issue(k + 1, cur ^ 1);  // prefetch the next tile while this one computes
+        cp_async_wait<1>();
+        __syncthreads();
+        double2 *t0 = buf + (u64)cur * NV * T, *t1 = t0 + T, *t2 = t0 + 2 * T;
+        const u64 base = tile_base(tile) + vec * p.N;
+        if constexpr (SYNTH || ZERO3 || VLOAD) {
+            const u64 jb = SYNTH ? (u64)p.basis[vec] + vec * p.N : 0ull;
+            for (unsigned l = tid; l < T; l += NT) {
+                const unsigned s = swz(l);
+                if constexpr (SYNTH) {
+                    const u64 a = base + (l & cmask) + hiofs[l >> c];
+                    t0[s] = make_double2(a == jb ? 1.0 : 0.0, 0.0);  // psi_0 = |j>, no HBM read
+                }
+                if constexpr (ZERO3) t2[s] = czero();
+                if constexpr (VLOAD) {
+                    const double2 b = t1[s], x = t0[s];
+                    vre = fma(b.x, x.x, vre);
+                    vre = fma(-b.y, x.y, vre);
+                    vim = fma(b.x, x.y, vim);
+                    vim = fma(b.y, x.x, vim);
+                }
+            }
+            __syncthreads();
+        }
+        run_slots<OP, NT>(p, t0, t1, t2, scratch, sacc, __popcll(tile), T);
+        const int sm = p.store_mask;
+        for (unsigned l = tid; l < T; l += NT) {
+            const u64 a = base + (l & cmask) + hiofs[l >> c];
+            const unsigned s = swz(l);
+            const double2 x = t0[s];
+            if (sm & 1) p.psi[a] = x;
+            if constexpr (NV >= 2) if (sm & 2) p.bra[a] = t1[s];
+            if constexpr (NV >= 3) if (sm & 4) p.aux[a] = t2[s];
+            if constexpr (VSTORE) {
+                const double2 f = p.phi0[a];
+                vre = fma(f.x, x.x, vre);
+                vre = fma(-f.y, x.y, vre);
+                vim = fma(f.x, x.y, vim);
+                vim = fma(f.y, x.x, vim);
+            }
+        }
+        // segment finished: flush its partials (scaled by the summand weight)
+        if ((k + 1) % segt == 0) {
+            const double w = p.weights ? p.weights[vec] : 1.0;
+            __syncthreads();
+            for (int i = tid; i < p.nslots * 64; i += NT) {
+                const int si = i >> 6, hole = (i >> 5) & 1, e = i & 31;
+                if ((hole == 0 && HD) || (hole == 1 && HH)) {
+                    double *dst = hole == 0 ? p.partD : p.partH;
+                    const u64 slot = (u64)p.ps[si].slot;
+                    dst[((slot * p.nvec + vec) * nseg + seg) * 32 + e] = w * sacc[(si * 2 + hole) * 32 + e];
+                }
+                sacc[i] = 0.0;
+            }
+            if constexpr (VLOAD || VSTORE) {
+                vre = warp_sum(vre);
+                vim = warp_sum(vim);
+                if (lane == 0) {
+                    scratch[warp * 2] = vre;
+                    scratch[warp * 2 + 1] = vim;
+                }
+                __syncthreads();
+                if (tid < 2) {
+                    double s = 0.0;
+                    for (int ww = 0; ww < NW; ++ww) s += scratch[ww * 2 + tid];
+                    p.partV[(vec * nseg + seg) * 2 + tid] = w * s;
+                }
+                vre = vim = 0.0;
+            }
+            // the last segment of this vector to finish reduces its partials
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) s_last = (atomicAdd(&p.tickets[vec], 1u) == (unsigned)nseg - 1u);
+            __syncthreads();
+            if (s_last) {
+                __threadfence();
+                for (int i = tid; i < p.nslots * 64; i += NT) {
+                    const int si = i >> 6, hole = (i >> 5) & 1, e = i & 31;
+                    if ((hole == 0 && HD) || (hole == 1 && HH)) {
+                        const double *src = hole == 0 ? p.partD : p.partH;
+                        double *dst = hole == 0 ? p.qD : p.qH;
+                        const u64 slot = (u64)p.ps[si].slot;
+                        const double *q = src + ((slot * p.nvec + vec) * nseg) * 32 + e;
+                        double sum = 0.0;
+                        for (u64 sg = 0; sg < nseg; ++sg) sum += __ldcg(q + sg * 32);
+                        dst[(slot * p.nvec + vec) * 32 + e] = sum;
+                    }
+                }
+                if constexpr (VLOAD || VSTORE) {
+                    if (tid < 2) {
+                        double sum = 0.0;
+                        for (u64 sg = 0; sg < nseg; ++sg) sum += __ldcg(p.partV + (vec * nseg + sg) * 2 + tid);
+                        p.qV[vec * 2 + tid] = sum;
+                    }
+                }
+                if (tid == 0) p.tickets[vec] = 0u;
+            }
+        }
+        __syncthreads();  // buffer `cur` is free for the prefetch issued next iteration
+        cur ^= 1;
+    }
+    cp_async_wait<0>();
+    (void)vsum;
 }
 
 // |j> for every vector of the batch (basis index per vector).
@@ -735,7 +946,10 @@ struct gf_plan {
     int last_flags = 0;
     // fused tile engine
     bool fused = false;
+    bool pipe = false;   // pipelined persistent variant (k_fused_pipe)
     int fm = 0, fc = 0;
+    unsigned long long seg_tiles = 1;
+    int nsm = 148;
     // geometry only (matrices filled per eval).  The ascending HVP sweep must
     // replay exactly the reverse slot order of the reverse sweep (the two HVP
     // half-sums are only order-invariant together), so asc_passes is
@@ -863,8 +1077,11 @@ extern "C" int gf_plan_create(gf_plan **out, int k, int sector, int n_slots, con
     {
         const char *eng = getenv("GF_ENGINE");
         p->fused = p->K >= 6 && !(eng && strcmp(eng, "stream") == 0);
+        const char *penv = getenv("GF_PIPE");
+        p->pipe = p->fused && !(penv && strcmp(penv, "0") == 0);
         const char *fmenv = getenv("GF_FUSED_M");
-        int fm = fmenv ? atoi(fmenv) : 11;
+        // pipelined kernel double-buffers 2^10 tiles (2 CTAs/SM); the classic one uses 2^11
+        int fm = fmenv ? atoi(fmenv) : (p->pipe ? 10 : 11);
         p->fm = std::max(5, std::min(std::min(fm, FMAXM), p->K));
         p->fc = std::min(4, p->fm);
         if (p->fused) {
@@ -873,9 +1090,18 @@ extern "C" int gf_plan_create(gf_plan **out, int k, int sector, int n_slots, con
             p->asc_passes.assign(p->rev_passes.rbegin(), p->rev_passes.rend());
             for (auto &f : p->asc_passes) std::reverse(f.ps, f.ps + f.nslots);
             u64 ntiles = 1ull << (p->K - p->fm);
-            const char *cenv = getenv("GF_FUSED_CTAS");
-            u64 want = cenv ? (u64)atoll(cenv) : (u64)(148 * 8);  // all tiles, up to 8 per SM
-            p->ctas = (int)std::max<u64>(1, std::min<u64>(want, ntiles));
+            if (p->pipe) {
+                // partial segments: <= 4096 per vector, sized by the vector only
+                p->seg_tiles = std::max<u64>(1, ntiles / 4096);
+                p->ctas = (int)(ntiles / p->seg_tiles);
+                int dev = 0, nsm = 148;
+                cudaGetDevice(&dev);
+                if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess) p->nsm = nsm;
+            } else {
+                const char *cenv = getenv("GF_FUSED_CTAS");
+                u64 want = cenv ? (u64)atoll(cenv) : (u64)(148 * 8);  // all tiles, up to 8 per SM
+                p->ctas = (int)std::max<u64>(1, std::min<u64>(want, ntiles));
+            }
         }
     }
     // workspace
@@ -1076,11 +1302,35 @@ static int launch_fused_nt(const gf_plan *p, FusedParams &fp, int64_t nvec, cuda
     return GF_OK;
 }
 
+template <int OP, bool FIRST>
+static int launch_pipe(const gf_plan *p, FusedParams &fp, int64_t nvec, cudaStream_t st)
+{
+    constexpr int NT = 256;
+    const int nv = (OP == OP_FWD || OP == OP_FWD_DOT) ? 1 : (OP == OP_REV_G ? 2 : 3);
+    const size_t smem = fused_smem(2 * nv, fp.m, fp.c, NT / 32);
+    static int bps = 0;
+    if (bps == 0) {
+        cudaError_t ae = cudaFuncSetAttribute(k_fused_pipe<OP, FIRST, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              226 * 1024);
+        if (ae != cudaSuccess) return gf_fail(GF_ECUDA, "k_fused_pipe smem attribute: %s", cudaGetErrorString(ae));
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_fused_pipe<OP, FIRST, NT>, NT, smem) != cudaSuccess ||
+            bps < 1)
+            bps = 1;
+    }
+    if (smem > 226 * 1024) return gf_fail(GF_EINVAL, "pipelined tile needs %zu B of shared memory", smem);
+    fp.seg_tiles = p->seg_tiles;
+    const unsigned long long nsegall = (fp.ntiles / fp.seg_tiles) * (unsigned long long)nvec;
+    const unsigned long long grid = std::min<unsigned long long>(nsegall, (unsigned long long)p->nsm * bps);
+    k_fused_pipe<OP, FIRST, NT><<<(unsigned)grid, NT, smem, st>>>(fp);
+    return GF_OK;
+}
+
 // 256 threads (2 CTAs/SM) for tiles up to 2^11; 512 threads (1 CTA/SM, same 16
 // warps per SM) for 2^12 tiles
 template <int OP, bool FIRST>
 static int launch_fused(const gf_plan *p, FusedParams &fp, int64_t nvec, cudaStream_t st)
 {
+    if (p->pipe) return launch_pipe<OP, FIRST>(p, fp, nvec, st);
     if (fp.m >= 12) return launch_fused_nt<OP, FIRST, 512>(p, fp, nvec, st);
     return launch_fused_nt<OP, FIRST, 256>(p, fp, nvec, st);
 }

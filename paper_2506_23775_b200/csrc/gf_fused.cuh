@@ -42,6 +42,7 @@ struct FusedParams {
     unsigned int *tickets;   // [nvec] arrival counters, self-resetting
     unsigned long long N;
     unsigned long long ntiles;  // 2^(K-m)
+    unsigned long long seg_tiles;  // pipelined kernel: tiles per partial segment
     int nvec, ctas, sector;
     int m, c, nglob, nslots;
     int store_mask;  // bit 0 psi, bit 1 bra, bit 2 chi/v: vectors written back after the pass
