@@ -1078,11 +1078,12 @@ extern "C" int gf_plan_create(gf_plan **out, int k, int sector, int n_slots, con
         const char *eng = getenv("GF_ENGINE");
         p->fused = p->K >= 6 && !(eng && strcmp(eng, "stream") == 0);
         const char *penv = getenv("GF_PIPE");
-        p->pipe = p->fused && !(penv && strcmp(penv, "0") == 0);
+        p->pipe = p->fused && (penv && strcmp(penv, "1") == 0);  // experimental, off by default
         const char *fmenv = getenv("GF_FUSED_M");
         // pipelined kernel double-buffers 2^10 tiles (2 CTAs/SM); the classic one uses 2^11
         int fm = fmenv ? atoi(fmenv) : (p->pipe ? 10 : 11);
         p->fm = std::max(5, std::min(std::min(fm, FMAXM), p->K));
+        if (p->pipe && p->fm > 11) p->pipe = false;  // two 3-vector buffers must fit in shared memory
         p->fc = std::min(4, p->fm);
         if (p->fused) {
             p->fwd_passes = plan_passes(p, false);
@@ -1092,7 +1093,9 @@ extern "C" int gf_plan_create(gf_plan **out, int k, int sector, int n_slots, con
             u64 ntiles = 1ull << (p->K - p->fm);
             if (p->pipe) {
                 // partial segments: <= 4096 per vector, sized by the vector only
-                p->seg_tiles = std::max<u64>(1, ntiles / 4096);
+                const char *senv = getenv("GF_SEG_TILES");
+                p->seg_tiles = senv ? std::max<u64>(1, std::min<u64>((u64)atoll(senv), ntiles))
+                                    : std::max<u64>(1, ntiles / 4096);
                 p->ctas = (int)(ntiles / p->seg_tiles);
                 int dev = 0, nsm = 148;
                 cudaGetDevice(&dev);
