@@ -274,7 +274,7 @@ def _default_batch(N: int, total: int) -> int:
     env = os.environ.get("GF_BATCH")
     if env:
         return max(1, min(int(env), total))
-    budget = 64 * 2**20  # bytes per workspace vector set member
+    budget = 512 * 2**20  # bytes per workspace vector (3 resident): batch 512 at 16 qubits
     return max(1, min(total, budget // (16 * N)))
 
 
