@@ -29,6 +29,8 @@ CONFIGS = {
     "c3": (12, 7, False, True, 0, False, 2, 64),
     "c4": (14, 9, True, True, 0, True, 3, 8),
     "c5": (16, 9, True, True, 0, True, 4, 1),
+    "c2h": (8, 5, False, False, None, False, 1, None),   # configs[1]: full Hessian assembly, full 2^16 sum
+    "c3tr": (12, 7, False, True, 0, False, 2, 64),       # configs[2]: one TR step, gradient + 10 tCG HVPs
 }
 
 
@@ -46,6 +48,28 @@ def run(name):
     k = circ.num_qubits
     out = {"config": name, "L": L, "qubits": k, "layers": layers, "slots": circ.num_slots,
            "logical": circ.num_logical, "periodic": periodic, "sector": sector, "fold": fold}
+    if name == "c2h":
+        orc = gf.ChebyshevOracle(spec, 0.25)
+        cache = gf.models.CachedTargetColumns(orc, k, 0, 1 << k, batch=512)
+        del orc
+        torch.cuda.empty_cache()
+        gf.gradient_and_hvp(circ, cache, X)  # warm-up
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rep = gf.full_hessian(circ, cache)
+        torch.cuda.synchronize()
+        out["full_hessian_s"] = time.perf_counter() - t0
+        out["hvp_evaluations"] = circ.num_logical * 16
+        out["blocks"] = len(rep.hessian.blocks)
+        # size-independent parity: assembled blocks applied to X == engine HVP along X
+        hv = gf.hessian_vector_product(circ, cache, X)
+        via = rep.hessian.apply_direction(X)
+        sc = max(np.abs(np.stack(hv)).max(), 1e-300)
+        out["blocks_vs_hvp_max_rel_dev"] = float(max(np.abs(a - b).max() for a, b in zip(via, hv)) / sc)
+        diag = [rep.hessian.blocks[(a, a)] for a in range(circ.num_logical) if (a, a) in rep.hessian.blocks]
+        out["diag_block_symmetry_max_rel_dev"] = float(max(np.abs(b - b.T).max() / np.abs(b).max() for b in diag))
+        out["reference_cpu_estimate_h"] = 149.0  # 8.2 s per summand x 2^16, single core
+        return out
     if name == "c1":
         orc = gf.DenseOracle(spec, 0.25)
         for _ in range(3):
@@ -108,6 +132,18 @@ def run(name):
     total = out.get("orbit_reps_total_burnside") or sect_size
     out["full_sum_summands"] = total
     out["extrapolated_full_sum_grad_hvp_hours_1gpu"] = total * dt / idx.size / 3600
+    if name == "c3tr":
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        params = gf.TrustRegionParams(max_iterations=1, use_hvp=True, tcg=gf.TcgParams(max_inner=10))
+        final, trace = gf.trust_region_optimize(circ, cache, params, parity_mode=True, sector=0, basis=basis)
+        torch.cuda.synchronize()
+        r = trace.records[0]
+        out["tr_step_s"] = time.perf_counter() - t0
+        out["tr_inner_iterations"] = r.inner_iterations
+        out["tr_stop_reason"] = r.stop_reason
+        out["tr_engine_evaluations"] = 1 + r.inner_iterations + 1 + 1  # gradient, tCG HVPs, model HVP, value
+        return out
     # HVP-only (tCG inner step) throughput
     t0 = time.perf_counter()
     hv2 = gf.hessian_vector_product(circ, cache, X, sector=0, basis=basis)
@@ -139,7 +175,7 @@ if __name__ == "__main__":
     if len(sys.argv) == 3 and sys.argv[1] == "--one":
         print(json.dumps(run(sys.argv[2])), flush=True)
         sys.exit(0)
-    names = sys.argv[1:] or ["c1", "c3", "c4", "c5"]
+    names = sys.argv[1:] or ["c1", "c3", "c4", "c5", "c2h", "c3tr"]
     for nm in names:  # one process per config: each frees its device memory on exit
         r = subprocess.run([sys.executable, os.path.abspath(__file__), "--one", nm], capture_output=True, text=True)
         line = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else json.dumps(
