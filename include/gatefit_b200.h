@@ -124,13 +124,19 @@ int gf_plan_create(gf_plan **plan, int k, int sector, int n_slots, const int32_t
 int gf_plan_set_gates(gf_plan *plan, const double *mats);
 /* HVP directions Z per logical gate [n_logical][4][4] complex (host). */
 int gf_plan_set_directions(gf_plan *plan, const double *zmats);
+/* nd (<= 3) HVP directions [nd][n_logical][4][4] evaluated together: the
+ * fused engine shares the psi / bra sweeps across them (full-Hessian columns,
+ * reference objective.py:701-767).  gf_plan_eval records then carry nd H
+ * blocks: rec = 2 + 32*n_logical*(1 + nd). */
+int gf_plan_set_directions_multi(gf_plan *plan, int nd, const double *zmats);
 /* Evaluate `nvec` summands.  basis_dev: int64 [nvec] basis indices (in the
  * compressed space when sector >= 0).  weights_dev: double [nvec] or NULL
  * (translation-fold orbit sizes).  phi0_dev: complex [nvec][2^K] target
  * columns conj(U|j>) (K = k, or k-1 with a sector).  out_dev: double
- * [ceil(nvec/chunk_states)][rec] with rec = 2 + 64*n_logical doubles:
+ * [ceil(nvec/chunk_states)][rec] with rec = 2 + 32*n_logical*(1 + nd) doubles:
  *   value (complex), D[n_logical][4][4] (holomorphic, logical orientation,
- *   accumulated over shared slots), H[n_logical][4][4] (holomorphic HVP);
+ *   accumulated over shared slots), H_d[n_logical][4][4] (holomorphic HVP per
+ *   direction; nd = 1 unless gf_plan_set_directions_multi);
  * each record is the deterministic sum over its chunk (the reference's
  * _Partial, objective.py:536-558).  value is phi0 . C|j> summed (the
  * objective is f = -Re of the total, objective.py:606). */

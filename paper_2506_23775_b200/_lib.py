@@ -32,6 +32,7 @@ EXPORTS = (
     "gf_plan_create",
     "gf_plan_set_gates",
     "gf_plan_set_directions",
+    "gf_plan_set_directions_multi",
     "gf_plan_eval",
     "gf_plan_slot_outputs",
     "gf_plan_last_launches",
@@ -78,6 +79,7 @@ for _name, _args in {
     "gf_plan_create": [ctypes.POINTER(_vp), _i, _i, _i, _vp, _vp, _vp, _i, _i64, _i],
     "gf_plan_set_gates": [_vp, _vp],
     "gf_plan_set_directions": [_vp, _vp],
+    "gf_plan_set_directions_multi": [_vp, _i, _vp],
     "gf_plan_eval": [_vp, _i, _i64, _vp, _vp, _vp, _vp, _vp],
     "gf_plan_slot_outputs": [_vp, _i64, _vp, _vp, _vp],
     "gf_plan_destroy": [_vp],

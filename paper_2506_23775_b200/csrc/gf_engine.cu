@@ -263,8 +263,10 @@ __device__ __forceinline__ double2 dmma_mv2(double2 x, double b0, double b1, dou
 }
 
 // The slots of one pass applied to a tile staged in shared memory (t0 = psi,
-// t1 = bra, t2 = chi / v); hole partials accumulate into sacc.
-template <int OP, int NT>
+// t1 = bra, t2 + d*T = chi_d (REV) / v_d (ASC) for ND directions); hole
+// partials accumulate into sacc[slot][1 + ND][32] (hole 0 = gradient D,
+// hole 1 + d = HVP direction d).
+template <int OP, int NT, int ND>
 __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, double2 *t1, double2 *t2, double *scratch,
                                           double *sacc, const int tpop, const unsigned T)
 {
@@ -272,210 +274,259 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
     constexpr bool HD = (OP == OP_REV_G || OP == OP_REV_GH);
     constexpr bool HH = (OP == OP_REV_GH || OP == OP_ASC_H);
     constexpr bool REV = (OP == OP_REV_G || OP == OP_REV_GH);
+    constexpr int NH = 1 + ND;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, tq = lane & 3;
+    // hole operand rows: component g = 2*amp + part (re/im of one amplitude adjacent)
     const int gi = g >> 1, gpart = g & 1;
-        for (int si = 0; si < p.nslots; ++si) {
-            const int mode = p.ps[si].mode;
-            const int llo = p.ps[si].llo, lhi = p.ps[si].lhi;
-            const Mat4 &MA = p.mat[si][0];
-            const Mat4 &MB = p.mat[si][1];
-            const Mat4 &MC = p.mat[si][2];
-            const bool c1q = (mode == PM_C1Q);
-            const unsigned nunit = c1q ? (T >> 1) : (T >> 2);
-            // units per active warp: multiple of 4 (hole MMA K) -- and of 8 for the
-            // 2q tensor path (8-tuple groups, paired hole MMAs)
-            const unsigned TW = max(nunit / (unsigned)NW, c1q ? 4u : 8u);
-            const unsigned nwa = nunit / TW;
-            const unsigned olo = 1u << llo, ohi = 1u << lhi;
-            double cD0 = 0.0, cD1 = 0.0, cH0 = 0.0, cH1 = 0.0;
-            if ((unsigned)warp < nwa) {
-                const unsigned wbase = warp * TW;
-                if (c1q) {
-                    // ---- parity-controlled 1q slot (sector implicit qubit): FMA on pairs
+    for (int si = 0; si < p.nslots; ++si) {
+        const int mode = p.ps[si].mode;
+        const int llo = p.ps[si].llo, lhi = p.ps[si].lhi;
+        const int zmask = p.ps[si].zmask;
+        const Mat4 &MA = p.mat[si][0];
+        const Mat4 &MB = p.mat[si][1];
+        const bool c1q = (mode == PM_C1Q);
+        const unsigned nunit = c1q ? (T >> 1) : (T >> 2);
+        // units per active warp: multiple of 4 (hole MMA K) -- and of 8 for the
+        // 2q tensor path (8-tuple groups, paired hole MMAs)
+        const unsigned TW = max(nunit / (unsigned)NW, c1q ? 4u : 8u);
+        const unsigned nwa = nunit / TW;
+        const unsigned olo = 1u << llo, ohi = 1u << lhi;
+        double cD0 = 0.0, cD1 = 0.0, cH0[ND], cH1[ND];
+#pragma unroll
+        for (int d = 0; d < ND; ++d) cH0[d] = cH1[d] = 0.0;
+        if ((unsigned)warp < nwa) {
+            const unsigned wbase = warp * TW;
+            if (c1q) {
+                // ---- parity-controlled 1q slot (sector implicit qubit): FMA on pairs
+                double2 *V = (OP == OP_ASC_H) ? t1 : t0;
+                for (unsigned j = lane; j < TW; j += 32) {
+                    const unsigned l0r = ins0u(wbase + j, llo);
+                    const int P = (tpop + __popc(l0r)) & 1 ^ p.sector;
+                    const unsigned s0 = swz(l0r), s1 = swz(l0r | olo);
+                    double2 x[2] = {V[s0], V[s1]}, y[2];
+                    mv2(MA, P, x, y);
+                    V[s0] = y[0];
+                    V[s1] = y[1];
+                }
+                if constexpr (HD || HH) {
+                    __syncwarp();
+                    const double *d0 = reinterpret_cast<const double *>(t0);
+                    const double *d1 = reinterpret_cast<const double *>(t1);
+                    const double *d2 = reinterpret_cast<const double *>(t2);
+                    for (unsigned q = 0; q < TW / 4; ++q) {
+                        const unsigned l0 = ins0u(wbase + 4 * q + tq, llo);
+                        const int P = (tpop + __popc(l0)) & 1 ^ p.sector;
+                        const int i0 = P ? 1 : 0, i1 = P ? 2 : 3;
+                        const int li = (gi == i0) ? (int)l0 : ((gi == i1) ? (int)(l0 | olo) : -1);
+                        const int o = li >= 0 ? 2 * (int)swz((unsigned)li) + gpart : 0;
+                        if constexpr (REV) {
+                            const double k = li >= 0 ? d0[o] : 0.0;
+                            dmma(cD0, cD1, li >= 0 ? d1[o] : 0.0, k);
+                            if constexpr (HH) {
+#pragma unroll
+                                for (int d = 0; d < ND; ++d) dmma(cH0[d], cH1[d], li >= 0 ? d2[2 * d * T + o] : 0.0, k);
+                            }
+                        } else {
+                            const double bq = li >= 0 ? d1[o] : 0.0;
+#pragma unroll
+                            for (int d = 0; d < ND; ++d) dmma(cH0[d], cH1[d], bq, li >= 0 ? d2[2 * d * T + o] : 0.0);
+                        }
+                    }
+                    __syncwarp();
+                }
+                if constexpr (OP != OP_FWD && OP != OP_FWD_DOT) {
                     for (unsigned j = lane; j < TW; j += 32) {
-                        const unsigned l0r = ins0u(wbase + j, llo);
+                        const unsigned l0r = ins0u(wbase + j, llo), l0 = swz(l0r), l1 = swz(l0r | olo);
                         const int P = (tpop + __popc(l0r)) & 1 ^ p.sector;
-                        const unsigned s0 = swz(l0r), s1 = swz(l0r | olo);
-                        double2 *V = (OP == OP_ASC_H) ? t1 : t0;
-                        double2 x[2] = {V[s0], V[s1]}, y[2];
-                        mv2(MA, P, x, y);
-                        V[s0] = y[0];
-                        V[s1] = y[1];
-                    }
-                    if constexpr (HD || HH) {
-                        __syncwarp();
-                        const double *d0 = reinterpret_cast<const double *>(t0);
-                        const double *d1 = reinterpret_cast<const double *>(t1);
-                        const double *d2 = reinterpret_cast<const double *>(t2);
-                        for (unsigned q = 0; q < TW / 4; ++q) {
-                            const unsigned l0 = ins0u(wbase + 4 * q + tq, llo);
-                            const int P = (tpop + __popc(l0)) & 1 ^ p.sector;
-                            const int i0 = P ? 1 : 0, i1 = P ? 2 : 3;
-                            const int li = (gi == i0) ? (int)l0 : ((gi == i1) ? (int)(l0 | olo) : -1);
-                            const int o = li >= 0 ? 2 * (int)swz((unsigned)li) + gpart : 0;
-                            if constexpr (REV) {
-                                const double k = li >= 0 ? d0[o] : 0.0;
-                                dmma(cD0, cD1, li >= 0 ? d1[o] : 0.0, k);
-                                if constexpr (HH) dmma(cH0, cH1, li >= 0 ? d2[o] : 0.0, k);
-                            } else {
-                                dmma(cH0, cH1, li >= 0 ? d1[o] : 0.0, li >= 0 ? d2[o] : 0.0);
-                            }
-                        }
-                        __syncwarp();
-                    }
-                    if constexpr (OP != OP_FWD && OP != OP_FWD_DOT) {
-                        for (unsigned j = lane; j < TW; j += 32) {
-                            const unsigned l0r = ins0u(wbase + j, llo), l0 = swz(l0r), l1 = swz(l0r | olo);
-                            const int P = (tpop + __popc(l0r)) & 1 ^ p.sector;
-                            if constexpr (REV) {
-                                double2 b[2] = {t1[l0], t1[l1]}, bn[2];
-                                if constexpr (OP == OP_REV_GH) {
-                                    double2 cc[2] = {t2[l0], t2[l1]}, cn[2];
+                        if constexpr (REV) {
+                            double2 b[2] = {t1[l0], t1[l1]}, bn[2];
+                            if constexpr (OP == OP_REV_GH) {
+#pragma unroll
+                                for (int d = 0; d < ND; ++d) {
+                                    double2 *X = t2 + d * T;
+                                    double2 cc[2] = {X[l0], X[l1]}, cn[2];
                                     mv2(MB, P, cc, cn);
-                                    mv2_acc(MC, P, b, cn);
-                                    t2[l0] = cn[0];
-                                    t2[l1] = cn[1];
+                                    if ((zmask >> d) & 1) mv2_acc(p.mat[si][2 + d], P, b, cn);
+                                    X[l0] = cn[0];
+                                    X[l1] = cn[1];
                                 }
-                                mv2(MB, P, b, bn);
-                                t1[l0] = bn[0];
-                                t1[l1] = bn[1];
-                            } else {
-                                double2 x[2] = {t0[l0], t0[l1]}, v[2] = {t2[l0], t2[l1]}, vn[2], y[2];
+                            }
+                            mv2(MB, P, b, bn);
+                            t1[l0] = bn[0];
+                            t1[l1] = bn[1];
+                        } else {
+                            double2 x[2] = {t0[l0], t0[l1]}, y[2];
+#pragma unroll
+                            for (int d = 0; d < ND; ++d) {
+                                double2 *X = t2 + d * T;
+                                double2 v[2] = {X[l0], X[l1]}, vn[2];
                                 mv2(MB, P, v, vn);
-                                mv2_acc(MC, P, x, vn);
-                                mv2(MB, P, x, y);
-                                t2[l0] = vn[0];
-                                t2[l1] = vn[1];
-                                t0[l0] = y[0];
-                                t0[l1] = y[1];
+                                if ((zmask >> d) & 1) mv2_acc(p.mat[si][2 + d], P, x, vn);
+                                X[l0] = vn[0];
+                                X[l1] = vn[1];
                             }
+                            mv2(MB, P, x, y);
+                            t0[l0] = y[0];
+                            t0[l1] = y[1];
                         }
                     }
-                } else {
-                    // ---- two-qubit slot, all FP64 math on the tensor cores (DMMA m8n8k4).
-                    // Tuple -> swizzled tile index is GF(2)-linear (bit insertion +
-                    // XOR swizzle), so every address is an XOR of precomputed columns.
-                    auto F = [&](unsigned x) { return swz(ins0u(ins0u(x, llo), lhi)); };
-                    const unsigned offA = swz(((tq & 2) ? ohi : 0u) | ((tq & 1) ? olo : 0u));
-                    const unsigned baseA = F(wbase + g) ^ offA;  // gate layout: lane (g, tq) = amp tq of tuple g
-                    const unsigned ngrp = TW >> 3;                // groups of 8 tuples (TW >= 8 here when m >= 7)
-                    unsigned colA[4];
+                }
+            } else {
+                // ---- two-qubit slot, all FP64 math on the tensor cores (DMMA m8n8k4).
+                // Tuple -> swizzled tile index is GF(2)-linear (bit insertion +
+                // XOR swizzle), so every address is an XOR of precomputed columns.
+                auto F = [&](unsigned x) { return swz(ins0u(ins0u(x, llo), lhi)); };
+                const unsigned offA = swz(((tq & 2) ? ohi : 0u) | ((tq & 1) ? olo : 0u));
+                const unsigned baseA = F(wbase + g) ^ offA;  // gate layout: lane (g, tq) = amp tq of tuple g
+                const unsigned ngrp = TW >> 3;                // groups of 8 tuples
+                unsigned colA[4];
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) colA[i] = F(8u << i);
-                    auto addrA = [&](unsigned grp) {
-                        unsigned a = baseA;
+                for (int i = 0; i < 4; ++i) colA[i] = F(8u << i);
+                auto addrA = [&](unsigned grp) {
+                    unsigned a = baseA;
 #pragma unroll
-                        for (int i = 0; i < 4; ++i)
-                            if ((grp >> i) & 1u) a ^= colA[i];
-                        return a;
-                    };
-                    double2 *V = (OP == OP_ASC_H) ? t1 : t0;
-                    {
-                        double fa0, fa1;
-                        gate_frag(MA, g, tq, fa0, fa1);
+                    for (int i = 0; i < 4; ++i)
+                        if ((grp >> i) & 1u) a ^= colA[i];
+                    return a;
+                };
+                double2 *V = (OP == OP_ASC_H) ? t1 : t0;
+                {
+                    double fa0, fa1;
+                    gate_frag(MA, g, tq, fa0, fa1);
 #pragma unroll 8
-                        for (unsigned grp = 0; grp < ngrp; ++grp) {
-                            const unsigned ad = addrA(grp);
-                            V[ad] = dmma_mv(V[ad], fa0, fa1);
-                        }
+                    for (unsigned grp = 0; grp < ngrp; ++grp) {
+                        const unsigned ad = addrA(grp);
+                        V[ad] = dmma_mv(V[ad], fa0, fa1);
                     }
-                    if constexpr (HD || HH) {
-                        __syncwarp();
-                        // hole layout: lane (g, tq) = component g (amp g&3, part g>>2) of tuple tq
-                        const unsigned offH = swz(((gi & 2) ? ohi : 0u) | ((gi & 1) ? olo : 0u));
-                        const unsigned baseH = F(wbase + tq) ^ offH;
-                        unsigned colH[5];
+                }
+                if constexpr (HD || HH) {
+                    __syncwarp();
+                    // hole layout: lane (g, tq) = component g (amp g>>1, part g&1) of tuple tq
+                    const unsigned offH = swz(((gi & 2) ? ohi : 0u) | ((gi & 1) ? olo : 0u));
+                    const unsigned baseH = F(wbase + tq) ^ offH;
+                    unsigned colH[5];
 #pragma unroll
-                        for (int i = 0; i < 5; ++i) colH[i] = F(4u << i);
-                        const double *d0 = reinterpret_cast<const double *>(t0) + gpart;
-                        const double *d1 = reinterpret_cast<const double *>(t1) + gpart;
-                        const double *d2 = reinterpret_cast<const double *>(t2) + gpart;
-                        double eD0 = 0.0, eD1 = 0.0, eH0 = 0.0, eH1 = 0.0;  // second accumulators (ILP)
-                        const unsigned nq = TW >> 2;
+                    for (int i = 0; i < 5; ++i) colH[i] = F(4u << i);
+                    const double *d0 = reinterpret_cast<const double *>(t0) + gpart;
+                    const double *d1 = reinterpret_cast<const double *>(t1) + gpart;
+                    const double *d2 = reinterpret_cast<const double *>(t2) + gpart;
+                    double eD0 = 0.0, eD1 = 0.0, eH0[ND], eH1[ND];  // second accumulators (ILP)
+#pragma unroll
+                    for (int d = 0; d < ND; ++d) eH0[d] = eH1[d] = 0.0;
+                    const unsigned nq = TW >> 2;
 #pragma unroll 4
-                        for (unsigned q = 0; q < nq; q += 2) {
-                            unsigned a0 = baseH;
+                    for (unsigned q = 0; q < nq; q += 2) {
+                        unsigned a0 = baseH;
 #pragma unroll
-                            for (int i = 1; i < 5; ++i)
-                                if ((q >> i) & 1u) a0 ^= colH[i];
-                            const unsigned a1 = a0 ^ colH[0];
-                            const unsigned o0 = 2 * a0, o1 = 2 * a1;
-                            if constexpr (REV) {
-                                const double k0 = d0[o0], k1 = d0[o1];
-                                dmma(cD0, cD1, d1[o0], k0);
-                                dmma(eD0, eD1, d1[o1], k1);
-                                if constexpr (HH) {
-                                    dmma(cH0, cH1, d2[o0], k0);
-                                    dmma(eH0, eH1, d2[o1], k1);
+                        for (int i = 1; i < 5; ++i)
+                            if ((q >> i) & 1u) a0 ^= colH[i];
+                        const unsigned a1 = a0 ^ colH[0];
+                        const unsigned o0 = 2 * a0, o1 = 2 * a1;
+                        if constexpr (REV) {
+                            const double k0 = d0[o0], k1 = d0[o1];
+                            dmma(cD0, cD1, d1[o0], k0);
+                            dmma(eD0, eD1, d1[o1], k1);
+                            if constexpr (HH) {
+#pragma unroll
+                                for (int d = 0; d < ND; ++d) {
+                                    dmma(cH0[d], cH1[d], d2[2 * d * T + o0], k0);
+                                    dmma(eH0[d], eH1[d], d2[2 * d * T + o1], k1);
                                 }
-                            } else {
-                                dmma(cH0, cH1, d1[o0], d2[o0]);
-                                dmma(eH0, eH1, d1[o1], d2[o1]);
+                            }
+                        } else {
+                            const double b0 = d1[o0], b1 = d1[o1];
+#pragma unroll
+                            for (int d = 0; d < ND; ++d) {
+                                dmma(cH0[d], cH1[d], b0, d2[2 * d * T + o0]);
+                                dmma(eH0[d], eH1[d], b1, d2[2 * d * T + o1]);
                             }
                         }
-                        cD0 += eD0;
-                        cD1 += eD1;
-                        cH0 += eH0;
-                        cH1 += eH1;
-                        __syncwarp();
                     }
-                    if constexpr (OP != OP_FWD && OP != OP_FWD_DOT) {
-                        double fb0, fb1, fc0 = 0.0, fc1 = 0.0;
-                        gate_frag(MB, g, tq, fb0, fb1);
-                        if constexpr (OP == OP_REV_GH || OP == OP_ASC_H) gate_frag(MC, g, tq, fc0, fc1);
+                    cD0 += eD0;
+                    cD1 += eD1;
+#pragma unroll
+                    for (int d = 0; d < ND; ++d) {
+                        cH0[d] += eH0[d];
+                        cH1[d] += eH1[d];
+                    }
+                    __syncwarp();
+                }
+                if constexpr (OP != OP_FWD && OP != OP_FWD_DOT) {
+                    double fb0, fb1, fc0[ND], fc1[ND];
+                    gate_frag(MB, g, tq, fb0, fb1);
+#pragma unroll
+                    for (int d = 0; d < ND; ++d) {
+                        fc0[d] = fc1[d] = 0.0;
+                        if (OP == OP_REV_GH || OP == OP_ASC_H) gate_frag(p.mat[si][2 + d], g, tq, fc0[d], fc1[d]);
+                    }
 #pragma unroll 8
-                        for (unsigned grp = 0; grp < ngrp; ++grp) {
-                            const unsigned ad = addrA(grp);
-                            if constexpr (REV) {
-                                const double2 bb = t1[ad];
-                                if constexpr (OP == OP_REV_GH) t2[ad] = dmma_mv2(t2[ad], fb0, fb1, bb, fc0, fc1);
-                                t1[ad] = dmma_mv(bb, fb0, fb1);
-                            } else {
-                                const double2 x = t0[ad];
-                                t2[ad] = dmma_mv2(t2[ad], fb0, fb1, x, fc0, fc1);
-                                t0[ad] = dmma_mv(x, fb0, fb1);
+                    for (unsigned grp = 0; grp < ngrp; ++grp) {
+                        const unsigned ad = addrA(grp);
+                        if constexpr (REV) {
+                            const double2 bb = t1[ad];
+                            if constexpr (OP == OP_REV_GH) {
+#pragma unroll
+                                for (int d = 0; d < ND; ++d) {
+                                    double2 *X = t2 + d * T;
+                                    X[ad] = ((zmask >> d) & 1) ? dmma_mv2(X[ad], fb0, fb1, bb, fc0[d], fc1[d])
+                                                               : dmma_mv(X[ad], fb0, fb1);
+                                }
                             }
+                            t1[ad] = dmma_mv(bb, fb0, fb1);
+                        } else {
+                            const double2 x = t0[ad];
+#pragma unroll
+                            for (int d = 0; d < ND; ++d) {
+                                double2 *X = t2 + d * T;
+                                X[ad] = ((zmask >> d) & 1) ? dmma_mv2(X[ad], fb0, fb1, x, fc0[d], fc1[d])
+                                                           : dmma_mv(X[ad], fb0, fb1);
+                            }
+                            t0[ad] = dmma_mv(x, fb0, fb1);
                         }
                     }
                 }
             }
-            if constexpr (HD || HH) {
-                if ((unsigned)warp < nwa) {
-                    if (HD) {
-                        scratch[(0 * NW + warp) * 64 + g * 8 + 2 * tq] = cD0;
-                        scratch[(0 * NW + warp) * 64 + g * 8 + 2 * tq + 1] = cD1;
-                    }
-                    if (HH) {
-                        scratch[(1 * NW + warp) * 64 + g * 8 + 2 * tq] = cH0;
-                        scratch[(1 * NW + warp) * 64 + g * 8 + 2 * tq + 1] = cH1;
-                    }
+        }
+        if constexpr (HD || HH) {
+            if ((unsigned)warp < nwa) {
+                if (HD) {
+                    scratch[(0 * NW + warp) * 64 + g * 8 + 2 * tq] = cD0;
+                    scratch[(0 * NW + warp) * 64 + g * 8 + 2 * tq + 1] = cD1;
                 }
-                __syncthreads();
-                if (tid < 64) {
-                    const int hole = tid >> 5;
-                    if ((hole == 0 && HD) || (hole == 1 && HH)) {
-                        const int i = tid & 31, e = i >> 1, part = i & 1, ii = e >> 2, jj = e & 3;
-                        double sum = 0.0;
-                        for (unsigned ww = 0; ww < nwa; ++ww) {
-                            const double *C = scratch + (hole * NW + ww) * 64;
-                            sum += part == 0 ? (C[(2 * ii) * 8 + 2 * jj] - C[(2 * ii + 1) * 8 + 2 * jj + 1])
-                                             : (C[(2 * ii) * 8 + 2 * jj + 1] + C[(2 * ii + 1) * 8 + 2 * jj]);
-                        }
-                        sacc[(si * 2 + hole) * 32 + i] += sum;
+                if (HH) {
+#pragma unroll
+                    for (int d = 0; d < ND; ++d) {
+                        scratch[((1 + d) * NW + warp) * 64 + g * 8 + 2 * tq] = cH0[d];
+                        scratch[((1 + d) * NW + warp) * 64 + g * 8 + 2 * tq + 1] = cH1[d];
                     }
                 }
             }
             __syncthreads();
+            if (tid < 32 * NH) {
+                const int hole = tid >> 5;
+                if ((hole == 0 && HD) || (hole >= 1 && HH)) {
+                    const int i = tid & 31, e = i >> 1, part = i & 1, ii = e >> 2, jj = e & 3;
+                    double sum = 0.0;
+                    for (unsigned ww = 0; ww < nwa; ++ww) {
+                        const double *C = scratch + (hole * NW + ww) * 64;
+                        sum += part == 0 ? (C[(2 * ii) * 8 + 2 * jj] - C[(2 * ii + 1) * 8 + 2 * jj + 1])
+                                         : (C[(2 * ii) * 8 + 2 * jj + 1] + C[(2 * ii + 1) * 8 + 2 * jj]);
+                    }
+                    sacc[(si * NH + hole) * 32 + i] += sum;
+                }
+            }
         }
-
+        __syncthreads();
+    }
 }
 
-template <int OP, bool FIRST, int NT>
+template <int OP, bool FIRST, int NT, int ND>
 __global__ void __launch_bounds__(NT, 512 / NT) k_fused(const FusedParams p)
 {
     constexpr int NW = NT / 32;  // warps per CTA
-    constexpr int NV = (OP == OP_FWD || OP == OP_FWD_DOT) ? 1 : (OP == OP_REV_G ? 2 : 3);
+    constexpr int NH = 1 + ND;   // hole slots: gradient + ND directions
+    constexpr int NV = (OP == OP_FWD || OP == OP_FWD_DOT) ? 1 : (OP == OP_REV_G ? 2 : 2 + ND);
     constexpr bool HD = (OP == OP_REV_G || OP == OP_REV_GH);
     constexpr bool HH = (OP == OP_REV_GH || OP == OP_ASC_H);
     constexpr bool HV = (OP == OP_FWD_DOT) || (HD && FIRST);
@@ -485,10 +536,10 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_fused(const FusedParams p)
     const unsigned T = 1u << m;
     double2 *t0 = reinterpret_cast<double2 *>(fsm);  // psi
     double2 *t1 = t0 + T;                            // bra
-    double2 *t2 = t0 + 2 * T;                        // chi (REV) / v (ASC)
-    double *scratch = reinterpret_cast<double *>(t0 + NV * T);  // [2][NW][64]
-    double *sacc = scratch + 2 * NW * 64;                       // [FMAXSLOTS][2][32]
-    u64 *hiofs = reinterpret_cast<u64 *>(sacc + FMAXSLOTS * 2 * 32);
+    double2 *t2 = t0 + 2 * T;                        // chi_d (REV) / v_d (ASC), ND tiles
+    double *scratch = reinterpret_cast<double *>(t0 + NV * T);  // [NH][NW][64]
+    double *sacc = scratch + NH * NW * 64;                      // [FMAXSLOTS][NH][32]
+    u64 *hiofs = reinterpret_cast<u64 *>(sacc + FMAXSLOTS * NH * 32);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const u64 vb = (u64)blockIdx.y * p.N;
     double2 *psi = p.psi + vb;
@@ -504,7 +555,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_fused(const FusedParams p)
             if ((h >> i) & 1) o |= 1ull << p.lpos[c + i];
         hiofs[h] = o;
     }
-    for (int i = tid; i < FMAXSLOTS * 2 * 32; i += NT) sacc[i] = 0.0;
+    for (int i = tid; i < FMAXSLOTS * NH * 32; i += NT) sacc[i] = 0.0;
     __syncthreads();
     double vre = 0.0, vim = 0.0;
     const unsigned cmask = (1u << c) - 1u;
@@ -538,11 +589,14 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_fused(const FusedParams p)
                 }
                 t1[swz(l)] = b;
             }
-            if constexpr (NV >= 3) t2[swz(l)] = FIRST ? czero() : aux[a];
+            if constexpr (NV >= 3) {
+#pragma unroll
+                for (int d = 0; d < ND; ++d) t2[d * T + swz(l)] = FIRST ? czero() : aux[a + d * p.auxstride];
+            }
         }
         __syncthreads();
 
-        run_slots<OP, NT>(p, t0, t1, t2, scratch, sacc, tpop, T);
+        run_slots<OP, NT, ND>(p, t0, t1, t2, scratch, sacc, tpop, T);
 
         const int sm = p.store_mask;
         for (unsigned l = tid; l < T; l += NT) {
@@ -550,7 +604,12 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_fused(const FusedParams p)
             const double2 x = t0[swz(l)];
             if (sm & 1) psi[a] = x;
             if constexpr (NV >= 2) if (sm & 2) bra[a] = t1[swz(l)];
-            if constexpr (NV >= 3) if (sm & 4) aux[a] = t2[swz(l)];
+            if constexpr (NV >= 3) {
+                if (sm & 4) {
+#pragma unroll
+                    for (int d = 0; d < ND; ++d) aux[a + d * p.auxstride] = t2[d * T + swz(l)];
+                }
+            }
             if constexpr (OP == OP_FWD_DOT) {
                 const double2 f = cscale(phi0[a], w);
                 vre = fma(f.x, x.x, vre);
@@ -562,12 +621,12 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_fused(const FusedParams p)
         __syncthreads();
     }
 
-    for (int i = tid; i < p.nslots * 64; i += NT) {
-        const int si = i >> 6, hole = (i >> 5) & 1, e = i & 31;
-        if ((hole == 0 && HD) || (hole == 1 && HH)) {
-            double *dst = hole == 0 ? p.partD : p.partH;
+    for (int i = tid; i < p.nslots * NH * 32; i += NT) {
+        const int si = i / (NH * 32), hole = (i >> 5) % NH, e = i & 31;
+        if ((hole == 0 && HD) || (hole >= 1 && HH)) {
+            double *dst = hole == 0 ? p.partD : p.partH + (u64)(hole - 1) * p.hstride;
             const u64 slot = (u64)p.ps[si].slot;
-            dst[((slot * p.nvec + blockIdx.y) * p.ctas + blockIdx.x) * 32 + e] = sacc[(si * 2 + hole) * 32 + e];
+            dst[((slot * p.nvec + blockIdx.y) * p.ctas + blockIdx.x) * 32 + e] = sacc[(si * NH + hole) * 32 + e];
         }
     }
     if constexpr (HV) {
@@ -596,11 +655,11 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_fused(const FusedParams p)
     if (s_last) {
         __threadfence();
         const u64 b = blockIdx.y;
-        for (int i = tid; i < p.nslots * 64; i += NT) {
-            const int si = i >> 6, hole = (i >> 5) & 1, e = i & 31;
-            if ((hole == 0 && HD) || (hole == 1 && HH)) {
-                const double *src = hole == 0 ? p.partD : p.partH;
-                double *dst = hole == 0 ? p.qD : p.qH;
+        for (int i = tid; i < p.nslots * NH * 32; i += NT) {
+            const int si = i / (NH * 32), hole = (i >> 5) % NH, e = i & 31;
+            if ((hole == 0 && HD) || (hole >= 1 && HH)) {
+                const double *src = hole == 0 ? p.partD : p.partH + (u64)(hole - 1) * p.hstride;
+                double *dst = hole == 0 ? p.qD : p.qH + (u64)(hole - 1) * p.qhstride;
                 const u64 slot = (u64)p.ps[si].slot;
                 const double *q = src + ((slot * p.nvec + b) * p.ctas) * 32 + e;
                 double sum = 0.0;
@@ -735,7 +794,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_fused_pipe(const FusedParams p
             }
             __syncthreads();
         }
-        run_slots<OP, NT>(p, t0, t1, t2, scratch, sacc, __popcll(tile), T);
+        run_slots<OP, NT, 1>(p, t0, t1, t2, scratch, sacc, __popcll(tile), T);
         const int sm = p.store_mask;
         for (unsigned l = tid; l < T; l += NT) {
             const u64 a = base + (l & cmask) + hiofs[l >> c];
@@ -845,9 +904,9 @@ __global__ void k_reduce_ctas(const double *part, double *q, int64_t nsb, int ct
 __global__ void k_chunk_records(const double *qD, const double *qHd, const double *qHa, const double *partV,
                                 int64_t nvec, int ctas, int nslots, int nlog, const int *lstart,
                                 const int *lslots, const int *swapped, int chunk, int flags, int parity_only,
-                                double *out)
+                                int nd, int64_t qhstride, double *out)
 {
-    const int rec = 2 + 64 * nlog;
+    const int rec = 2 + 32 * nlog * (1 + nd);
     const int64_t nchunks = (nvec + chunk - 1) / chunk;
     const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
@@ -863,12 +922,14 @@ __global__ void k_chunk_records(const double *qD, const double *qHd, const doubl
         }
     } else {
         int rr = r - 2;
-        const bool isH = rr >= 32 * nlog;
-        if (isH) rr -= 32 * nlog;
+        const int blk = rr / (32 * nlog);  // 0 = gradient D, 1 + d = HVP direction d
+        rr -= blk * 32 * nlog;
+        const bool isH = blk >= 1;
+        const int64_t hoff = isH ? (int64_t)(blk - 1) * qhstride : 0;
         const int l = rr >> 5, q = rr & 31;
         const int e = q >> 1, ri = q & 1;
         const int ii = e >> 2, jj = e & 3;
-        const double *src = isH ? qHd : qD;
+        const double *src = isH ? qHd + hoff : qD;
         // compressed-sector hole entries pairing opposite-parity rows/cols
         // would pair different implicit-qubit values: exactly zero in the
         // full-space sum (both vectors live in the sector)
@@ -885,7 +946,7 @@ __global__ void k_chunk_records(const double *qD, const double *qHd, const doubl
                     }
                     int64_t o = ((int64_t)s * nvec + b) * 32 + 2 * (4 * si + sj) + ri;
                     acc += src[o];
-                    if (isH) acc += qHa[o];
+                    if (isH) acc += qHa[hoff + o];
                 }
         }
     }
@@ -934,9 +995,13 @@ struct gf_plan {
     u64 N;
     int ctas;
     std::vector<SlotInfo> slots;
-    std::vector<Mat4> G, Gd, Gt, Gc, Z, Zt;  // per slot, normalised orientation
+    std::vector<Mat4> G, Gd, Gt, Gc, Z, Zt;  // per slot, normalised orientation (direction 0)
     std::vector<char> spG, spZ;
     bool have_z = false;
+    int nd = 1;                                           // HVP directions per sweep
+    std::vector<Mat4> Zm[FMAXDIR], Ztm[FMAXDIR];          // per direction, per slot
+    std::vector<char> spZm[FMAXDIR], nzZm[FMAXDIR];       // parity zeros / any nonzero
+    int aux_dirs = 1;                                     // directions the aux workspace holds
     double2 *psi = nullptr, *bra = nullptr, *aux = nullptr;
     double *partD = nullptr, *partHd = nullptr, *partHa = nullptr, *partV = nullptr;
     double *qD = nullptr, *qHd = nullptr, *qHa = nullptr, *qV = nullptr;
@@ -1172,24 +1237,62 @@ extern "C" int gf_plan_set_gates(gf_plan *p, const double *mats)
     return GF_OK;
 }
 
-extern "C" int gf_plan_set_directions(gf_plan *p, const double *zmats)
+// nd HVP directions [nd][n_logical][4][4] evaluated in one set of sweeps
+// (the fused engine shares psi / bra across them: full-Hessian columns).
+extern "C" int gf_plan_set_directions_multi(gf_plan *p, int nd, const double *zmats)
 {
     if (!p || !zmats) return gf_fail(GF_EINVAL, "null argument");
-    p->Z.resize(p->n); p->Zt.resize(p->n);
-    p->spZ.assign(p->n, 0);
-    for (int s = 0; s < p->n; ++s) {
-        Mat4 z = to_mat4(zmats + 32 * p->slots[s].logical);
-        if (p->slots[s].swapped) z = wire_swap(z);
-        if (p->sector >= 0 && !parity_zeros(z))
-            return gf_fail(GF_EINVAL, "sector-compressed HVP needs parity-conserving directions (slot %d)", s);
-        p->Z[s] = z;
-        p->Zt[s] = transpose(z);
-        p->spZ[s] = parity_zeros(z);
+    if (nd < 1 || nd > FMAXDIR) return gf_fail(GF_EINVAL, "direction count %d outside [1, %d]", nd, FMAXDIR);
+    if (nd > 1 && !p->fused) return gf_fail(GF_EINVAL, "multi-direction HVP needs the fused engine");
+    if (nd > p->aux_dirs) {
+        // grow the per-direction workspace (chi / v vectors and HVP partials)
+        const size_t vbytes = sizeof(double2) * p->N * (size_t)p->max_batch;
+        const size_t pbytes = sizeof(double) * 32 * (size_t)p->ctas * p->max_batch * std::max(1, p->n);
+        const size_t qbytes = sizeof(double) * 32 * (size_t)p->max_batch * std::max(1, p->n);
+        double2 *aux = nullptr;
+        double *phd = nullptr, *pha = nullptr, *qhd = nullptr, *qha = nullptr;
+        cudaError_t e = cudaMalloc(&aux, vbytes * nd);
+        if (e == cudaSuccess) e = cudaMalloc(&phd, pbytes * nd);
+        if (e == cudaSuccess) e = cudaMalloc(&pha, pbytes * nd);
+        if (e == cudaSuccess) e = cudaMalloc(&qhd, qbytes * nd);
+        if (e == cudaSuccess) e = cudaMalloc(&qha, qbytes * nd);
+        if (e != cudaSuccess) {
+            cudaFree(aux); cudaFree(phd); cudaFree(pha); cudaFree(qhd); cudaFree(qha);
+            cudaGetLastError();
+            return gf_fail(GF_ENOMEM, "direction workspace: %s", cudaGetErrorString(e));
+        }
+        cudaFree(p->aux); cudaFree(p->partHd); cudaFree(p->partHa); cudaFree(p->qHd); cudaFree(p->qHa);
+        p->aux = aux; p->partHd = phd; p->partHa = pha; p->qHd = qhd; p->qHa = qha;
+        p->aux_dirs = nd;
     }
+    for (int d = 0; d < nd; ++d) {
+        p->Zm[d].resize(p->n); p->Ztm[d].resize(p->n);
+        p->spZm[d].assign(p->n, 0); p->nzZm[d].assign(p->n, 0);
+        for (int s = 0; s < p->n; ++s) {
+            Mat4 z = to_mat4(zmats + 32 * (size_t)(d * p->nlog + p->slots[s].logical));
+            if (p->slots[s].swapped) z = wire_swap(z);
+            if (p->sector >= 0 && !parity_zeros(z))
+                return gf_fail(GF_EINVAL, "sector-compressed HVP needs parity-conserving directions (slot %d)", s);
+            bool nz = false;
+            for (int q = 0; q < 16; ++q) nz = nz || z.m[q].x != 0.0 || z.m[q].y != 0.0;
+            p->Zm[d][s] = z;
+            p->Ztm[d][s] = transpose(z);
+            p->spZm[d][s] = parity_zeros(z);
+            p->nzZm[d][s] = nz;
+        }
+    }
+    p->Z = p->Zm[0];
+    p->Zt = p->Ztm[0];
+    p->spZ = p->spZm[0];
+    p->nd = nd;
     p->have_z = true;
     return GF_OK;
 }
 
+extern "C" int gf_plan_set_directions(gf_plan *p, const double *zmats)
+{
+    return gf_plan_set_directions_multi(p, 1, zmats);
+}
 
 // ---------------------------------------------------------------------------
 // Fused pass planning: greedy over the sweep order.  A slot joins the current
@@ -1280,28 +1383,28 @@ static std::vector<FusedParams> plan_passes(const gf_plan *p, bool reverse)
     return out;
 }
 
-static size_t fused_smem(int nv, int m, int c, int nw)
+static size_t fused_smem(int nv, int m, int c, int nw, int nd = 1)
 {
-    return sizeof(double2) * ((size_t)nv << m) + sizeof(double) * (2 * nw * 64 + FMAXSLOTS * 2 * 32) +
+    return sizeof(double2) * ((size_t)nv << m) + sizeof(double) * ((1 + nd) * nw * 64 + FMAXSLOTS * (1 + nd) * 32) +
            sizeof(unsigned long long) * ((size_t)1 << (m - c));
 }
 
-template <int OP, bool FIRST, int NT>
+template <int OP, bool FIRST, int NT, int ND>
 static int launch_fused_nt(const gf_plan *p, FusedParams &fp, int64_t nvec, cudaStream_t st)
 {
-    const int nv = (OP == OP_FWD || OP == OP_FWD_DOT) ? 1 : (OP == OP_REV_G ? 2 : 3);
-    const size_t smem = fused_smem(nv, fp.m, fp.c, NT / 32);
+    const int nv = (OP == OP_FWD || OP == OP_FWD_DOT) ? 1 : (OP == OP_REV_G ? 2 : 2 + ND);
+    const size_t smem = fused_smem(nv, fp.m, fp.c, NT / 32, ND);
     static bool attr_done = false;
     if (!attr_done) {
         // 226 KB: the opt-in limit (227 KB) minus the kernel's static shared memory
-        cudaError_t ae = cudaFuncSetAttribute(k_fused<OP, FIRST, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              226 * 1024);
+        cudaError_t ae = cudaFuncSetAttribute(k_fused<OP, FIRST, NT, ND>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
         if (ae != cudaSuccess) return gf_fail(GF_ECUDA, "k_fused smem attribute: %s", cudaGetErrorString(ae));
         attr_done = true;
     }
     if (smem > 226 * 1024) return gf_fail(GF_EINVAL, "fused tile needs %zu B of shared memory", smem);
     dim3 grid(p->ctas, (unsigned)nvec);
-    k_fused<OP, FIRST, NT><<<grid, NT, smem, st>>>(fp);
+    k_fused<OP, FIRST, NT, ND><<<grid, NT, smem, st>>>(fp);
     return GF_OK;
 }
 
@@ -1329,13 +1432,18 @@ static int launch_pipe(const gf_plan *p, FusedParams &fp, int64_t nvec, cudaStre
 }
 
 // 256 threads (2 CTAs/SM) for tiles up to 2^11; 512 threads (1 CTA/SM, same 16
-// warps per SM) for 2^12 tiles
+// warps per SM) for 2^12 tiles and for multi-direction HVP sweeps (2 + ND
+// vectors per tile)
 template <int OP, bool FIRST>
-static int launch_fused(const gf_plan *p, FusedParams &fp, int64_t nvec, cudaStream_t st)
+static int launch_fused(const gf_plan *p, FusedParams &fp, int64_t nvec, cudaStream_t st, int nd = 1)
 {
+    if (nd >= 2 && (OP == OP_REV_GH || OP == OP_ASC_H)) {
+        if (nd == 2) return launch_fused_nt<OP, FIRST, 512, 2>(p, fp, nvec, st);
+        return launch_fused_nt<OP, FIRST, 512, 3>(p, fp, nvec, st);
+    }
     if (p->pipe) return launch_pipe<OP, FIRST>(p, fp, nvec, st);
-    if (fp.m >= 12) return launch_fused_nt<OP, FIRST, 512>(p, fp, nvec, st);
-    return launch_fused_nt<OP, FIRST, 256>(p, fp, nvec, st);
+    if (fp.m >= 12) return launch_fused_nt<OP, FIRST, 512, 1>(p, fp, nvec, st);
+    return launch_fused_nt<OP, FIRST, 256, 1>(p, fp, nvec, st);
 }
 
 static int collect_phases(gf_plan *p);
@@ -1369,6 +1477,8 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
     if (!(flags & (GF_VALUE | GF_GRAD | GF_HVP))) return gf_fail(GF_EINVAL, "empty flags");
     cudaStream_t st = (cudaStream_t)stream;
     const int n = p->n;
+    const int nd = (flags & GF_HVP) ? p->nd : 1;
+    if (nd > 1 && !p->fused) return gf_fail(GF_EINVAL, "multi-direction HVP needs the fused engine");
     int64_t launches = 0;
     SweepParams sp;
     memset(&sp, 0, sizeof sp);
@@ -1421,6 +1531,9 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
             f.tickets = p->tickets;
             f.basis = basis;
             f.store_mask = 7;
+            f.auxstride = p->N * (u64)p->max_batch;
+            f.hstride = (u64)std::max(1, p->n) * p->max_batch * p->ctas * 32;
+            f.qhstride = (u64)std::max(1, p->n) * p->max_batch * 32;
             if (exp_noslots) f.nslots = 0;
         };
         const int nf = (int)p->fwd_passes.size(), nr = (int)p->rev_passes.size();
@@ -1458,16 +1571,23 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
                     const int s = fp.ps[t].slot;
                     fp.mat[t][0] = p->Gd[s];
                     fp.mat[t][1] = p->Gt[s];
-                    if (h) fp.mat[t][2] = p->Zt[s];
-                    bool sp = p->spG[s] && (!h || p->spZ[s]);
+                    bool sp = p->spG[s];
+                    fp.ps[t].zmask = 0;
+                    if (h) {
+                        for (int d = 0; d < nd; ++d) {
+                            fp.mat[t][2 + d] = p->Ztm[d][s];
+                            sp = sp && p->spZm[d][s];
+                            fp.ps[t].zmask |= p->nzZm[d][s] ? (1 << d) : 0;
+                        }
+                    }
                     if (fp.ps[t].mode != PM_C1Q) fp.ps[t].mode = sp ? PM_SPARSE : PM_DENSE;
                 }
                 // after the reverse sweep psi_0 = |j> is known exactly and chi is dead:
                 // the last pass writes back only the bra (needed by the ascending sweep)
                 if (pi == nr - 1) fp.store_mask = h ? 2 : 0;
                 if (h) {
-                    if (pi == 0) { int rc_ = launch_fused<OP_REV_GH, true>(p, fp, nvec, st); if (rc_) return rc_; }
-                    else { int rc_ = launch_fused<OP_REV_GH, false>(p, fp, nvec, st); if (rc_) return rc_; }
+                    if (pi == 0) { int rc_ = launch_fused<OP_REV_GH, true>(p, fp, nvec, st, nd); if (rc_) return rc_; }
+                    else { int rc_ = launch_fused<OP_REV_GH, false>(p, fp, nvec, st, nd); if (rc_) return rc_; }
                 } else {
                     if (pi == 0) { int rc_ = launch_fused<OP_REV_G, true>(p, fp, nvec, st); if (rc_) return rc_; }
                     else { int rc_ = launch_fused<OP_REV_G, false>(p, fp, nvec, st); if (rc_) return rc_; }
@@ -1486,13 +1606,18 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
                         const int s = fp.ps[t].slot;
                         fp.mat[t][0] = p->Gc[s];
                         fp.mat[t][1] = p->G[s];
-                        fp.mat[t][2] = p->Z[s];
-                        bool sp = p->spG[s] && p->spZ[s];
+                        bool sp = p->spG[s];
+                        fp.ps[t].zmask = 0;
+                        for (int d = 0; d < nd; ++d) {
+                            fp.mat[t][2 + d] = p->Zm[d][s];
+                            sp = sp && p->spZm[d][s];
+                            fp.ps[t].zmask |= p->nzZm[d][s] ? (1 << d) : 0;
+                        }
                         if (fp.ps[t].mode != PM_C1Q) fp.ps[t].mode = sp ? PM_SPARSE : PM_DENSE;
                     }
                     if (pi == nr - 1) fp.store_mask = 0;  // nothing is read after the ascending sweep
-                    if (pi == 0) { int rc_ = launch_fused<OP_ASC_H, true>(p, fp, nvec, st); if (rc_) return rc_; }
-                    else { int rc_ = launch_fused<OP_ASC_H, false>(p, fp, nvec, st); if (rc_) return rc_; }
+                    if (pi == 0) { int rc_ = launch_fused<OP_ASC_H, true>(p, fp, nvec, st, nd); if (rc_) return rc_; }
+                    else { int rc_ = launch_fused<OP_ASC_H, false>(p, fp, nvec, st, nd); if (rc_) return rc_; }
                     ++launches;
                 }
             }
@@ -1572,13 +1697,14 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
     }
     {
         int64_t nchunks = (nvec + p->chunk - 1) / p->chunk;
-        int rec = 2 + 64 * p->nlog;
+        int rec = 2 + 32 * p->nlog * (1 + nd);
         int64_t tot = nchunks * rec;
         int eff = (n > 0) ? flags : (flags & GF_VALUE);
         const bool fusedV = p->fused && n > 0;
         k_chunk_records<<<(unsigned)((tot * 32 + 255) / 256), 256, 0, st>>>(
             p->qD, p->qHd, p->qHa, fusedV ? p->qV : p->partV, nvec, fusedV ? 1 : p->ctas, n, p->nlog, p->d_lstart,
-            p->d_lslots, p->d_swapped, p->chunk, eff, p->sector >= 0, out);
+            p->d_lslots, p->d_swapped, p->chunk, eff, p->sector >= 0, nd,
+            (int64_t)std::max(1, p->n) * p->max_batch * 32, out);
         ++launches;
     }
     if (p->profiling) {

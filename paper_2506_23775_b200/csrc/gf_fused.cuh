@@ -22,6 +22,7 @@ constexpr int FT = 256;         // threads per fused CTA (8 warps)
 constexpr int FMAXM = 12;       // max local bits
 constexpr int FMAXSLOTS = 14;   // max slots per pass (2 CTAs/SM of m=11 tiles fit 14)
 constexpr int FMAXGLOB = 40;
+constexpr int FMAXDIR = 3;      // HVP directions per sweep (full-Hessian columns)
 
 enum { PM_DENSE = 0, PM_SPARSE = 1, PM_C1Q = 2 };
 
@@ -30,6 +31,7 @@ struct PassSlot {
     int mode;  // PM_*
     int llo;   // local bit index of the low target bit (c1q: the explicit qubit)
     int lhi;   // local bit index of the high target bit (unused for c1q)
+    int zmask; // bit d: direction d has a nonzero Z at this slot (zero Z-terms are skipped)
 };
 
 struct FusedParams {
@@ -46,10 +48,13 @@ struct FusedParams {
     int nvec, ctas, sector;
     int m, c, nglob, nslots;
     int store_mask;  // bit 0 psi, bit 1 bra, bit 2 chi/v: vectors written back after the pass
+    unsigned long long auxstride; // aux (chi / v) offset between directions (amplitudes)
+    unsigned long long hstride;   // partH / qH offset between directions (doubles)
+    unsigned long long qhstride;
     int lpos[FMAXM];
     int gpos[FMAXGLOB];
     PassSlot ps[FMAXSLOTS];
-    Mat4 mat[FMAXSLOTS][3];  // per op: FWD {G}; REV {G^dag, G^T, Z^T}; ASC {conj G, G, Z}
+    Mat4 mat[FMAXSLOTS][2 + FMAXDIR];  // FWD {G}; REV {G^dag, G^T, Z_d^T...}; ASC {conj G, G, Z_d...}
 };
 
 }  // namespace gf

@@ -52,6 +52,7 @@ __all__ = [
     "gradient_and_hvp",
     "full_hessian",
     "hessian_vector_product",
+    "hessian_vector_products",
     "build_pass_cache",
     "parallel_reduce",
     "chunk_bounds",
@@ -192,6 +193,7 @@ class EnginePlan:
         self.n = circuit.num_slots
         self.N = 1 << (self.k - (1 if sector >= 0 else 0))
         self.rec = 2 + 64 * self.nlog
+        self.nd = 1
         h = ctypes.c_void_p()
         self._keep = (t1, t2, lid)
         with torch.cuda.device(torch.cuda.current_device()):
@@ -205,8 +207,13 @@ class EnginePlan:
         _lib.check(_lib.lib.gf_plan_set_gates(self.h, m.ctypes.data))
 
     def set_directions(self, zmats: np.ndarray):
+        """[n_logical, 4, 4] (one direction) or [nd, n_logical, 4, 4] (nd <= 3
+        directions evaluated in one set of sweeps)."""
         z = np.ascontiguousarray(zmats, dtype=np.complex128)
-        _lib.check(_lib.lib.gf_plan_set_directions(self.h, z.ctypes.data))
+        nd = 1 if z.ndim == 3 else z.shape[0]
+        _lib.check(_lib.lib.gf_plan_set_directions_multi(self.h, nd, z.ctypes.data))
+        self.nd = nd
+        self.rec = 2 + 32 * self.nlog * (1 + nd)
 
     def eval(self, flags, nvec, basis, weights, phi0, out):
         _lib.check(_lib.lib.gf_plan_eval(self.h, flags, nvec, basis.data_ptr(),
@@ -394,6 +401,8 @@ class _Run:
         self.plan.set_gates(circuit.gate_stack())
         if flags & _lib.GF_HVP:
             self.plan.set_directions(directions)
+        self.nd = self.plan.nd if flags & _lib.GF_HVP else 1
+        self.rec = 2 + 32 * circuit.num_logical * (1 + self.nd)
         self.oracle = oracle
 
     def run(self):
@@ -401,7 +410,7 @@ class _Run:
         total, chunk = self.spec.total, self.chunk
         nchunks = (total + chunk - 1) // chunk
         lo, hi = shard_chunks(nchunks, self.rank, self.world)
-        rec = self.plan.rec
+        rec = self.rec
         local = torch.zeros((hi - lo, rec), dtype=torch.float64, device=dev)
         phi0 = torch.empty((self.batch, self.N), dtype=torch.complex128, device=dev)
         idx_all = None if self.spec.indices is None else torch.from_numpy(self.spec.indices).to(dev)
@@ -435,8 +444,8 @@ class _Run:
         nlog = self.circuit.num_logical
         value = complex(tot[0], tot[1])
         d = tot[2:2 + 32 * nlog].view(np.complex128).reshape(nlog, 4, 4).copy()
-        h = tot[2 + 32 * nlog:].view(np.complex128).reshape(nlog, 4, 4).copy()
-        return value, d, h
+        hs = tot[2 + 32 * nlog:].view(np.complex128).reshape(self.nd, nlog, 4, 4).copy()
+        return value, d, (hs[0] if self.nd == 1 else hs)
 
     def _fill_phi0(self, basis: torch.Tensor, out: torch.Tensor):
         if self.sector >= 0:
@@ -558,6 +567,33 @@ def gradient_and_hvp(circuit: Circuit, oracle, directions, parity_mode: bool = F
     return rep, [h[i] for i in range(circuit.num_logical)]
 
 
+def hessian_vector_products(circuit: Circuit, oracle, direction_sets, *, sector=None, fold=False, basis=None,
+                            batch=None, chunk=None, distributed=None):
+    """Several HVPs with shared forward / reverse state sweeps: up to 3
+    directions per set of sweeps on the fused engine (the full-Hessian
+    columns).  Returns one list of per-logical 4x4 results per direction."""
+    _check_oracle(circuit, oracle)
+    zs = [_slot_directions(circuit, d) for d in direction_sets]
+    out = []
+    i = 0
+    while i < len(zs):
+        group = zs[i:i + 3]
+        z = np.ascontiguousarray(np.stack(group)) if len(group) > 1 else group[0]
+        try:
+            run = _Run(circuit, oracle, _lib.GF_HVP, z, sector, fold, basis, batch, chunk, distributed)
+        except ValueError:
+            if len(group) == 1:
+                raise
+            # the streaming engine (tiny state spaces) evaluates one direction per sweep
+            group = group[:1]
+            run = _Run(circuit, oracle, _lib.GF_HVP, group[0], sector, fold, basis, batch, chunk, distributed)
+        _, _, h = run.run()
+        hs = [h] if len(group) == 1 else list(h)
+        out += [[x[j] for j in range(circuit.num_logical)] for x in hs]
+        i += len(group)
+    return out
+
+
 def hessian_vector_product(circuit: Circuit, oracle, directions, workers: int | None = None, *, sector=None,
                            fold=False, basis=None, batch=None, chunk=None, distributed=None):
     """Holomorphic H~ . vec(Z) per logical gate (reference objective.py:770-814)."""
@@ -599,15 +635,19 @@ def full_hessian(circuit: Circuit, oracle, use_translation_dedup: bool = False, 
     sup = PARITY_SUPPORT if parity_mode else DENSE_SUPPORT
     nlog = circuit.num_logical
     used = _used_routes(circuit)
-    cols = {}
+    keys, dirs = [], []
     for b in range(nlog):
         if not any(b in key for key in used):
             continue
         for jj, e in enumerate(sup):
-            z = [np.zeros((4, 4), dtype=np.complex128) for _ in range(nlog)]
+            z = np.zeros((nlog, 4, 4), dtype=np.complex128)
             z[b].reshape(16)[e] = 1.0
-            cols[(b, jj)] = hessian_vector_product(circuit, oracle, z, sector=sector, fold=fold, basis=basis,
-                                                   batch=batch, chunk=chunk, distributed=distributed)
+            keys.append((b, jj))
+            dirs.append(z)
+    # columns in sweeps of up to 3 unit directions sharing the psi / bra work
+    res = hessian_vector_products(circuit, oracle, dirs, sector=sector, fold=fold, basis=basis, batch=batch,
+                                  chunk=chunk, distributed=distributed)
+    cols = dict(zip(keys, res))
     blocks = {}
     for a, b in sorted(used):
         blk = np.empty((sup.size, sup.size), dtype=np.complex128)

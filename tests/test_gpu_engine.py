@@ -408,3 +408,24 @@ def test_integration_stub_matches_reference_chunk_drivers():
         dsum = dsum + dacc
     assert abs(-vals.real - g["value"]) < TOL * abs(g["value"])
     assert rel_err(plan.logical_sum(dsum.reshape(-1, 16)), g["holo"]) < TOL
+
+
+@pytest.mark.parametrize("sector,m", [(None, None), (0, None), (None, "7")])
+def test_multi_direction_hvp_equals_single(monkeypatch, sector, m):
+    """gf_plan_set_directions_multi: 3 directions in one set of sweeps give the
+    same HVPs as three separate evaluations (full space, sector with
+    parity-controlled slots, forced small tiles)."""
+    if m:
+        monkeypatch.setenv("GF_FUSED_M", m)
+    parity = sector is not None
+    spec, circ, rng = gf.spinful_layer_circuit(5, 4, False, seed=21, parity=parity)
+    orc = gf.DenseOracle(spec, 0.25)
+    dirs = []
+    for _ in range(3):
+        dirs.append([manifold.project_tangent_gate(g.matrix, rng.normal(size=(4, 4)) + 1j * rng.normal(size=(4, 4)),
+                                                   parity) for g in circ.logical_gates])
+    dirs[2][1] = np.zeros((4, 4), complex)  # a zero logical block exercises the skipped Z-terms
+    multi = gf.hessian_vector_products(circ, orc, dirs, sector=sector)
+    for z, got in zip(dirs, multi):
+        one = gf.hessian_vector_product(circ, orc, z, sector=sector)
+        assert rel_err(np.stack(got), np.stack(one)) < 1e-12
