@@ -282,7 +282,7 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
     for (int si = 0; si < p.nslots; ++si) {
         const int mode = p.ps[si].mode;
         const int llo = p.ps[si].llo, lhi = p.ps[si].lhi;
-        const int zmask = p.ps[si].zmask;
+        const int zmask = p.ps[si].zmask, amask = p.ps[si].amask;
         const Mat4 &MA = p.mat[si][0];
         const Mat4 &MB = p.mat[si][1];
         const bool c1q = (mode == PM_C1Q);
@@ -325,12 +325,14 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                             dmma(cD0, cD1, li >= 0 ? d1[o] : 0.0, k);
                             if constexpr (HH) {
 #pragma unroll
-                                for (int d = 0; d < ND; ++d) dmma(cH0[d], cH1[d], li >= 0 ? d2[2 * d * T + o] : 0.0, k);
+                                for (int d = 0; d < ND; ++d)
+                                    if ((amask >> d) & 1) dmma(cH0[d], cH1[d], li >= 0 ? d2[2 * d * T + o] : 0.0, k);
                             }
                         } else {
                             const double bq = li >= 0 ? d1[o] : 0.0;
 #pragma unroll
-                            for (int d = 0; d < ND; ++d) dmma(cH0[d], cH1[d], bq, li >= 0 ? d2[2 * d * T + o] : 0.0);
+                            for (int d = 0; d < ND; ++d)
+                                if ((amask >> d) & 1) dmma(cH0[d], cH1[d], bq, li >= 0 ? d2[2 * d * T + o] : 0.0);
                         }
                     }
                     __syncwarp();
@@ -344,10 +346,12 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                             if constexpr (OP == OP_REV_GH) {
 #pragma unroll
                                 for (int d = 0; d < ND; ++d) {
+                                    const bool act = (amask >> d) & 1, zz = (zmask >> d) & 1;
+                                    if (!act && !zz) continue;  // chi_d stays exactly zero
                                     double2 *X = t2 + d * T;
-                                    double2 cc[2] = {X[l0], X[l1]}, cn[2];
-                                    mv2(MB, P, cc, cn);
-                                    if ((zmask >> d) & 1) mv2_acc(p.mat[si][2 + d], P, b, cn);
+                                    double2 cc[2] = {X[l0], X[l1]}, cn[2] = {czero(), czero()};
+                                    if (act) mv2(MB, P, cc, cn);
+                                    if (zz) mv2_acc(p.mat[si][2 + d], P, b, cn);
                                     X[l0] = cn[0];
                                     X[l1] = cn[1];
                                 }
@@ -359,10 +363,12 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                             double2 x[2] = {t0[l0], t0[l1]}, y[2];
 #pragma unroll
                             for (int d = 0; d < ND; ++d) {
+                                const bool act = (amask >> d) & 1, zz = (zmask >> d) & 1;
+                                if (!act && !zz) continue;  // v_d stays exactly zero
                                 double2 *X = t2 + d * T;
-                                double2 v[2] = {X[l0], X[l1]}, vn[2];
-                                mv2(MB, P, v, vn);
-                                if ((zmask >> d) & 1) mv2_acc(p.mat[si][2 + d], P, x, vn);
+                                double2 v[2] = {X[l0], X[l1]}, vn[2] = {czero(), czero()};
+                                if (act) mv2(MB, P, v, vn);
+                                if (zz) mv2_acc(p.mat[si][2 + d], P, x, vn);
                                 X[l0] = vn[0];
                                 X[l1] = vn[1];
                             }
@@ -430,6 +436,7 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                             if constexpr (HH) {
 #pragma unroll
                                 for (int d = 0; d < ND; ++d) {
+                                    if (!((amask >> d) & 1)) continue;
                                     dmma(cH0[d], cH1[d], d2[2 * d * T + o0], k0);
                                     dmma(eH0[d], eH1[d], d2[2 * d * T + o1], k1);
                                 }
@@ -438,6 +445,7 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                             const double b0 = d1[o0], b1 = d1[o1];
 #pragma unroll
                             for (int d = 0; d < ND; ++d) {
+                                if (!((amask >> d) & 1)) continue;
                                 dmma(cH0[d], cH1[d], b0, d2[2 * d * T + o0]);
                                 dmma(eH0[d], eH1[d], b1, d2[2 * d * T + o1]);
                             }
@@ -468,9 +476,11 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                             if constexpr (OP == OP_REV_GH) {
 #pragma unroll
                                 for (int d = 0; d < ND; ++d) {
+                                    const bool act = (amask >> d) & 1, zz = (zmask >> d) & 1;
                                     double2 *X = t2 + d * T;
-                                    X[ad] = ((zmask >> d) & 1) ? dmma_mv2(X[ad], fb0, fb1, bb, fc0[d], fc1[d])
-                                                               : dmma_mv(X[ad], fb0, fb1);
+                                    if (act && zz) X[ad] = dmma_mv2(X[ad], fb0, fb1, bb, fc0[d], fc1[d]);
+                                    else if (act) X[ad] = dmma_mv(X[ad], fb0, fb1);
+                                    else if (zz) X[ad] = dmma_mv(bb, fc0[d], fc1[d]);
                                 }
                             }
                             t1[ad] = dmma_mv(bb, fb0, fb1);
@@ -478,9 +488,11 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                             const double2 x = t0[ad];
 #pragma unroll
                             for (int d = 0; d < ND; ++d) {
+                                const bool act = (amask >> d) & 1, zz = (zmask >> d) & 1;
                                 double2 *X = t2 + d * T;
-                                X[ad] = ((zmask >> d) & 1) ? dmma_mv2(X[ad], fb0, fb1, x, fc0[d], fc1[d])
-                                                           : dmma_mv(X[ad], fb0, fb1);
+                                if (act && zz) X[ad] = dmma_mv2(X[ad], fb0, fb1, x, fc0[d], fc1[d]);
+                                else if (act) X[ad] = dmma_mv(X[ad], fb0, fb1);
+                                else if (zz) X[ad] = dmma_mv(x, fc0[d], fc1[d]);
                             }
                             t0[ad] = dmma_mv(x, fb0, fb1);
                         }
@@ -1560,6 +1572,7 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
         if (p->profiling) GF_CUDA(cudaEventRecord(p->ev[1], st));
         if (grad_like) {
             const bool h = (flags & GF_HVP) != 0;
+            int act_rev = 0;  // directions whose chi is nonzero entering the next slot
             for (int pi = 0; pi < nr; ++pi) {
                 fp = p->rev_passes[pi];
                 setup(fp);
@@ -1580,6 +1593,8 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
                             fp.ps[t].zmask |= p->nzZm[d][s] ? (1 << d) : 0;
                         }
                     }
+                    fp.ps[t].amask = act_rev;
+                    act_rev |= fp.ps[t].zmask;
                     if (fp.ps[t].mode != PM_C1Q) fp.ps[t].mode = sp ? PM_SPARSE : PM_DENSE;
                 }
                 // after the reverse sweep psi_0 = |j> is known exactly and chi is dead:
@@ -1597,6 +1612,7 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
             l_rev = launches - l_fwd;
             if (p->profiling) GF_CUDA(cudaEventRecord(p->ev[2], st));
             if (h) {
+                int act_asc = 0;  // directions whose v is nonzero entering the next slot
                 for (int pi = 0; pi < nr; ++pi) {
                     fp = p->asc_passes[pi];
                     setup(fp);
@@ -1613,6 +1629,8 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
                             sp = sp && p->spZm[d][s];
                             fp.ps[t].zmask |= p->nzZm[d][s] ? (1 << d) : 0;
                         }
+                        fp.ps[t].amask = act_asc;
+                        act_asc |= fp.ps[t].zmask;
                         if (fp.ps[t].mode != PM_C1Q) fp.ps[t].mode = sp ? PM_SPARSE : PM_DENSE;
                     }
                     if (pi == nr - 1) fp.store_mask = 0;  // nothing is read after the ascending sweep

@@ -32,6 +32,7 @@ struct PassSlot {
     int llo;   // local bit index of the low target bit (c1q: the explicit qubit)
     int lhi;   // local bit index of the high target bit (unused for c1q)
     int zmask; // bit d: direction d has a nonzero Z at this slot (zero Z-terms are skipped)
+    int amask; // bit d: chi_d / v_d is nonzero entering this slot (else its hole and update are skipped)
 };
 
 struct FusedParams {
