@@ -1450,6 +1450,10 @@ template <int OP, bool FIRST>
 static int launch_fused(const gf_plan *p, FusedParams &fp, int64_t nvec, cudaStream_t st, int nd = 1)
 {
     if (nd >= 2 && (OP == OP_REV_GH || OP == OP_ASC_H)) {
+        if (fp.m <= 10) {  // 2^10 tiles: 2 + ND vectors fit 2 CTAs/SM at 256 threads
+            if (nd == 2) return launch_fused_nt<OP, FIRST, 256, 2>(p, fp, nvec, st);
+            return launch_fused_nt<OP, FIRST, 256, 3>(p, fp, nvec, st);
+        }
         if (nd == 2) return launch_fused_nt<OP, FIRST, 512, 2>(p, fp, nvec, st);
         return launch_fused_nt<OP, FIRST, 512, 3>(p, fp, nvec, st);
     }
