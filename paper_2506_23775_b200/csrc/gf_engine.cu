@@ -397,7 +397,21 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                     return a;
                 };
                 double2 *V = (OP == OP_ASC_H) ? t1 : t0;
-                {
+                const bool sparse = (mode == PM_SPARSE);
+                if (sparse) {
+                    // parity-conserving gates: half of G is structural zeros, so the
+                    // sparse FMA form does half the flops of the dense DMMA form
+                    for (unsigned j = lane; j < TW; j += 32) {
+                        const unsigned b0 = ins0u(ins0u(wbase + j, llo), lhi);
+                        const unsigned L[4] = {swz(b0), swz(b0 + olo), swz(b0 + ohi), swz(b0 + olo + ohi)};
+                        double2 x[4], y[4];
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) x[i] = V[L[i]];
+                        mv4<true>(MA, x, y);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) V[L[i]] = y[i];
+                    }
+                } else {
                     double fa0, fa1;
                     gate_frag(MA, g, tq, fa0, fa1);
 #pragma unroll 8
@@ -460,7 +474,61 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                     }
                     __syncwarp();
                 }
-                if constexpr (OP != OP_FWD && OP != OP_FWD_DOT) {
+                if constexpr (OP != OP_FWD && OP != OP_FWD_DOT) if (sparse) {
+                    for (unsigned j = lane; j < TW; j += 32) {
+                        const unsigned b0 = ins0u(ins0u(wbase + j, llo), lhi);
+                        const unsigned L[4] = {swz(b0), swz(b0 + olo), swz(b0 + ohi), swz(b0 + olo + ohi)};
+                        if constexpr (REV) {
+                            double2 bb[4], bn[4];
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) bb[i] = t1[L[i]];
+                            if constexpr (OP == OP_REV_GH) {
+#pragma unroll
+                                for (int d = 0; d < ND; ++d) {
+                                    const bool act = (amask >> d) & 1, zz = (zmask >> d) & 1;
+                                    if (!act && !zz) continue;
+                                    double2 *X = t2 + d * T;
+                                    double2 cc[4], cn[4];
+#pragma unroll
+                                    for (int i = 0; i < 4; ++i) {
+                                        cc[i] = X[L[i]];
+                                        cn[i] = czero();
+                                    }
+                                    if (act) mv4<true>(MB, cc, cn);
+                                    if (zz) mv4_acc<true>(p.mat[si][2 + d], bb, cn);
+#pragma unroll
+                                    for (int i = 0; i < 4; ++i) X[L[i]] = cn[i];
+                                }
+                            }
+                            mv4<true>(MB, bb, bn);
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) t1[L[i]] = bn[i];
+                        } else {
+                            double2 x[4], y[4];
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) x[i] = t0[L[i]];
+#pragma unroll
+                            for (int d = 0; d < ND; ++d) {
+                                const bool act = (amask >> d) & 1, zz = (zmask >> d) & 1;
+                                if (!act && !zz) continue;
+                                double2 *X = t2 + d * T;
+                                double2 v[4], vn[4];
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) {
+                                    v[i] = X[L[i]];
+                                    vn[i] = czero();
+                                }
+                                if (act) mv4<true>(MB, v, vn);
+                                if (zz) mv4_acc<true>(p.mat[si][2 + d], x, vn);
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) X[L[i]] = vn[i];
+                            }
+                            mv4<true>(MB, x, y);
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) t0[L[i]] = y[i];
+                        }
+                    }
+                } else {
                     double fb0, fb1, fc0[ND], fc1[ND];
                     gate_frag(MB, g, tq, fb0, fb1);
 #pragma unroll
