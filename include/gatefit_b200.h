@@ -177,6 +177,22 @@ int gf_cheb_step(const void *t_cur, const void *t_prev, void *t_next, void *acc,
                  const int32_t *tb, const double *coef, const int32_t *hop, int nterms, double scale, double shift,
                  double c_re, double c_im, int64_t nvec, int sector_flags, void *stream);
 
+/* Number-block target oracle: exp(-iHt)|j> inside j's particle-number block
+ * (hopping conserves the occupation of each connected component of the hop
+ * graph).  desc = [k, ncomp, then per component: L, n, qubit_0..qubit_{L-1}];
+ * block vectors are indexed by the mixed-radix colex ranks of the component
+ * patterns.  terms = [kind (0 hop, 1 nn), comp_a, local_a, comp_b, local_b]
+ * per term, coef per term.  gf_nb_cheb_step: one Chebyshev order as in
+ * gf_cheb_step; gf_nb_scatter: block vectors cols[colidx[b]] -> zeroed rows
+ * rows[rowidx[b]], dense (sector -1) or sector-compressed (null maps mean the
+ * identity); gf_nb_rank: block indices of full-space states of the block. */
+int gf_nb_cheb_step(const void *t_cur, const void *t_prev, void *t_next, void *acc, const int32_t *desc, int ndesc,
+                    const int32_t *terms, const double *coef, int nterms, double scale, double shift, double c_re,
+                    double c_im, int64_t nvec, void *stream);
+int gf_nb_scatter(const void *cols, const int64_t *colidx, void *rows, const int64_t *rowidx, int64_t nrows,
+                  int64_t row_len, const int32_t *desc, int ndesc, int sector, void *stream);
+int gf_nb_rank(const int64_t *js, int64_t *out, int64_t n, const int32_t *desc, int ndesc, void *stream);
+
 /* Device-memory helpers for bindings without a tensor library (the ctypes
  * stub of INTEGRATION.md).  gf_memcpy kind: 0 = H2D, 1 = D2H, 2 = D2D
  * (asynchronous on `stream`; pair with gf_stream_sync). */

@@ -266,7 +266,7 @@ __device__ __forceinline__ double2 dmma_mv2(double2 x, double b0, double b1, dou
 // t1 = bra, t2 + d*T = chi_d (REV) / v_d (ASC) for ND directions); hole
 // partials accumulate into sacc[slot][1 + ND][32] (hole 0 = gradient D,
 // hole 1 + d = HVP direction d).
-template <int OP, int NT, int ND>
+template <int OP, int NT, int ND, bool SPX>
 __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, double2 *t1, double2 *t2, double *scratch,
                                           double *sacc, const int tpop, const unsigned T)
 {
@@ -397,7 +397,10 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                     return a;
                 };
                 double2 *V = (OP == OP_ASC_H) ? t1 : t0;
-                const bool sparse = (mode == PM_SPARSE);
+                // SPX: the pass has sparse slots; dense-only passes compile
+                // without the sparse branch (it costs them registers and
+                // scheduling freedom even when never taken)
+                const bool sparse = SPX && (mode == PM_SPARSE);
                 if (sparse) {
                     // parity-conserving gates: half of G is structural zeros, so the
                     // sparse FMA form does half the flops of the dense DMMA form
@@ -601,7 +604,7 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
     }
 }
 
-template <int OP, bool FIRST, int NT, int ND>
+template <int OP, bool FIRST, int NT, int ND, bool SPX>
 __global__ void __launch_bounds__(NT, 512 / NT) k_fused(const FusedParams p)
 {
     constexpr int NW = NT / 32;  // warps per CTA
@@ -676,7 +679,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_fused(const FusedParams p)
         }
         __syncthreads();
 
-        run_slots<OP, NT, ND>(p, t0, t1, t2, scratch, sacc, tpop, T);
+        run_slots<OP, NT, ND, SPX>(p, t0, t1, t2, scratch, sacc, tpop, T);
 
         const int sm = p.store_mask;
         for (unsigned l = tid; l < T; l += NT) {
@@ -874,7 +877,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_fused_pipe(const FusedParams p
             }
             __syncthreads();
         }
-        run_slots<OP, NT, 1>(p, t0, t1, t2, scratch, sacc, __popcll(tile), T);
+        run_slots<OP, NT, 1, true>(p, t0, t1, t2, scratch, sacc, __popcll(tile), T);
         const int sm = p.store_mask;
         for (unsigned l = tid; l < T; l += NT) {
             const u64 a = base + (l & cmask) + hiofs[l >> c];
@@ -1469,7 +1472,7 @@ static size_t fused_smem(int nv, int m, int c, int nw, int nd = 1)
            sizeof(unsigned long long) * ((size_t)1 << (m - c));
 }
 
-template <int OP, bool FIRST, int NT, int ND>
+template <int OP, bool FIRST, int NT, int ND, bool SPX>
 static int launch_fused_nt(const gf_plan *p, FusedParams &fp, int64_t nvec, cudaStream_t st)
 {
     const int nv = (OP == OP_FWD || OP == OP_FWD_DOT) ? 1 : (OP == OP_REV_G ? 2 : 2 + ND);
@@ -1477,14 +1480,14 @@ static int launch_fused_nt(const gf_plan *p, FusedParams &fp, int64_t nvec, cuda
     static bool attr_done = false;
     if (!attr_done) {
         // 226 KB: the opt-in limit (227 KB) minus the kernel's static shared memory
-        cudaError_t ae = cudaFuncSetAttribute(k_fused<OP, FIRST, NT, ND>,
+        cudaError_t ae = cudaFuncSetAttribute(k_fused<OP, FIRST, NT, ND, SPX>,
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
         if (ae != cudaSuccess) return gf_fail(GF_ECUDA, "k_fused smem attribute: %s", cudaGetErrorString(ae));
         attr_done = true;
     }
     if (smem > 226 * 1024) return gf_fail(GF_EINVAL, "fused tile needs %zu B of shared memory", smem);
     dim3 grid(p->ctas, (unsigned)nvec);
-    k_fused<OP, FIRST, NT, ND><<<grid, NT, smem, st>>>(fp);
+    k_fused<OP, FIRST, NT, ND, SPX><<<grid, NT, smem, st>>>(fp);
     return GF_OK;
 }
 
@@ -1514,20 +1517,31 @@ static int launch_pipe(const gf_plan *p, FusedParams &fp, int64_t nvec, cudaStre
 // 256 threads (2 CTAs/SM) for tiles up to 2^11; 512 threads (1 CTA/SM, same 16
 // warps per SM) for 2^12 tiles and for multi-direction HVP sweeps (2 + ND
 // vectors per tile)
+template <int OP, bool FIRST, bool SPX>
+static int launch_fused_sp(const gf_plan *p, FusedParams &fp, int64_t nvec, cudaStream_t st, int nd)
+{
+    if constexpr (OP == OP_REV_GH || OP == OP_ASC_H) {
+        if (nd >= 2) {
+            if (fp.m <= 10) {  // 2^10 tiles: 2 + ND vectors fit 2 CTAs/SM at 256 threads
+                if (nd == 2) return launch_fused_nt<OP, FIRST, 256, 2, SPX>(p, fp, nvec, st);
+                return launch_fused_nt<OP, FIRST, 256, 3, SPX>(p, fp, nvec, st);
+            }
+            if (nd == 2) return launch_fused_nt<OP, FIRST, 512, 2, SPX>(p, fp, nvec, st);
+            return launch_fused_nt<OP, FIRST, 512, 3, SPX>(p, fp, nvec, st);
+        }
+    }
+    if (fp.m >= 12) return launch_fused_nt<OP, FIRST, 512, 1, SPX>(p, fp, nvec, st);
+    return launch_fused_nt<OP, FIRST, 256, 1, SPX>(p, fp, nvec, st);
+}
+
 template <int OP, bool FIRST>
 static int launch_fused(const gf_plan *p, FusedParams &fp, int64_t nvec, cudaStream_t st, int nd = 1)
 {
-    if (nd >= 2 && (OP == OP_REV_GH || OP == OP_ASC_H)) {
-        if (fp.m <= 10) {  // 2^10 tiles: 2 + ND vectors fit 2 CTAs/SM at 256 threads
-            if (nd == 2) return launch_fused_nt<OP, FIRST, 256, 2>(p, fp, nvec, st);
-            return launch_fused_nt<OP, FIRST, 256, 3>(p, fp, nvec, st);
-        }
-        if (nd == 2) return launch_fused_nt<OP, FIRST, 512, 2>(p, fp, nvec, st);
-        return launch_fused_nt<OP, FIRST, 512, 3>(p, fp, nvec, st);
-    }
-    if (p->pipe) return launch_pipe<OP, FIRST>(p, fp, nvec, st);
-    if (fp.m >= 12) return launch_fused_nt<OP, FIRST, 512, 1>(p, fp, nvec, st);
-    return launch_fused_nt<OP, FIRST, 256, 1>(p, fp, nvec, st);
+    if (nd < 2 && p->pipe) return launch_pipe<OP, FIRST>(p, fp, nvec, st);
+    bool spx = false;
+    for (int t = 0; t < fp.nslots; ++t) spx |= (fp.ps[t].mode == PM_SPARSE);
+    if (spx) return launch_fused_sp<OP, FIRST, true>(p, fp, nvec, st, nd);
+    return launch_fused_sp<OP, FIRST, false>(p, fp, nvec, st, nd);
 }
 
 static int collect_phases(gf_plan *p);

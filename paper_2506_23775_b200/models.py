@@ -45,6 +45,7 @@ __all__ = [
     "make_oracle",
     "DenseOracle",
     "ChebyshevOracle",
+    "NumberBlockOracle",
     "KrylovOracle",
     "KrylovConvergenceError",
     "spinful_layer_circuit",
@@ -433,6 +434,140 @@ class ChebyshevOracle:
         self._series(v0, sector, out=out)
 
 
+class NumberBlockOracle(ChebyshevOracle):
+    """exp(-iHt)|j> inside j's particle-number block, on the GPU.
+
+    Hopping terms conserve the occupation of each connected component of the
+    hop graph (each spin chain of the Fermi-Hubbard models, reference
+    models.py:37-45, 247-255), so U|j> is supported on the states with j's
+    particle count per component: C(8,a) C(8,b) <= 4900 of 65536 states at
+    16 qubits.  The same Chebyshev series as :class:`ChebyshevOracle` runs in
+    block coordinates (colex ranks, csrc/gf_target.cu), then the block
+    vectors are scattered into dense (or sector-compressed) rows.  Blocks of
+    dimension <= ``cache_dim`` are expanded once as whole matrices (the
+    series on the identity) and reused for every column of the block; larger
+    blocks run the series on the requested columns only.
+    """
+
+    def __init__(self, spec: HamiltonianSpec, t: float, tol: float = 1e-16, cache_dim: int = 8192):
+        super().__init__(spec, t, tol)
+        k = spec.num_qubits
+        ta, tb, c, h = self._terms
+        parent = list(range(k))
+
+        def find(a):
+            while parent[a] != a:
+                parent[a] = parent[parent[a]]
+                a = parent[a]
+            return a
+
+        for a, b, hop in zip(ta, tb, h):
+            if hop:
+                parent[find(int(a))] = find(int(b))
+        comps = {}
+        for q in range(k):
+            comps.setdefault(find(q), []).append(q)
+        self.components = sorted(comps.values())
+        if len(self.components) > 4 or max(len(cq) for cq in self.components) > 32:
+            raise ValueError("number-block oracle supports <= 4 hop components of <= 32 qubits")
+        where = {}
+        for ci, cq in enumerate(self.components):
+            for i, q in enumerate(cq):
+                where[q] = (ci, i)
+        rows = []
+        for a, b, hop in zip(ta, tb, h):
+            ca, ia = where[int(a)]
+            cb, ib = where[int(b)]
+            rows.append((0 if hop else 1, ca, ia, cb, ib))
+        self._nb_terms = np.ascontiguousarray(np.array(rows, np.int32).reshape(-1, 5))
+        self._nb_coef = np.ascontiguousarray(c, np.float64)
+        self._masks = np.array([sum(1 << (k - 1 - q) for q in cq) for cq in self.components], np.int64)
+        self.cache_dim = int(cache_dim)
+        self._blocks = {}
+
+    def block_of(self, j: int):
+        return tuple(bin(int(j) & int(m)).count("1") for m in self._masks)
+
+    def block_dim(self, counts) -> int:
+        from math import comb
+
+        d = 1
+        for cq, n in zip(self.components, counts):
+            d *= comb(len(cq), n)
+        return d
+
+    def _desc(self, counts):
+        d = [self.num_qubits, len(self.components)]
+        for cq, n in zip(self.components, counts):
+            d += [len(cq), int(n)] + list(cq)
+        return np.ascontiguousarray(np.array(d, np.int32))
+
+    def _block_series(self, desc, v0: torch.Tensor) -> torch.Tensor:
+        """sum conj(c_m) T_m(H~) v0 for block vectors v0 [B, D]."""
+        B = v0.shape[0]
+        acc = v0 * complex(self.coef[0])
+        prev, cur = None, v0
+        nxt = torch.empty_like(v0)
+        spare = torch.empty_like(v0)
+        scale, shift = 1.0 / self.b, -self.a / self.b
+        st = _lib.stream_ptr()
+        tr, co = self._nb_terms, self._nb_coef
+        for m in range(1, self.order + 1):
+            cm = complex(self.coef[m])
+            _lib.check(_lib.lib.gf_nb_cheb_step(cur.data_ptr(), None if prev is None else prev.data_ptr(),
+                                                nxt.data_ptr(), acc.data_ptr(), desc.ctypes.data, len(desc),
+                                                tr.ctypes.data, co.ctypes.data, len(co), scale, shift, cm.real,
+                                                cm.imag, B, st))
+            if prev is None:
+                prev, cur, nxt = cur, nxt, spare
+            else:
+                prev, cur, nxt = cur, nxt, prev
+        return acc
+
+    def _ranks(self, desc, js: torch.Tensor) -> torch.Tensor:
+        out = torch.empty_like(js)
+        _lib.check(_lib.lib.gf_nb_rank(js.data_ptr(), out.data_ptr(), js.numel(), desc.ctypes.data, len(desc),
+                                       _lib.stream_ptr()))
+        return out
+
+    def block_matrix(self, counts) -> torch.Tensor:
+        """[D, D] rows = conj(U e_x) in block coordinates (cached)."""
+        counts = tuple(int(n) for n in counts)
+        mat = self._blocks.get(counts)
+        if mat is None:
+            D = self.block_dim(counts)
+            dev = torch.device("cuda", torch.cuda.current_device())
+            mat = self._block_series(self._desc(counts), torch.eye(D, dtype=torch.complex128, device=dev))
+            self._blocks[counts] = mat
+        return mat
+
+    def phi0_into(self, js_full: torch.Tensor, sector, out: torch.Tensor) -> None:
+        B, N = out.shape
+        out.zero_()
+        js_host = js_full.cpu().numpy().astype(np.int64)
+        occ = np.stack([np.bitwise_count(js_host & m) for m in self._masks], axis=1)
+        keys, inv = np.unique(occ, axis=0, return_inverse=True)
+        sec = -1 if sector is None else int(sector)
+        st = _lib.stream_ptr()
+        dev = out.device
+        for bi, counts in enumerate(keys):
+            sel = np.nonzero(inv.reshape(-1) == bi)[0]
+            desc = self._desc(counts)
+            rows = torch.from_numpy(sel).to(dev)
+            cols = self._ranks(desc, js_full[rows].contiguous())
+            D = self.block_dim(counts)
+            if D <= self.cache_dim:
+                src = self.block_matrix(counts)
+            else:
+                v0 = torch.zeros((len(sel), D), dtype=torch.complex128, device=dev)
+                v0[torch.arange(len(sel), device=dev), cols] = 1.0
+                src = self._block_series(desc, v0)
+                cols = None
+            _lib.check(_lib.lib.gf_nb_scatter(src.data_ptr(), None if cols is None else cols.data_ptr(),
+                                              out.data_ptr(), rows.data_ptr(), len(sel), N, desc.ctypes.data,
+                                              len(desc), sec, st))
+
+
 class CachedTargetColumns:
     """phi0 rows for basis positions [p0, p1) of one basis-sum layout,
     computed once by an inner oracle and kept resident in HBM (the target
@@ -495,4 +630,6 @@ def make_oracle(spec: HamiltonianSpec, t: float, method: str = "dense"):
         return DenseOracle(spec, t)
     if method in ("krylov", "chebyshev"):
         return ChebyshevOracle(spec, t)
+    if method == "blocks":
+        return NumberBlockOracle(spec, t)
     raise ValueError(f"unknown oracle method {method!r}")

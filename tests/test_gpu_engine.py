@@ -310,6 +310,53 @@ def test_chebyshev_oracle_matches_dense_and_reference_krylov():
     assert torch.max(torch.abs(a - b)).item() < 1e-13
 
 
+
+@pytest.mark.parametrize("cache_dim", [8192, 0])
+def test_number_block_oracle_matches_dense(cache_dim):
+    """Block-coordinate Chebyshev (colex ranks, O(1) adjacent-hop rank steps,
+    periodic wrap bonds by full re-rank) == dense expm, full and sector rows,
+    whole-block cache and per-column modes."""
+    for spec in (gf.build_spinful_fh(4, 1.0, 4.0, False), gf.build_spinful_fh(3, 0.7, 2.5, True),
+                 gf.build_spinless_fh(7, 1.0, 3.0, True)):
+        k = spec.num_qubits
+        d = gf.DenseOracle(spec, 0.25)
+        nb = gf.NumberBlockOracle(spec, 0.25, cache_dim=cache_dim)
+        js = torch.arange(0, 1 << k, dtype=torch.int64, device="cuda")
+        a = torch.empty((1 << k, 1 << k), dtype=torch.complex128, device="cuda")
+        b = torch.full_like(a, 7.0)
+        d.phi0_into(js, None, a)
+        nb.phi0_into(js, None, b)
+        assert torch.max(torch.abs(a - b)).item() < 1e-13
+        for sector in (0, 1):
+            st = torch.arange(0, 1 << (k - 1), dtype=torch.int64, device="cuda")
+            jf = torch.from_numpy(O.sector_unrank(st.cpu().numpy(), sector)).cuda()
+            a2 = torch.empty((1 << (k - 1), 1 << (k - 1)), dtype=torch.complex128, device="cuda")
+            b2 = torch.full_like(a2, 7.0)
+            d.phi0_into(jf, sector, a2)
+            nb.phi0_into(jf, sector, b2)
+            assert torch.max(torch.abs(a2 - b2)).item() < 1e-13
+
+
+def test_number_block_oracle_c2_reference_krylov_checks():
+    """configs[1] target columns from the number-block oracle against the
+    reference Krylov phi0 checksums (tests/golden/c2_slice.npz), then the
+    c2 slice gradient / HVP through it."""
+    g = golden("c2_slice")
+    spec, circ, rng = gf.spinful_layer_circuit(8, 5, False, seed=1)
+    orc = gf.NumberBlockOracle(spec, 0.25)
+    js = g["js"]
+    srng = np.random.default_rng(2)
+    srng.choice(2**16, size=16, replace=False)
+    w = srng.normal(size=2**16) + 1j * srng.normal(size=2**16)
+    phi = torch.empty((16, 2**16), dtype=torch.complex128, device="cuda")
+    orc.phi0_into(torch.from_numpy(js).cuda(), None, phi)
+    P = phi.cpu().numpy()
+    chk = np.array([[p.sum(), p @ w, np.vdot(p, p).real] for p in P])
+    assert rel_err(chk, g["phi_checks"]) < 1e-10
+    rep, hv = gf.gradient_and_hvp(circ, orc, list(g["direction"]), basis=js)
+    assert rel_err(np.stack(rep.holomorphic_derivatives), g["holo"]) < TOL
+    assert rel_err(np.stack(hv), g["hvp"]) < TOL
+
 def test_c2_slice_vs_reference_chunk_drivers():
     """BASELINE configs[1] (16 qubits, 36 slots): reference _gradient_chunk /
     _hvp_chunk with Krylov phi0 on a seeded 16-state sample."""
