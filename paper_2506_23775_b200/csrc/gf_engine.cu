@@ -14,6 +14,8 @@
 // contractions and the Z-terms of the HVP.
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -266,6 +268,9 @@ __device__ __forceinline__ double2 dmma_mv2(double2 x, double b0, double b1, dou
 // t1 = bra, t2 + d*T = chi_d (REV) / v_d (ASC) for ND directions); hole
 // partials accumulate into sacc[slot][1 + ND][32] (hole 0 = gradient D,
 // hole 1 + d = HVP direction d).
+template <int V>
+using IC = std::integral_constant<int, V>;
+
 template <int OP, int NT, int ND, bool SPX>
 __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, double2 *t1, double2 *t2, double *scratch,
                                           double *sacc, const int tpop, const unsigned T)
@@ -438,35 +443,46 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
 #pragma unroll
                     for (int d = 0; d < ND; ++d) eH0[d] = eH1[d] = 0.0;
                     const unsigned nq = TW >> 2;
+                    // AC: 1/0 = direction active/inactive known at compile time
+                    // (ND == 1, hoisted out of the loop), 2 = test amask per d
+                    auto hole_loop = [&](auto AC) {
+                        constexpr int A = decltype(AC)::value;
 #pragma unroll 4
-                    for (unsigned q = 0; q < nq; q += 2) {
-                        unsigned a0 = baseH;
+                        for (unsigned q = 0; q < nq; q += 2) {
+                            unsigned a0 = baseH;
 #pragma unroll
-                        for (int i = 1; i < 5; ++i)
-                            if ((q >> i) & 1u) a0 ^= colH[i];
-                        const unsigned a1 = a0 ^ colH[0];
-                        const unsigned o0 = 2 * a0, o1 = 2 * a1;
-                        if constexpr (REV) {
-                            const double k0 = d0[o0], k1 = d0[o1];
-                            dmma(cD0, cD1, d1[o0], k0);
-                            dmma(eD0, eD1, d1[o1], k1);
-                            if constexpr (HH) {
+                            for (int i = 1; i < 5; ++i)
+                                if ((q >> i) & 1u) a0 ^= colH[i];
+                            const unsigned a1 = a0 ^ colH[0];
+                            const unsigned o0 = 2 * a0, o1 = 2 * a1;
+                            if constexpr (REV) {
+                                const double k0 = d0[o0], k1 = d0[o1];
+                                dmma(cD0, cD1, d1[o0], k0);
+                                dmma(eD0, eD1, d1[o1], k1);
+                                if constexpr (HH) {
+#pragma unroll
+                                    for (int d = 0; d < ND; ++d) {
+                                        if (!(A == 2 ? ((amask >> d) & 1) : A)) continue;
+                                        dmma(cH0[d], cH1[d], d2[2 * d * T + o0], k0);
+                                        dmma(eH0[d], eH1[d], d2[2 * d * T + o1], k1);
+                                    }
+                                }
+                            } else {
+                                const double b0 = d1[o0], b1 = d1[o1];
 #pragma unroll
                                 for (int d = 0; d < ND; ++d) {
-                                    if (!((amask >> d) & 1)) continue;
-                                    dmma(cH0[d], cH1[d], d2[2 * d * T + o0], k0);
-                                    dmma(eH0[d], eH1[d], d2[2 * d * T + o1], k1);
+                                    if (!(A == 2 ? ((amask >> d) & 1) : A)) continue;
+                                    dmma(cH0[d], cH1[d], b0, d2[2 * d * T + o0]);
+                                    dmma(eH0[d], eH1[d], b1, d2[2 * d * T + o1]);
                                 }
                             }
-                        } else {
-                            const double b0 = d1[o0], b1 = d1[o1];
-#pragma unroll
-                            for (int d = 0; d < ND; ++d) {
-                                if (!((amask >> d) & 1)) continue;
-                                dmma(cH0[d], cH1[d], b0, d2[2 * d * T + o0]);
-                                dmma(eH0[d], eH1[d], b1, d2[2 * d * T + o1]);
-                            }
                         }
+                    };
+                    if constexpr (ND == 1 && HH) {
+                        if (amask & 1) hole_loop(IC<1>{});
+                        else hole_loop(IC<0>{});
+                    } else {
+                        hole_loop(IC<2>{});
                     }
                     cD0 += eD0;
                     cD1 += eD1;
@@ -539,34 +555,37 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                         fc0[d] = fc1[d] = 0.0;
                         if (OP == OP_REV_GH || OP == OP_ASC_H) gate_frag(p.mat[si][2 + d], g, tq, fc0[d], fc1[d]);
                     }
+                    // AC / ZC: 1/0 = chi_d (v_d) active / Z_d nonzero known at
+                    // compile time (ND == 1, hoisted), 2 = test the masks per d
+                    auto grp_loop = [&](auto AC, auto ZC) {
+                        constexpr int A = decltype(AC)::value, Z = decltype(ZC)::value;
 #pragma unroll 8
-                    for (unsigned grp = 0; grp < ngrp; ++grp) {
-                        const unsigned ad = addrA(grp);
-                        if constexpr (REV) {
-                            const double2 bb = t1[ad];
-                            if constexpr (OP == OP_REV_GH) {
+                        for (unsigned grp = 0; grp < ngrp; ++grp) {
+                            const unsigned ad = addrA(grp);
+                            const double2 x = REV ? t1[ad] : t0[ad];
+                            if constexpr (OP == OP_REV_GH || OP == OP_ASC_H) {
 #pragma unroll
                                 for (int d = 0; d < ND; ++d) {
-                                    const bool act = (amask >> d) & 1, zz = (zmask >> d) & 1;
+                                    const bool act = A == 2 ? ((amask >> d) & 1) : A;
+                                    const bool zz = Z == 2 ? ((zmask >> d) & 1) : Z;
                                     double2 *X = t2 + d * T;
-                                    if (act && zz) X[ad] = dmma_mv2(X[ad], fb0, fb1, bb, fc0[d], fc1[d]);
+                                    if (act && zz) X[ad] = dmma_mv2(X[ad], fb0, fb1, x, fc0[d], fc1[d]);
                                     else if (act) X[ad] = dmma_mv(X[ad], fb0, fb1);
-                                    else if (zz) X[ad] = dmma_mv(bb, fc0[d], fc1[d]);
+                                    else if (zz) X[ad] = dmma_mv(x, fc0[d], fc1[d]);
                                 }
                             }
-                            t1[ad] = dmma_mv(bb, fb0, fb1);
-                        } else {
-                            const double2 x = t0[ad];
-#pragma unroll
-                            for (int d = 0; d < ND; ++d) {
-                                const bool act = (amask >> d) & 1, zz = (zmask >> d) & 1;
-                                double2 *X = t2 + d * T;
-                                if (act && zz) X[ad] = dmma_mv2(X[ad], fb0, fb1, x, fc0[d], fc1[d]);
-                                else if (act) X[ad] = dmma_mv(X[ad], fb0, fb1);
-                                else if (zz) X[ad] = dmma_mv(x, fc0[d], fc1[d]);
-                            }
-                            t0[ad] = dmma_mv(x, fb0, fb1);
+                            if constexpr (REV) t1[ad] = dmma_mv(x, fb0, fb1);
+                            else t0[ad] = dmma_mv(x, fb0, fb1);
                         }
+                    };
+                    if constexpr (ND == 1 && (OP == OP_REV_GH || OP == OP_ASC_H)) {
+                        const bool a = amask & 1, z = zmask & 1;
+                        if (a && z) grp_loop(IC<1>{}, IC<1>{});
+                        else if (a) grp_loop(IC<1>{}, IC<0>{});
+                        else if (z) grp_loop(IC<0>{}, IC<1>{});
+                        else grp_loop(IC<0>{}, IC<0>{});
+                    } else {
+                        grp_loop(IC<2>{}, IC<2>{});
                     }
                 }
             }
