@@ -192,6 +192,18 @@ int gf_nb_cheb_step(const void *t_cur, const void *t_prev, void *t_next, void *a
 int gf_nb_scatter(const void *cols, const int64_t *colidx, void *rows, const int64_t *rowidx, int64_t nrows,
                   int64_t row_len, const int32_t *desc, int ndesc, int sector, void *stream);
 int gf_nb_rank(const int64_t *js, int64_t *out, int64_t n, const int32_t *desc, int ndesc, void *stream);
+/* Whole block matrix in one launch (row b = sum_m coefs[m] T_m(H~) e_b, block
+ * coordinates; one CTA per row, series on chip); D <= 6400; coefs: device
+ * array of norder + 1 complex values; work: device scratch of at least
+ * D * (16 + 12 * n_hop_terms) bytes. */
+int gf_nb_block_matrix(void *out, const int32_t *desc, int ndesc, const int32_t *terms, const double *coef, int nterms,
+                       const void *coefs, int norder, double scale, double shift, void *work, void *stream);
+/* Rows from precomputed block matrices (all device arrays, no host sync):
+ * row b = block row rank_of[j] of block block_of[j] (j = js[b]) scattered to
+ * full_of[stoff[blk] + x] >> shift; rows must be zeroed; nrows <= 65535. */
+int gf_nb_gather(const int64_t *js, int64_t nrows, const void *mats, const int64_t *matoff, const int64_t *stoff,
+                 const int32_t *blkdim, const int32_t *block_of, const int32_t *rank_of, const int64_t *full_of,
+                 int64_t max_dim, int shift, void *out, int64_t row_len, void *stream);
 
 /* Device-memory helpers for bindings without a tensor library (the ctypes
  * stub of INTEGRATION.md).  gf_memcpy kind: 0 = H2D, 1 = D2H, 2 = D2D

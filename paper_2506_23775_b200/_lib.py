@@ -45,6 +45,8 @@ EXPORTS = (
     "gf_nb_cheb_step",
     "gf_nb_scatter",
     "gf_nb_rank",
+    "gf_nb_gather",
+    "gf_nb_block_matrix",
     "gf_peak_fp64",
     "gf_set_device",
     "gf_malloc",
@@ -97,6 +99,8 @@ for _name, _args in {
                         ctypes.c_double, _i64, _vp],
     "gf_nb_scatter": [_vp, _vp, _vp, _vp, _i64, _i64, _vp, _i, _i, _vp],
     "gf_nb_rank": [_vp, _vp, _i64, _vp, _i, _vp],
+    "gf_nb_block_matrix": [_vp, _vp, _i, _vp, _vp, _i, _vp, _i, ctypes.c_double, ctypes.c_double, _vp, _vp],
+    "gf_nb_gather": [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i, _vp, _i64, _vp],
     "gf_set_device": [_i],
     "gf_malloc": [ctypes.POINTER(_vp), _i64],
     "gf_free": [_vp],

@@ -193,40 +193,47 @@ struct NbBlock {
 };
 
 __constant__ unsigned long long c_binom[kMaxCompQ + 1][kMaxCompQ + 1];
+// binomials indexed with thread-dependent (a, b): the kernels copy the table
+// to shared memory, the constant cache would serialise divergent lookups
+constexpr int kBin = kMaxCompQ + 1;
+typedef unsigned long long BinTab[kBin];
 
-__device__ __forceinline__ unsigned long long binom(int a, int b)
+__device__ __forceinline__ void load_binom(BinTab *s)
 {
-    return (b < 0 || b > a) ? 0ull : c_binom[a][b];
+    for (int i = threadIdx.x; i < kBin * kBin; i += blockDim.x) s[i / kBin][i % kBin] = c_binom[i / kBin][i % kBin];
+    __syncthreads();
 }
 
 // colex unrank: the n-particle pattern of rank r over positions [0, L)
-__device__ __forceinline__ unsigned unrank_colex(unsigned long long r, int n, int L)
+// (binom[a][b] is zero for b > a, so the scan stops at the right position)
+__device__ __forceinline__ unsigned unrank_colex(const BinTab *binom, unsigned long long r, int n, int L)
 {
     unsigned pat = 0;
     int p = L - 1;
     for (int t = n; t >= 1; --t) {
-        while (binom(p, t) > r) --p;
+        while (binom[p][t] > r) --p;
         pat |= 1u << p;
-        r -= binom(p, t);
+        r -= binom[p][t];
         --p;
     }
     return pat;
 }
 
-__device__ __forceinline__ unsigned long long rank_colex(unsigned pat)
+__device__ __forceinline__ unsigned long long rank_colex(const BinTab *binom, unsigned pat)
 {
     unsigned long long r = 0;
     int t = 0;
     while (pat) {
         const int p = __ffs(pat) - 1;
-        r += binom(p, ++t);
+        r += binom[p][++t];
         pat &= pat - 1;
     }
     return r;
 }
 
 // (H~ v)[x] for one block vector, H~ = scale * H + shift
-__device__ __forceinline__ double2 nb_happly(const double2 *__restrict__ v, unsigned long long x, const NbBlock &B)
+__device__ __forceinline__ double2 nb_happly(const BinTab *binom, const double2 *__restrict__ v, unsigned long long x,
+                                             const NbBlock &B)
 {
     unsigned pat[kMaxComp];
     unsigned long long r[kMaxComp];
@@ -234,7 +241,7 @@ __device__ __forceinline__ double2 nb_happly(const double2 *__restrict__ v, unsi
     for (int c = B.ncomp - 1; c >= 0; --c) {
         r[c] = rem / B.stride[c];
         rem -= r[c] * B.stride[c];
-        pat[c] = unrank_colex(r[c], B.n[c], B.L[c]);
+        pat[c] = unrank_colex(binom, r[c], B.n[c], B.L[c]);
     }
     double d = 0.0;
     for (int t = 0; t < B.nnn; ++t)
@@ -248,10 +255,10 @@ __device__ __forceinline__ double2 nb_happly(const double2 *__restrict__ v, unsi
         if (j == i + 1) {
             // one particle crosses the adjacent pair; t = particles below i
             const int tt = __popc(pat[c] & ((1u << i) - 1u));
-            const long long step = (long long)binom(i, tt);
+            const long long step = (long long)binom[i][tt];
             dr = bi ? step : -step;  // i -> i+1 raises the rank, i+1 -> i lowers it
         } else {
-            dr = (long long)rank_colex(pat[c] ^ ((1u << i) | (1u << j))) - (long long)r[c];
+            dr = (long long)rank_colex(binom, pat[c] ^ ((1u << i) | (1u << j))) - (long long)r[c];
         }
         const double2 w = v[(unsigned long long)((long long)x + dr * (long long)B.stride[c])];
         acc.x = fma(B.hcoef[t], w.x, acc.x);
@@ -265,10 +272,12 @@ __global__ void __launch_bounds__(256) k_nb_cheb(const double2 *__restrict__ tcu
                                                  unsigned long long total, const NbBlock B, double scale, double shift,
                                                  double cre, double cim)
 {
+    __shared__ BinTab binom[kBin];
+    load_binom(binom);
     for (unsigned long long g = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; g < total;
          g += (unsigned long long)gridDim.x * blockDim.x) {
         const unsigned long long b = g / B.D, x = g - b * B.D;
-        double2 h = nb_happly(tcur + b * B.D, x, B);
+        double2 h = nb_happly(binom, tcur + b * B.D, x, B);
         const double2 cc = tcur[g];
         h.x = fma(scale, h.x, shift * cc.x);
         h.y = fma(scale, h.y, shift * cc.y);
@@ -295,6 +304,8 @@ __global__ void k_nb_scatter(const double2 *__restrict__ cols, const int64_t *__
                              double2 *__restrict__ rows, const int64_t *__restrict__ rowidx, unsigned long long nrows,
                              unsigned long long N, const NbBlock B)
 {
+    __shared__ BinTab binom[kBin];
+    load_binom(binom);
     const unsigned long long total = nrows * B.D;
     for (unsigned long long g = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; g < total;
          g += (unsigned long long)gridDim.x * blockDim.x) {
@@ -303,7 +314,7 @@ __global__ void k_nb_scatter(const double2 *__restrict__ cols, const int64_t *__
         for (int c = B.ncomp - 1; c >= 0; --c) {
             const unsigned long long r = rem / B.stride[c];
             rem -= r * B.stride[c];
-            unsigned pat = unrank_colex(r, B.n[c], B.L[c]);
+            unsigned pat = unrank_colex(binom, r, B.n[c], B.L[c]);
             while (pat) {
                 const int pp = __ffs(pat) - 1;
                 full |= 1ull << (B.k - 1 - B.q[c][pp]);
@@ -319,13 +330,15 @@ __global__ void k_nb_scatter(const double2 *__restrict__ cols, const int64_t *__
 // block index of full-space states: out[i] = x (the mixed-radix rank)
 __global__ void k_nb_rank(const int64_t *__restrict__ js, int64_t *__restrict__ out, int64_t n, const NbBlock B)
 {
+    __shared__ BinTab binom[kBin];
+    load_binom(binom);
     for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n; g += (int64_t)gridDim.x * blockDim.x) {
         const unsigned long long j = (unsigned long long)js[g];
         unsigned long long x = 0;
         for (int c = 0; c < B.ncomp; ++c) {
             unsigned pat = 0;
             for (int i = 0; i < B.L[c]; ++i) pat |= (unsigned)((j >> (B.k - 1 - B.q[c][i])) & 1ull) << i;
-            x += rank_colex(pat) * B.stride[c];
+            x += rank_colex(binom, pat) * B.stride[c];
         }
         out[g] = (int64_t)x;
     }
@@ -451,6 +464,178 @@ extern "C" int gf_nb_rank(const int64_t *js, int64_t *out, int64_t n, const int3
     rc = make_block(desc, ndesc, nullptr, nullptr, 0, -1, B);
     if (rc) return rc;
     k_nb_rank<<<grid_for((unsigned long long)n), 256, 0, (cudaStream_t)stream>>>(js, out, n, B);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return gf_fail(GF_ECUDA, "%s", cudaGetErrorString(e));
+    return GF_OK;
+}
+
+// Target rows from precomputed block matrices, no host round trip: row b gets
+// mats[matoff[blk] + rank_of[j] * D + x] at full index full_of[stoff[blk] + x]
+// for x < D (blk = block_of[j], D = blkdim[blk], j = js[b]); everything else
+// in the row must already be zero.  Rows are dense (shift 0) or compressed on
+// qubit k-1 (shift 1).
+__global__ void k_nb_gather(const int64_t *__restrict__ js, const double2 *__restrict__ mats,
+                            const int64_t *__restrict__ matoff, const int64_t *__restrict__ stoff,
+                            const int32_t *__restrict__ blkdim, const int32_t *__restrict__ block_of,
+                            const int32_t *__restrict__ rank_of, const int64_t *__restrict__ full_of, int shift,
+                            double2 *__restrict__ out, int64_t row_len)
+{
+    const int64_t b = blockIdx.y;
+    const int64_t j = js[b];
+    const int blk = block_of[j];
+    const int64_t D = blkdim[blk];
+    const double2 *src = mats + matoff[blk] + (int64_t)rank_of[j] * D;
+    const int64_t *dst = full_of + stoff[blk];
+    double2 *row = out + b * row_len;
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < D; x += (int64_t)gridDim.x * blockDim.x)
+        row[dst[x] >> shift] = src[x];
+}
+
+extern "C" int gf_nb_gather(const int64_t *js, int64_t nrows, const void *mats, const int64_t *matoff,
+                            const int64_t *stoff, const int32_t *blkdim, const int32_t *block_of,
+                            const int32_t *rank_of, const int64_t *full_of, int64_t max_dim, int shift, void *out,
+                            int64_t row_len, void *stream)
+{
+    if (!js || !mats || !out || nrows < 0 || max_dim < 1 || (shift != 0 && shift != 1) || nrows > 65535)
+        return gf_fail(GF_EINVAL, "bad gather arguments");
+    if (nrows == 0) return GF_OK;
+    const unsigned gx = (unsigned)std::min<int64_t>((max_dim + 255) / 256, 64);
+    k_nb_gather<<<dim3(gx, (unsigned)nrows), 256, 0, (cudaStream_t)stream>>>(
+        js, (const double2 *)mats, matoff, stoff, blkdim, block_of, rank_of, full_of, shift, (double2 *)out, row_len);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return gf_fail(GF_ECUDA, "%s", cudaGetErrorString(e));
+    return GF_OK;
+}
+
+// Block Hamiltonian as an ELL table (computed once per block; identical for
+// every column): diag[x], cnt[x] valid hops, (nbr, coef) at t * D + x.
+__global__ void k_nb_ell(const NbBlock B, double *__restrict__ diag, int *__restrict__ cnt, int *__restrict__ nbr,
+                         double *__restrict__ hc, int nh)
+{
+    __shared__ BinTab binom[kBin];
+    load_binom(binom);
+    for (unsigned long long x = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; x < B.D;
+         x += (unsigned long long)gridDim.x * blockDim.x) {
+        unsigned pat[kMaxComp];
+        unsigned long long r[kMaxComp];
+        unsigned long long rem = x;
+        for (int c = B.ncomp - 1; c >= 0; --c) {
+            r[c] = rem / B.stride[c];
+            rem -= r[c] * B.stride[c];
+            pat[c] = unrank_colex(binom, r[c], B.n[c], B.L[c]);
+        }
+        double d = 0.0;
+        for (int t = 0; t < B.nnn; ++t)
+            if (((pat[B.nca[t]] >> B.nia[t]) & 1u) && ((pat[B.ncb[t]] >> B.nib[t]) & 1u)) d += B.ncoef[t];
+        diag[x] = d;
+        int k = 0;
+        for (int t = 0; t < B.nhop; ++t) {
+            const int c = B.hc[t], i = B.hi[t], j = B.hj[t];
+            const unsigned bi = (pat[c] >> i) & 1u, bj = (pat[c] >> j) & 1u;
+            if (bi == bj) continue;
+            long long dr;
+            if (j == i + 1) {
+                const long long step = (long long)binom[i][__popc(pat[c] & ((1u << i) - 1u))];
+                dr = bi ? step : -step;
+            } else {
+                dr = (long long)rank_colex(binom, pat[c] ^ ((1u << i) | (1u << j))) - (long long)r[c];
+            }
+            nbr[k * B.D + x] = (int)((long long)x + dr * (long long)B.stride[c]);
+            hc[k * B.D + x] = B.hcoef[t];
+            ++k;
+        }
+        cnt[x] = k;
+    }
+}
+
+// Whole block matrix in one launch: CTA b runs every Chebyshev order of
+// column e_b on chip.  cur and prev live in shared memory (neighbours read
+// cur; each thread overwrites only its own prev entries with next, then the
+// two buffers swap roles); the ELL Hamiltonian and the accumulator row out[b]
+// stay L2-resident.  Row b of the result = sum_m c_m T_m(H~) e_b.  The hop
+// terms are summed in term order after the diagonal, exactly as nb_happly.
+__global__ void __launch_bounds__(1024) k_nb_series(double2 *__restrict__ out, const double2 *__restrict__ coefs,
+                                                    int norder, long long D, const double *__restrict__ diag,
+                                                    const int *__restrict__ cnt, const int *__restrict__ nbr,
+                                                    const double *__restrict__ hc, int nh, double scale, double shift)
+{
+    extern __shared__ double2 nb_smem[];
+    const long long b = blockIdx.x;
+    double2 *cur = nb_smem, *prev = nb_smem + D;
+    double2 *row = out + b * D;
+    const double2 c0 = coefs[0];
+    for (long long x = threadIdx.x; x < D; x += blockDim.x) {
+        const double v = (x == b) ? 1.0 : 0.0;
+        cur[x] = make_double2(v, 0.0);
+        row[x] = make_double2(c0.x * v, c0.y * v);
+    }
+    __syncthreads();
+    for (int m = 1; m <= norder; ++m) {
+        const double2 cm = coefs[m];
+        for (long long x = threadIdx.x; x < D; x += blockDim.x) {
+            const double2 cc = cur[x];
+            double2 h = cscale(cc, diag[x]);
+            const int k = cnt[x];
+            for (int t = 0; t < k; ++t) {
+                const double w = hc[t * D + x];
+                const double2 v = cur[nbr[t * D + x]];
+                h.x = fma(w, v.x, h.x);
+                h.y = fma(w, v.y, h.y);
+            }
+            h.x = fma(scale, h.x, shift * cc.x);
+            h.y = fma(scale, h.y, shift * cc.y);
+            if (m > 1) {
+                const double2 p = prev[x];
+                h.x = 2.0 * h.x - p.x;
+                h.y = 2.0 * h.y - p.y;
+            }
+            prev[x] = h;
+            double2 a = row[x];
+            const double2 ch = cmul(cm, h);
+            a.x += ch.x;
+            a.y += ch.y;
+            row[x] = a;
+        }
+        __syncthreads();
+        double2 *t = cur;
+        cur = prev;
+        prev = t;
+    }
+}
+
+// Block matrix (rows conj(U e_b) in block coordinates when coefs are the
+// conjugated series coefficients) for one number block, D <= 6400.
+// coefs: device array of norder + 1 complex coefficients.  work: device
+// scratch of at least D * (16 + 12 * nhop) bytes for the ELL Hamiltonian.
+extern "C" int gf_nb_block_matrix(void *out, const int32_t *desc, int ndesc, const int32_t *terms, const double *coef,
+                                  int nterms, const void *coefs, int norder, double scale, double shift, void *work,
+                                  void *stream)
+{
+    if (!out || !coefs || !work || norder < 1) return gf_fail(GF_EINVAL, "bad block-matrix arguments");
+    int rc = ensure_binom();
+    if (rc) return rc;
+    NbBlock B;
+    rc = make_block(desc, ndesc, terms, coef, nterms, -1, B);
+    if (rc) return rc;
+    const size_t smem = 2 * sizeof(double2) * (size_t)B.D;
+    if (smem > 200 * 1024) return gf_fail(GF_EINVAL, "block dimension %llu too large for on-chip series", B.D);
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t ae = cudaFuncSetAttribute(k_nb_series, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        if (ae != cudaSuccess) return gf_fail(GF_ECUDA, "k_nb_series smem attribute: %s", cudaGetErrorString(ae));
+        attr = true;
+    }
+    const int nh = std::max(1, B.nhop);
+    char *w = (char *)work;
+    double *diag = (double *)w;
+    double *hc = diag + B.D;
+    int *nbr = (int *)(hc + B.D * nh);
+    int *cnt = nbr + B.D * nh;
+    cudaStream_t st = (cudaStream_t)stream;
+    k_nb_ell<<<grid_for(B.D), 256, 0, st>>>(B, diag, cnt, nbr, hc, nh);
+    const int nt = (int)std::min<unsigned long long>(1024, (B.D + 31) / 32 * 32);
+    k_nb_series<<<(unsigned)B.D, nt, smem, st>>>((double2 *)out, (const double2 *)coefs, norder, (long long)B.D, diag,
+                                                 cnt, nbr, hc, nh, scale, shift);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return gf_fail(GF_ECUDA, "%s", cudaGetErrorString(e));
     return GF_OK;

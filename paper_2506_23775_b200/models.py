@@ -434,6 +434,9 @@ class ChebyshevOracle:
         self._series(v0, sector, out=out)
 
 
+_NB_INDEX_MAPS: dict = {}
+
+
 class NumberBlockOracle(ChebyshevOracle):
     """exp(-iHt)|j> inside j's particle-number block, on the GPU.
 
@@ -484,6 +487,7 @@ class NumberBlockOracle(ChebyshevOracle):
         self._masks = np.array([sum(1 << (k - 1 - q) for q in cq) for cq in self.components], np.int64)
         self.cache_dim = int(cache_dim)
         self._blocks = {}
+        self._tab = None
 
     def block_of(self, j: int):
         return tuple(bin(int(j) & int(m)).count("1") for m in self._masks)
@@ -502,10 +506,11 @@ class NumberBlockOracle(ChebyshevOracle):
             d += [len(cq), int(n)] + list(cq)
         return np.ascontiguousarray(np.array(d, np.int32))
 
-    def _block_series(self, desc, v0: torch.Tensor) -> torch.Tensor:
+    def _block_series(self, desc, v0: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         """sum conj(c_m) T_m(H~) v0 for block vectors v0 [B, D]."""
         B = v0.shape[0]
-        acc = v0 * complex(self.coef[0])
+        acc = out if out is not None else torch.empty_like(v0)
+        torch.mul(v0, complex(self.coef[0]), out=acc)
         prev, cur = None, v0
         nxt = torch.empty_like(v0)
         spare = torch.empty_like(v0)
@@ -541,9 +546,96 @@ class NumberBlockOracle(ChebyshevOracle):
             self._blocks[counts] = mat
         return mat
 
+    def _tables(self):
+        """Whole-space block tables (when every block has dimension <=
+        cache_dim): every block matrix in one device buffer plus the maps
+        state -> (block, rank) and (block, rank) -> state, so target rows are
+        gathered on the device without a host round trip."""
+        if self._tab is not None:
+            return self._tab or None
+        k = self.num_qubits
+        if k > 26:
+            self._tab = False
+            return None
+        dev = torch.device("cuda", torch.cuda.current_device())
+        idx = self._index_maps(dev)
+        if idx["dims"].max() > self.cache_dim:
+            self._tab = False
+            return None
+        keys, dims, matoff = idx["keys"], idx["dims"], idx["matoff"]
+        mats = torch.empty(int((dims * dims).sum()), dtype=torch.complex128, device=dev)
+        coefs = torch.from_numpy(np.ascontiguousarray(self.coef, np.complex128)).to(dev)
+        nh = max(1, int(self._nb_terms[:, 0].tolist().count(0)))
+        work = torch.empty(int(dims.max()) * (16 + 12 * nh) // 8 + 1, dtype=torch.float64, device=dev)
+        st = _lib.stream_ptr()
+        tr, co = self._nb_terms, self._nb_coef
+        for bi, counts in enumerate(keys):
+            D = int(dims[bi])
+            dst = mats[matoff[bi]:matoff[bi] + D * D].view(D, D)
+            desc = self._desc(counts)
+            if D <= 6400:  # whole series on chip, one launch per block
+                _lib.check(_lib.lib.gf_nb_block_matrix(dst.data_ptr(), desc.ctypes.data, len(desc), tr.ctypes.data,
+                                                       co.ctypes.data, len(co), coefs.data_ptr(), self.order,
+                                                       1.0 / self.b, -self.a / self.b, work.data_ptr(), st))
+            else:
+                self._block_series(desc, torch.eye(D, dtype=torch.complex128, device=dev), out=dst)
+        self._tab = dict(idx["dev"], mats=mats, max_dim=int(dims.max()))
+        return self._tab
+
+    def _index_maps(self, dev):
+        """state <-> (block, rank) maps of the whole space.  They depend only
+        on the hop graph (not on t or the coefficients), so they are shared by
+        every oracle of the same structure."""
+        from math import comb
+
+        key = (self.num_qubits, tuple(tuple(c) for c in self.components), str(dev))
+        hit = _NB_INDEX_MAPS.get(key)
+        if hit is not None:
+            return hit
+        k = self.num_qubits
+        states = np.arange(1 << k, dtype=np.int64)
+        occ = np.stack([np.bitwise_count(states & m).astype(np.int64) for m in self._masks], axis=1)
+        keys, block_of = np.unique(occ, axis=0, return_inverse=True)
+        block_of = block_of.reshape(-1)
+        dims = np.array([self.block_dim(c) for c in keys], dtype=np.int64)
+        binom = np.array([[comb(a, b) for b in range(34)] for a in range(33)], dtype=np.int64)
+        rank = np.zeros(1 << k, dtype=np.int64)
+        stride = np.ones(1 << k, dtype=np.int64)
+        for ci, cq in enumerate(self.components):
+            cnt = np.zeros(1 << k, dtype=np.int64)
+            r = np.zeros(1 << k, dtype=np.int64)
+            for i, q in enumerate(cq):
+                bit = (states >> (k - 1 - q)) & 1
+                r += bit * binom[i, cnt + 1]
+                cnt += bit
+            rank += r * stride
+            stride *= binom[len(cq), occ[:, ci]]
+        full_of = np.lexsort((rank, block_of)).astype(np.int64)
+        stoff = np.concatenate([[0], np.cumsum(dims)[:-1]]).astype(np.int64)
+        matoff = np.concatenate([[0], np.cumsum(dims * dims)[:-1]]).astype(np.int64)
+        put = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a.astype(dt))).to(dev)
+        hit = {"keys": keys, "dims": dims, "matoff": matoff,
+               "dev": {"matoff": put(matoff, np.int64), "stoff": put(stoff, np.int64), "blkdim": put(dims, np.int32),
+                       "block_of": put(block_of, np.int32), "rank_of": put(rank, np.int32),
+                       "full_of": put(full_of, np.int64)}}
+        _NB_INDEX_MAPS[key] = hit
+        return hit
+
     def phi0_into(self, js_full: torch.Tensor, sector, out: torch.Tensor) -> None:
         B, N = out.shape
         out.zero_()
+        tab = self._tables()
+        if tab is not None:
+            js = js_full.contiguous()
+            st = _lib.stream_ptr()
+            for r0 in range(0, B, 65535):
+                nr = min(B, r0 + 65535) - r0
+                _lib.check(_lib.lib.gf_nb_gather(
+                    js[r0:].data_ptr(), nr, tab["mats"].data_ptr(), tab["matoff"].data_ptr(),
+                    tab["stoff"].data_ptr(), tab["blkdim"].data_ptr(), tab["block_of"].data_ptr(),
+                    tab["rank_of"].data_ptr(), tab["full_of"].data_ptr(), tab["max_dim"],
+                    0 if sector is None else 1, out[r0:].data_ptr(), N, st))
+            return
         js_host = js_full.cpu().numpy().astype(np.int64)
         occ = np.stack([np.bitwise_count(js_host & m) for m in self._masks], axis=1)
         keys, inv = np.unique(occ, axis=0, return_inverse=True)

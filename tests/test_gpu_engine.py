@@ -311,8 +311,8 @@ def test_chebyshev_oracle_matches_dense_and_reference_krylov():
 
 
 
-@pytest.mark.parametrize("cache_dim", [8192, 0])
-def test_number_block_oracle_matches_dense(cache_dim):
+@pytest.mark.parametrize("mode", ["tables", "blocks", "columns"])
+def test_number_block_oracle_matches_dense(mode):
     """Block-coordinate Chebyshev (colex ranks, O(1) adjacent-hop rank steps,
     periodic wrap bonds by full re-rank) == dense expm, full and sector rows,
     whole-block cache and per-column modes."""
@@ -320,7 +320,9 @@ def test_number_block_oracle_matches_dense(cache_dim):
                  gf.build_spinless_fh(7, 1.0, 3.0, True)):
         k = spec.num_qubits
         d = gf.DenseOracle(spec, 0.25)
-        nb = gf.NumberBlockOracle(spec, 0.25, cache_dim=cache_dim)
+        nb = gf.NumberBlockOracle(spec, 0.25, cache_dim=0 if mode == "columns" else 8192)
+        if mode == "blocks":
+            nb._tab = False  # per-group path with cached block matrices
         js = torch.arange(0, 1 << k, dtype=torch.int64, device="cuda")
         a = torch.empty((1 << k, 1 << k), dtype=torch.complex128, device="cuda")
         b = torch.full_like(a, 7.0)
