@@ -106,14 +106,25 @@ def run(name):
         weights = size.cpu().numpy()[first].astype(np.float64)
         out["orbit_reps_total_burnside"] = {14: 19173968, 16: 268443720}.get(L)
     out["sample_summands"] = int(idx.size)
-    # target columns of the sample: Chebyshev oracle in the compressed sector, timed separately
-    orc = gf.ChebyshevOracle(spec, 0.25)
+    # target columns of the sample: number-block Chebyshev oracle (each
+    # column inside its particle-number block), timed separately
+    orc = gf.NumberBlockOracle(spec, 0.25)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     cache = gf.models.CachedTargetColumns(orc, k, 0, idx.size, sector=0, indices=idx, batch=1)
     torch.cuda.synchronize()
     out["oracle_s_per_summand"] = (time.perf_counter() - t0) / idx.size
     out["oracle_chebyshev_order"] = orc.order
+    out["oracle"] = type(orc).__name__
+    # cross-check one column against the full-space Chebyshev oracle
+    chk = gf.ChebyshevOracle(spec, 0.25)
+    first = torch.from_numpy(idx[:1]).cuda()
+    jf = torch.empty_like(first)
+    gf._lib.check(gf._lib.lib.gf_sector_unrank(first.data_ptr(), 1, 0, jf.data_ptr(), gf._lib.stream_ptr()))
+    col = torch.empty((1, sect_size), dtype=torch.complex128, device="cuda")
+    chk.phi0_into(jf, 0, col)
+    out["oracle_vs_full_space_chebyshev_max_abs"] = float(torch.max(torch.abs(col - cache.rows[:1])).item())
+    del chk, col
     del orc
     torch.cuda.empty_cache()
     basis = (idx, weights)

@@ -235,13 +235,16 @@ __device__ __forceinline__ unsigned long long rank_colex(const BinTab *binom, un
 __device__ __forceinline__ double2 nb_happly(const BinTab *binom, const double2 *__restrict__ v, unsigned long long x,
                                              const NbBlock &B)
 {
+    // block dimensions are < 2^32 (make_block), so the mixed-radix split
+    // runs in 32-bit integer math
     unsigned pat[kMaxComp];
     unsigned long long r[kMaxComp];
-    unsigned long long rem = x;
+    unsigned rem = (unsigned)x;
     for (int c = B.ncomp - 1; c >= 0; --c) {
-        r[c] = rem / B.stride[c];
-        rem -= r[c] * B.stride[c];
-        pat[c] = unrank_colex(binom, r[c], B.n[c], B.L[c]);
+        const unsigned rc = rem / (unsigned)B.stride[c];
+        rem -= rc * (unsigned)B.stride[c];
+        r[c] = rc;
+        pat[c] = unrank_colex(binom, rc, B.n[c], B.L[c]);
     }
     double d = 0.0;
     for (int t = 0; t < B.nnn; ++t)
@@ -368,6 +371,7 @@ int make_block(const int32_t *desc, int ndesc, const int32_t *terms, const doubl
         for (int i = 0; i < B.n[c]; ++i) cnt = cnt * (B.L[c] - i) / (i + 1);
         D *= cnt;
     }
+    if (D >= (1ull << 32)) return gf_fail(GF_EINVAL, "number block of dimension %llu too large", D);
     B.D = D;
     // terms: [kind(0 hop / 1 nn), ca, ia, cb, ib] x nterms
     for (int t = 0; t < nterms; ++t) {

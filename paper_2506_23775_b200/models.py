@@ -553,15 +553,17 @@ class NumberBlockOracle(ChebyshevOracle):
         gathered on the device without a host round trip."""
         if self._tab is not None:
             return self._tab or None
+        from math import comb
+
         k = self.num_qubits
-        if k > 26:
+        largest = 1
+        for cq in self.components:
+            largest *= comb(len(cq), len(cq) // 2)
+        if k > 26 or largest > self.cache_dim:
             self._tab = False
             return None
         dev = torch.device("cuda", torch.cuda.current_device())
         idx = self._index_maps(dev)
-        if idx["dims"].max() > self.cache_dim:
-            self._tab = False
-            return None
         keys, dims, matoff = idx["keys"], idx["dims"], idx["matoff"]
         mats = torch.empty(int((dims * dims).sum()), dtype=torch.complex128, device=dev)
         coefs = torch.from_numpy(np.ascontiguousarray(self.coef, np.complex128)).to(dev)
