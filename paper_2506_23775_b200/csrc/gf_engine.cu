@@ -212,6 +212,15 @@ __global__ void __launch_bounds__(kThreads) k_sweep(const SweepParams p)
 // Fused tile pass (see gf_fused.cuh).  Grid: (ctas, nvec); each CTA walks the
 // tiles blockIdx.x, blockIdx.x + ctas, ... of vector blockIdx.y.
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
+{
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
 __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
 {
     asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -591,35 +600,44 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
             }
         }
         if constexpr (HD || HH) {
-            if ((unsigned)warp < nwa) {
-                if (HD) {
-                    scratch[(0 * NW + warp) * 64 + g * 8 + 2 * tq] = cD0;
-                    scratch[(0 * NW + warp) * 64 + g * 8 + 2 * tq + 1] = cD1;
+            // Fold the 8x8 real fragment to the complex 4x4 hole inside the warp:
+            // lane (2i, j) holds C[2i][2j..2j+1], its partner lane (2i+1, j)
+            // C[2i+1][2j..2j+1]; Re D_ij = C[2i][2j] - C[2i+1][2j+1],
+            // Im D_ij = C[2i][2j+1] + C[2i+1][2j].  The even-g lanes store 32
+            // doubles per warp and hole into the slot-parity half of scratch,
+            // so one barrier per slot orders both the tile and the partials:
+            // scratch[s & 1] is next written at slot s + 2, after the barrier of
+            // slot s + 1, which the reducing warps pass only after reducing.
+            double *sbuf = scratch + (si & 1) * (NH * NW * 32);
+            auto fold_store = [&](int hole, double c0, double c1) {
+                const double o0 = __shfl_xor_sync(0xffffffffu, c0, 4);
+                const double o1 = __shfl_xor_sync(0xffffffffu, c1, 4);
+                if (!(g & 1)) {
+                    double *dst = sbuf + (hole * NW + warp) * 32 + ((g >> 1) * 4 + tq) * 2;
+                    dst[0] = c0 - o1;
+                    dst[1] = c1 + o0;
                 }
+            };
+            if ((unsigned)warp < nwa) {
+                if (HD) fold_store(0, cD0, cD1);
                 if (HH) {
 #pragma unroll
-                    for (int d = 0; d < ND; ++d) {
-                        scratch[((1 + d) * NW + warp) * 64 + g * 8 + 2 * tq] = cH0[d];
-                        scratch[((1 + d) * NW + warp) * 64 + g * 8 + 2 * tq + 1] = cH1[d];
-                    }
+                    for (int d = 0; d < ND; ++d) fold_store(1 + d, cH0[d], cH1[d]);
                 }
             }
             __syncthreads();
             if (tid < 32 * NH) {
                 const int hole = tid >> 5;
                 if ((hole == 0 && HD) || (hole >= 1 && HH)) {
-                    const int i = tid & 31, e = i >> 1, part = i & 1, ii = e >> 2, jj = e & 3;
+                    const int i = tid & 31;
                     double sum = 0.0;
-                    for (unsigned ww = 0; ww < nwa; ++ww) {
-                        const double *C = scratch + (hole * NW + ww) * 64;
-                        sum += part == 0 ? (C[(2 * ii) * 8 + 2 * jj] - C[(2 * ii + 1) * 8 + 2 * jj + 1])
-                                         : (C[(2 * ii) * 8 + 2 * jj + 1] + C[(2 * ii + 1) * 8 + 2 * jj]);
-                    }
+                    for (unsigned ww = 0; ww < nwa; ++ww) sum += sbuf[(hole * NW + ww) * 32 + i];
                     sacc[(si * NH + hole) * 32 + i] += sum;
                 }
             }
+        } else {
+            __syncthreads();
         }
-        __syncthreads();
     }
 }
 
@@ -670,31 +688,44 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_fused(const FusedParams p)
         // the first forward and first ascending passes start from psi_0 = |j>
         constexpr bool SYNTH = (OP == OP_FWD || OP == OP_FWD_DOT || OP == OP_ASC_H) && FIRST;
         const u64 jb = SYNTH ? (u64)p.basis[blockIdx.y] : 0ull;
+        // Plain copies go global -> shared with cp.async (no register round
+        // trip, every element of the tile in flight at once); the synthesised
+        // |j>, the zero chi/v and the weighted phi0 are written by the threads.
         for (unsigned l = tid; l < T; l += NT) {
             const u64 a = base + (l & cmask) + hiofs[l >> c];
-            double2 x;
+            const unsigned sl = swz(l);
             if constexpr (SYNTH)
-                x = make_double2(a == jb ? 1.0 : 0.0, 0.0);  // psi_0 = |j>, no HBM read
+                t0[sl] = make_double2(a == jb ? 1.0 : 0.0, 0.0);  // psi_0 = |j>, no HBM read
             else
-                x = psi[a];
-            t0[swz(l)] = x;
+                cp_async16(&t0[sl], &psi[a]);
             if constexpr (NV >= 2) {
-                double2 b;
-                if constexpr (REV && FIRST) {
-                    b = cscale(phi0[a], w);
-                    vre = fma(b.x, x.x, vre);
-                    vre = fma(-b.y, x.y, vre);
-                    vim = fma(b.x, x.y, vim);
-                    vim = fma(b.y, x.x, vim);
-                } else {
-                    b = bra[a];
-                }
-                t1[swz(l)] = b;
+                if constexpr (!(REV && FIRST)) cp_async16(&t1[sl], &bra[a]);
             }
             if constexpr (NV >= 3) {
 #pragma unroll
-                for (int d = 0; d < ND; ++d) t2[d * T + swz(l)] = FIRST ? czero() : aux[a + d * p.auxstride];
+                for (int d = 0; d < ND; ++d) {
+                    if constexpr (FIRST) t2[d * T + sl] = czero();
+                    else cp_async16(&t2[d * T + sl], &aux[a + d * p.auxstride]);
+                }
             }
+        }
+        cp_async_commit();
+        if constexpr (REV && FIRST) {
+            // bra_0 = w phi0; the value <phi0|psi_n> is read back from the tile
+            for (unsigned l = tid; l < T; l += NT) {
+                const u64 a = base + (l & cmask) + hiofs[l >> c];
+                t1[swz(l)] = cscale(phi0[a], w);
+            }
+            cp_async_wait<0>();
+            for (unsigned l = tid; l < T; l += NT) {
+                const double2 x = t0[swz(l)], b = t1[swz(l)];
+                vre = fma(b.x, x.x, vre);
+                vre = fma(-b.y, x.y, vre);
+                vim = fma(b.x, x.y, vim);
+                vim = fma(b.y, x.x, vim);
+            }
+        } else {
+            cp_async_wait<0>();
         }
         __syncthreads();
 
@@ -791,15 +822,6 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_fused(const FusedParams p)
 // All partials are scaled by the summand weight at flush time (the engine is
 // linear in the bra), so raw target columns can be copied asynchronously.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
-{
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
-
 template <int OP, bool FIRST, int NT>
 __global__ void __launch_bounds__(NT, 512 / NT) k_fused_pipe(const FusedParams p)
 {
