@@ -429,8 +429,11 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                         for (int i = 0; i < 4; ++i) V[L[i]] = y[i];
                     }
                 } else {
-                    double fa0, fa1;
-                    gate_frag(MA, g, tq, fa0, fa1);
+                    // coalesced per-lane fragment rows (a dynamically indexed
+                    // Mat4 in parameter space serialises 16 ways in the
+                    // constant cache)
+                    const double2 fA = __ldg(&p.frag[p.ps[si].fa * 32 + lane]);
+                    const double fa0 = fA.x, fa1 = fA.y;
 #pragma unroll 8
                     for (unsigned grp = 0; grp < ngrp; ++grp) {
                         const unsigned ad = addrA(grp);
@@ -557,12 +560,17 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                         }
                     }
                 } else {
-                    double fb0, fb1, fc0[ND], fc1[ND];
-                    gate_frag(MB, g, tq, fb0, fb1);
+                    double fc0[ND], fc1[ND];
+                    const double2 fB = __ldg(&p.frag[p.ps[si].fb * 32 + lane]);
+                    const double fb0 = fB.x, fb1 = fB.y;
 #pragma unroll
                     for (int d = 0; d < ND; ++d) {
                         fc0[d] = fc1[d] = 0.0;
-                        if (OP == OP_REV_GH || OP == OP_ASC_H) gate_frag(p.mat[si][2 + d], g, tq, fc0[d], fc1[d]);
+                        if (OP == OP_REV_GH || OP == OP_ASC_H) {
+                            const double2 fZ = __ldg(&p.frag[(p.ps[si].fz + d) * 32 + lane]);
+                            fc0[d] = fZ.x;
+                            fc1[d] = fZ.y;
+                        }
                     }
                     // AC / ZC: 1/0 = chi_d (v_d) active / Z_d nonzero known at
                     // compile time (ND == 1, hoisted), 2 = test the masks per d
@@ -822,7 +830,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_fused(const FusedParams p)
 // All partials are scaled by the summand weight at flush time (the engine is
 // linear in the bra), so raw target columns can be copied asynchronously.
 // ---------------------------------------------------------------------------
-template <int OP, bool FIRST, int NT>
+template <int OP, bool FIRST, int NT, bool SPX>
 __global__ void __launch_bounds__(NT, 512 / NT) k_fused_pipe(const FusedParams p)
 {
     constexpr int NW = NT / 32;
@@ -918,7 +926,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_fused_pipe(const FusedParams p
             }
             __syncthreads();
         }
-        run_slots<OP, NT, 1, true>(p, t0, t1, t2, scratch, sacc, __popcll(tile), T);
+        run_slots<OP, NT, 1, SPX>(p, t0, t1, t2, scratch, sacc, __popcll(tile), T);
         const int sm = p.store_mask;
         for (unsigned l = tid; l < T; l += NT) {
             const u64 a = base + (l & cmask) + hiofs[l >> c];
@@ -1144,6 +1152,11 @@ struct gf_plan {
     // half-sums are only order-invariant together), so asc_passes is
     // rev_passes reversed with each pass's slot list reversed.
     std::vector<FusedParams> fwd_passes, rev_passes, asc_passes;
+    // per-lane DMMA B fragments of every slot matrix, [slot][FK_*][32 lanes]
+    // (double2 = the two k-steps); rebuilt on the eval stream when dirty
+    double2 *d_frag = nullptr;
+    std::vector<double2> h_frag;
+    bool frag_dirty = true;
     // optional phase timing (CUDA events on the eval stream)
     bool profiling = false;
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -1201,8 +1214,52 @@ static bool parity_zeros(const Mat4 &a)
         }                                                                               \
     } while (0)
 
+// host mirror of gate_frag for every lane
+static void frag_rows(const Mat4 &M, double2 *row)
+{
+    for (int lane = 0; lane < 32; ++lane) {
+        const int g = lane >> 2, t = lane & 3;
+        const double2 e = M.m[4 * (g >> 1) + t];
+        const bool pi = g & 1;
+        row[lane] = make_double2(pi ? e.y : e.x, pi ? e.x : -e.y);
+    }
+}
+
+static int upload_frags(gf_plan *p, cudaStream_t st)
+{
+    if (!p->frag_dirty && p->d_frag) return GF_OK;
+    const int n = std::max(1, p->n);
+    const size_t rows = (size_t)n * NFK;
+    if (!p->d_frag) {
+        cudaError_t e = cudaMalloc(&p->d_frag, rows * 32 * sizeof(double2));
+        if (e != cudaSuccess) return gf_fail(GF_ENOMEM, "fragment table: %s", cudaGetErrorString(e));
+    }
+    p->h_frag.assign(rows * 32, make_double2(0.0, 0.0));
+    auto put = [&](int s, int kind, const std::vector<Mat4> &v) {
+        if ((size_t)s < v.size()) frag_rows(v[s], &p->h_frag[((size_t)s * NFK + kind) * 32]);
+    };
+    for (int s = 0; s < p->n; ++s) {
+        put(s, FK_G, p->G);
+        put(s, FK_GD, p->Gd);
+        put(s, FK_GT, p->Gt);
+        put(s, FK_GC, p->Gc);
+        for (int d = 0; d < FMAXDIR; ++d) {
+            put(s, FK_ZT + d, p->Ztm[d]);
+            put(s, FK_Z + d, p->Zm[d]);
+        }
+    }
+    // pageable source: the copy is staged before the call returns, so the
+    // host mirror can be rebuilt at once
+    cudaError_t e = cudaMemcpyAsync(p->d_frag, p->h_frag.data(), rows * 32 * sizeof(double2),
+                                    cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return gf_fail(GF_ECUDA, "fragment upload: %s", cudaGetErrorString(e));
+    p->frag_dirty = false;
+    return GF_OK;
+}
+
 static void plan_free(gf_plan *p)
 {
+    cudaFree(p->d_frag);
     for (auto &e : p->ev)
         if (e) cudaEventDestroy(e);
     void *ptrs[] = {p->psi, p->bra, p->aux, p->partD, p->partHd, p->partHa, p->partV,
@@ -1270,7 +1327,7 @@ extern "C" int gf_plan_create(gf_plan **out, int k, int sector, int n_slots, con
         p->pipe = p->fused && (penv && strcmp(penv, "1") == 0);  // experimental, off by default
         const char *fmenv = getenv("GF_FUSED_M");
         // pipelined kernel double-buffers 2^10 tiles (2 CTAs/SM); the classic one uses 2^11
-        int fm = fmenv ? atoi(fmenv) : (p->pipe ? 10 : 11);
+        int fm = fmenv ? atoi(fmenv) : 11;
         p->fm = std::max(5, std::min(std::min(fm, FMAXM), p->K));
         if (p->pipe && p->fm > 11) p->pipe = false;  // two 3-vector buffers must fit in shared memory
         p->fc = std::min(4, p->fm);
@@ -1343,6 +1400,7 @@ extern "C" int gf_plan_create(gf_plan **out, int k, int sector, int n_slots, con
 
 extern "C" int gf_plan_set_gates(gf_plan *p, const double *mats)
 {
+    if (p) p->frag_dirty = true;
     if (!p || !mats) return gf_fail(GF_EINVAL, "null argument");
     p->G.resize(p->n); p->Gd.resize(p->n); p->Gt.resize(p->n); p->Gc.resize(p->n);
     p->spG.assign(p->n, 0);
@@ -1365,6 +1423,7 @@ extern "C" int gf_plan_set_gates(gf_plan *p, const double *mats)
 // (the fused engine shares psi / bra across them: full-Hessian columns).
 extern "C" int gf_plan_set_directions_multi(gf_plan *p, int nd, const double *zmats)
 {
+    if (p) p->frag_dirty = true;
     if (!p || !zmats) return gf_fail(GF_EINVAL, "null argument");
     if (nd < 1 || nd > FMAXDIR) return gf_fail(GF_EINVAL, "direction count %d outside [1, %d]", nd, FMAXDIR);
     if (nd > 1 && !p->fused) return gf_fail(GF_EINVAL, "multi-direction HVP needs the fused engine");
@@ -1532,18 +1591,18 @@ static int launch_fused_nt(const gf_plan *p, FusedParams &fp, int64_t nvec, cuda
     return GF_OK;
 }
 
-template <int OP, bool FIRST>
-static int launch_pipe(const gf_plan *p, FusedParams &fp, int64_t nvec, cudaStream_t st)
+template <int OP, bool FIRST, int NT, bool SPX>
+static int launch_pipe_nt(const gf_plan *p, FusedParams &fp, int64_t nvec, cudaStream_t st)
 {
-    constexpr int NT = 256;
     const int nv = (OP == OP_FWD || OP == OP_FWD_DOT) ? 1 : (OP == OP_REV_G ? 2 : 3);
     const size_t smem = fused_smem(2 * nv, fp.m, fp.c, NT / 32);
     static int bps = 0;
     if (bps == 0) {
-        cudaError_t ae = cudaFuncSetAttribute(k_fused_pipe<OP, FIRST, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              226 * 1024);
+        cudaError_t ae = cudaFuncSetAttribute(k_fused_pipe<OP, FIRST, NT, SPX>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
         if (ae != cudaSuccess) return gf_fail(GF_ECUDA, "k_fused_pipe smem attribute: %s", cudaGetErrorString(ae));
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_fused_pipe<OP, FIRST, NT>, NT, smem) != cudaSuccess ||
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_fused_pipe<OP, FIRST, NT, SPX>, NT, smem) !=
+                cudaSuccess ||
             bps < 1)
             bps = 1;
     }
@@ -1551,8 +1610,23 @@ static int launch_pipe(const gf_plan *p, FusedParams &fp, int64_t nvec, cudaStre
     fp.seg_tiles = p->seg_tiles;
     const unsigned long long nsegall = (fp.ntiles / fp.seg_tiles) * (unsigned long long)nvec;
     const unsigned long long grid = std::min<unsigned long long>(nsegall, (unsigned long long)p->nsm * bps);
-    k_fused_pipe<OP, FIRST, NT><<<(unsigned)grid, NT, smem, st>>>(fp);
+    k_fused_pipe<OP, FIRST, NT, SPX><<<(unsigned)grid, NT, smem, st>>>(fp);
     return GF_OK;
+}
+
+// 2^11 tiles: 512 threads, one CTA per SM holding both buffers; smaller tiles:
+// 256 threads, 2 CTAs per SM
+template <int OP, bool FIRST>
+static int launch_pipe(const gf_plan *p, FusedParams &fp, int64_t nvec, cudaStream_t st)
+{
+    bool spx = false;
+    for (int t = 0; t < fp.nslots; ++t) spx |= (fp.ps[t].mode == PM_SPARSE);
+    if (fp.m >= 11) {
+        if (spx) return launch_pipe_nt<OP, FIRST, 512, true>(p, fp, nvec, st);
+        return launch_pipe_nt<OP, FIRST, 512, false>(p, fp, nvec, st);
+    }
+    if (spx) return launch_pipe_nt<OP, FIRST, 256, true>(p, fp, nvec, st);
+    return launch_pipe_nt<OP, FIRST, 256, false>(p, fp, nvec, st);
 }
 
 // 256 threads (2 CTAs/SM) for tiles up to 2^11; 512 threads (1 CTA/SM, same 16
@@ -1655,7 +1729,9 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
     if (p->fused && n > 0) {
         FusedParams fp;
         static const bool exp_noslots = getenv("GF_EXP_NOSLOTS") != nullptr;  // timing diagnostic only
+        if (int rc_ = upload_frags(p, st)) return rc_;
         auto setup = [&](FusedParams &f) {
+            f.frag = p->d_frag;
             f.psi = p->psi;
             f.bra = p->bra;
             f.aux = p->aux;
@@ -1682,6 +1758,9 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
             for (int t = 0; t < fp.nslots; ++t) {
                 const int s = fp.ps[t].slot;
                 fp.mat[t][0] = p->G[s];
+                fp.ps[t].fa = s * NFK + FK_G;
+                fp.ps[t].fb = fp.ps[t].fa;
+                fp.ps[t].fz = fp.ps[t].fa;
                 if (fp.ps[t].mode != PM_C1Q) fp.ps[t].mode = p->spG[s] ? PM_SPARSE : PM_DENSE;
             }
             const bool last = !grad_like && pi == nf - 1;
@@ -1711,6 +1790,9 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
                     const int s = fp.ps[t].slot;
                     fp.mat[t][0] = p->Gd[s];
                     fp.mat[t][1] = p->Gt[s];
+                    fp.ps[t].fa = s * NFK + FK_GD;
+                    fp.ps[t].fb = s * NFK + FK_GT;
+                    fp.ps[t].fz = s * NFK + FK_ZT;
                     bool sp = p->spG[s];
                     fp.ps[t].zmask = 0;
                     if (h) {
@@ -1749,6 +1831,9 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
                         const int s = fp.ps[t].slot;
                         fp.mat[t][0] = p->Gc[s];
                         fp.mat[t][1] = p->G[s];
+                        fp.ps[t].fa = s * NFK + FK_GC;
+                        fp.ps[t].fb = s * NFK + FK_G;
+                        fp.ps[t].fz = s * NFK + FK_Z;
                         bool sp = p->spG[s];
                         fp.ps[t].zmask = 0;
                         for (int d = 0; d < nd; ++d) {

@@ -26,6 +26,10 @@ constexpr int FMAXDIR = 3;      // HVP directions per sweep (full-Hessian column
 
 enum { PM_DENSE = 0, PM_SPARSE = 1, PM_C1Q = 2 };
 
+// rows of the per-slot DMMA fragment table: G, G^dag, G^T, conj G, then Z_d^T
+// and Z_d per direction (row = slot * NFK + kind, 32 lanes per row)
+enum { FK_G = 0, FK_GD = 1, FK_GT = 2, FK_GC = 3, FK_ZT = 4, FK_Z = 4 + FMAXDIR, NFK = 4 + 2 * FMAXDIR };
+
 struct PassSlot {
     int slot;  // circuit slot index (for the partial layout)
     int mode;  // PM_*
@@ -33,6 +37,7 @@ struct PassSlot {
     int lhi;   // local bit index of the high target bit (unused for c1q)
     int zmask; // bit d: direction d has a nonzero Z at this slot (zero Z-terms are skipped)
     int amask; // bit d: chi_d / v_d is nonzero entering this slot (else its hole and update are skipped)
+    int fa, fb, fz;  // fragment-table rows of mat[0], mat[1], mat[2 + d] (fz + d)
 };
 
 struct FusedParams {
@@ -40,6 +45,7 @@ struct FusedParams {
     const double2 *phi0;       // [nvec][N]
     const double *weights;     // [nvec] or null
     const int64_t *basis;      // [nvec] (first forward pass synthesises |j>)
+    const double2 *frag;       // [n slots][NFK][32] per-lane DMMA B fragments (gf_plan::d_frag)
     double *partD, *partH, *partV;
     double *qD, *qH, *qV;    // per-(slot, vector) sums written by the last CTA of each vector
     unsigned int *tickets;   // [nvec] arrival counters, self-resetting
