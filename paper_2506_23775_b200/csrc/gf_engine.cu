@@ -234,12 +234,18 @@ __device__ __forceinline__ unsigned ins0u(unsigned t, int b)
     return ((t >> b) << (b + 1)) | low;
 }
 
-// XOR swizzle of the tile index (double2 granularity): folds the bits above
-// the 128-byte bank group into it so that tuple members 2^llo / 2^lhi apart
-// land in different banks (ncu: half the smem wavefronts were conflicts).
+// XOR swizzle of the tile index (double2 granularity): l ^ f(l >> 3), f a
+// GF(2)-linear map onto the 16-byte slot within the 128-byte bank row.  Bit
+// i >= 3 of l moves the slot by v_i = {7,5,6,4,6,4,6,2,3}[i-3], chosen by
+// tools/swizzle_search.py so that the quarter-warp of a gate access (tuples
+// t, t+1 x amplitudes {0, lo, hi, lo+hi}) and the half-warp of a hole access
+// (tuples 4q..4q+3 x {0, lo}) hit distinct slots for the target pairs the
+// pass planner emits (modelled excess wavefronts at c2: 28% -> 4% of ideal;
+// the earlier fold (l>>3)^(l>>5)^(l>>7)^(l>>9) mapped bits 4, 6, 8, 10 alike).
 __device__ __forceinline__ unsigned swz(unsigned l)
 {
-    return l ^ (((l >> 3) ^ (l >> 5) ^ (l >> 7) ^ (l >> 9)) & 7u);
+    const unsigned x = l >> 3;
+    return l ^ ((__popc(x & 0x103u) & 1u) | ((__popc(x & 0x1D5u) & 1u) << 1) | ((__popc(x & 0x7Fu) & 1u) << 2));
 }
 
 // B fragment (two k-steps) of the real 8x8 form of a complex 4x4 gate for
@@ -304,7 +310,7 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
         // units per active warp: multiple of 4 (hole MMA K) -- and of 8 for the
         // 2q tensor path (8-tuple groups, paired hole MMAs)
         const unsigned TW = max(nunit / (unsigned)NW, c1q ? 4u : 8u);
-        const unsigned nwa = nunit / TW;
+        const unsigned nwa = nunit >> (31 - __clz(TW));  // powers of two
         const unsigned olo = 1u << llo, ohi = 1u << lhi;
         double cD0 = 0.0, cD1 = 0.0, cH0[ND], cH1[ND];
 #pragma unroll
@@ -396,13 +402,20 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                 // ---- two-qubit slot, all FP64 math on the tensor cores (DMMA m8n8k4).
                 // Tuple -> swizzled tile index is GF(2)-linear (bit insertion +
                 // XOR swizzle), so every address is an XOR of precomputed columns.
-                auto F = [&](unsigned x) { return swz(ins0u(ins0u(x, llo), lhi)); };
-                const unsigned offA = swz(((tq & 2) ? ohi : 0u) | ((tq & 1) ? olo : 0u));
+                const PassSlot &PS = p.ps[si];
+                auto F = [&](unsigned x) {  // = swz(ins0u(ins0u(x, llo), lhi))
+                    unsigned a = 0;
+#pragma unroll
+                    for (int i = 0; i < FMAXM - 2; ++i)
+                        if ((x >> i) & 1u) a ^= PS.col[i];
+                    return a;
+                };
+                const unsigned offA = ((tq & 2) ? PS.sh : 0u) ^ ((tq & 1) ? PS.so : 0u);
                 const unsigned baseA = F(wbase + g) ^ offA;  // gate layout: lane (g, tq) = amp tq of tuple g
                 const unsigned ngrp = TW >> 3;                // groups of 8 tuples
                 unsigned colA[4];
 #pragma unroll
-                for (int i = 0; i < 4; ++i) colA[i] = F(8u << i);
+                for (int i = 0; i < 4; ++i) colA[i] = PS.col[3 + i];
                 auto addrA = [&](unsigned grp) {
                     unsigned a = baseA;
 #pragma unroll
@@ -443,11 +456,11 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                 if constexpr (HD || HH) {
                     __syncwarp();
                     // hole layout: lane (g, tq) = component g (amp g>>1, part g&1) of tuple tq
-                    const unsigned offH = swz(((gi & 2) ? ohi : 0u) | ((gi & 1) ? olo : 0u));
+                    const unsigned offH = ((gi & 2) ? PS.sh : 0u) ^ ((gi & 1) ? PS.so : 0u);
                     const unsigned baseH = F(wbase + tq) ^ offH;
                     unsigned colH[5];
 #pragma unroll
-                    for (int i = 0; i < 5; ++i) colH[i] = F(4u << i);
+                    for (int i = 0; i < 5; ++i) colH[i] = PS.col[2 + i];
                     const double *d0 = reinterpret_cast<const double *>(t0) + gpart;
                     const double *d1 = reinterpret_cast<const double *>(t1) + gpart;
                     const double *d2 = reinterpret_cast<const double *>(t2) + gpart;
@@ -699,7 +712,10 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_fused(const FusedParams p)
         // Plain copies go global -> shared with cp.async (no register round
         // trip, every element of the tile in flight at once); the synthesised
         // |j>, the zero chi/v and the weighted phi0 are written by the threads.
-        for (unsigned l = tid; l < T; l += NT) {
+        if (p.exp_noio) {
+            for (unsigned l = tid; l < NV * T; l += NT) t0[l] = czero();
+        }
+        for (unsigned l = tid; l < T && !p.exp_noio; l += NT) {
             const u64 a = base + (l & cmask) + hiofs[l >> c];
             const unsigned sl = swz(l);
             if constexpr (SYNTH)
@@ -740,7 +756,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_fused(const FusedParams p)
         run_slots<OP, NT, ND, SPX>(p, t0, t1, t2, scratch, sacc, tpop, T);
 
         const int sm = p.store_mask;
-        for (unsigned l = tid; l < T; l += NT) {
+        for (unsigned l = tid; l < T && !p.exp_noio; l += NT) {
             const u64 a = base + (l & cmask) + hiofs[l >> c];
             const double2 x = t0[swz(l)];
             if (sm & 1) psi[a] = x;
@@ -1336,6 +1352,17 @@ extern "C" int gf_plan_create(gf_plan **out, int k, int sector, int n_slots, con
             p->rev_passes = plan_passes(p, true);
             p->asc_passes.assign(p->rev_passes.rbegin(), p->rev_passes.rend());
             for (auto &f : p->asc_passes) std::reverse(f.ps, f.ps + f.nslots);
+            if (getenv("GF_DUMP_PLAN")) {  // diagnostic: per-pass local bits and slot targets
+                for (int sw = 0; sw < 2; ++sw) {
+                    const auto &v = sw ? p->rev_passes : p->fwd_passes;
+                    for (const auto &f : v) {
+                        fprintf(stderr, "%s m=%d c=%d slots:", sw ? "rev" : "fwd", f.m, f.c);
+                        for (int t = 0; t < f.nslots; ++t)
+                            fprintf(stderr, " %d:%d,%d", f.ps[t].mode, f.ps[t].llo, f.ps[t].lhi);
+                        fprintf(stderr, "\n");
+                    }
+                }
+            }
             u64 ntiles = 1ull << (p->K - p->fm);
             if (p->pipe) {
                 // partial segments: <= 4096 per vector, sized by the vector only
@@ -1484,6 +1511,15 @@ extern "C" int gf_plan_set_directions(gf_plan *p, const double *zmats)
 // sector's implicit qubit share a virtual qubit so they never reorder among
 // themselves.
 // ---------------------------------------------------------------------------
+// host copies of the kernel's tile addressing (ins0u, swz)
+static unsigned ins0u_host(unsigned t, int b) { return ((t >> b) << (b + 1)) | (t & ((1u << b) - 1u)); }
+static unsigned swz_host(unsigned l)
+{
+    const unsigned x = l >> 3;
+    return l ^ ((__builtin_popcount(x & 0x103u) & 1u) | ((__builtin_popcount(x & 0x1D5u) & 1u) << 1) |
+                ((__builtin_popcount(x & 0x7Fu) & 1u) << 2));
+}
+
 static std::vector<FusedParams> plan_passes(const gf_plan *p, bool reverse)
 {
     std::vector<FusedParams> out;
@@ -1558,6 +1594,12 @@ static std::vector<FusedParams> plan_passes(const gf_plan *p, bool reverse)
             ps.mode = si.mode_c1q ? PM_C1Q : PM_DENSE;  // sparse decided per eval
             ps.llo = lidx[si.lo];
             ps.lhi = si.mode_c1q ? 0 : lidx[si.hi];
+            if (!si.mode_c1q) {
+                for (int i = 0; i < FMAXM - 2; ++i)
+                    ps.col[i] = swz_host(ins0u_host(ins0u_host(1u << i, ps.llo), ps.lhi));
+                ps.so = swz_host(1u << ps.llo);
+                ps.sh = swz_host(1u << ps.lhi);
+            }
             fp.ps[t] = ps;
         }
         out.push_back(fp);
@@ -1750,6 +1792,8 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
             f.hstride = (u64)std::max(1, p->n) * p->max_batch * p->ctas * 32;
             f.qhstride = (u64)std::max(1, p->n) * p->max_batch * 32;
             if (exp_noslots) f.nslots = 0;
+            static const bool exp_noio = getenv("GF_EXP_NOIO") != nullptr;  // timing diagnostic only
+            f.exp_noio = exp_noio ? 1 : 0;
         };
         const int nf = (int)p->fwd_passes.size(), nr = (int)p->rev_passes.size();
         for (int pi = 0; pi < nf; ++pi) {

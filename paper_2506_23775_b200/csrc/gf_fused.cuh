@@ -38,6 +38,11 @@ struct PassSlot {
     int zmask; // bit d: direction d has a nonzero Z at this slot (zero Z-terms are skipped)
     int amask; // bit d: chi_d / v_d is nonzero entering this slot (else its hole and update are skipped)
     int fa, fb, fz;  // fragment-table rows of mat[0], mat[1], mat[2 + d] (fz + d)
+    // 2q slots: col[i] = swz(tuple index 2^i with zeros inserted at llo, lhi),
+    // so = swz(2^llo), sh = swz(2^lhi) -- the GF(2)-linear tile addressing,
+    // precomputed on the host instead of per slot and lane in the kernel
+    unsigned col[FMAXM - 2];
+    unsigned so, sh;
 };
 
 struct FusedParams {
@@ -54,6 +59,7 @@ struct FusedParams {
     unsigned long long seg_tiles;  // pipelined kernel: tiles per partial segment
     int nvec, ctas, sector;
     int m, c, nglob, nslots;
+    int exp_noio;    // timing diagnostic (GF_EXP_NOIO): skip the tile loads and stores
     int store_mask;  // bit 0 psi, bit 1 bra, bit 2 chi/v: vectors written back after the pass
     unsigned long long auxstride; // aux (chi / v) offset between directions (amplitudes)
     unsigned long long hstride;   // partH / qH offset between directions (doubles)
