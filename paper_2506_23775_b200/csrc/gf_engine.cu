@@ -801,38 +801,8 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_fused(const FusedParams p)
             p.partV[((u64)blockIdx.y * p.ctas + blockIdx.x) * 2 + tid] = s;
         }
     }
-    // The last CTA of this vector sums the per-CTA partials in ascending CTA
-    // order (deterministic whichever CTA arrives last) -- no separate
-    // reduction launch.
-    __threadfence();
-    __syncthreads();
-    __shared__ unsigned s_last;
-    if (tid == 0) s_last = (atomicAdd(&p.tickets[blockIdx.y], 1u) == (unsigned)p.ctas - 1u);
-    __syncthreads();
-    if (s_last) {
-        __threadfence();
-        const u64 b = blockIdx.y;
-        for (int i = tid; i < p.nslots * NH * 32; i += NT) {
-            const int si = i / (NH * 32), hole = (i >> 5) % NH, e = i & 31;
-            if ((hole == 0 && HD) || (hole >= 1 && HH)) {
-                const double *src = hole == 0 ? p.partD : p.partH + (u64)(hole - 1) * p.hstride;
-                double *dst = hole == 0 ? p.qD : p.qH + (u64)(hole - 1) * p.qhstride;
-                const u64 slot = (u64)p.ps[si].slot;
-                const double *q = src + ((slot * p.nvec + b) * p.ctas) * 32 + e;
-                double sum = 0.0;
-                for (int cc = 0; cc < p.ctas; ++cc) sum += __ldcg(q + (u64)cc * 32);
-                dst[(slot * p.nvec + b) * 32 + e] = sum;
-            }
-        }
-        if constexpr (HV) {
-            if (tid < 2) {
-                double sum = 0.0;
-                for (int cc = 0; cc < p.ctas; ++cc) sum += __ldcg(p.partV + (b * p.ctas + cc) * 2 + tid);
-                p.qV[b * 2 + tid] = sum;
-            }
-        }
-        if (tid == 0) p.tickets[blockIdx.y] = 0u;
-    }
+    // per-CTA partials are summed in ascending CTA order by k_reduce_ctas after
+    // the sweeps (a last-CTA reduction here cost every CTA a memory fence)
 }
 
 
@@ -1034,15 +1004,16 @@ __global__ void k_init_basis(double2 *psi, u64 N, const int64_t *basis, int64_t 
 }
 
 // part[s][b][c][32] -> q[s][b][32], summing c ascending.
-__global__ void k_reduce_ctas(const double *part, double *q, int64_t nsb, int ctas)
+// q[sb][e] = sum over c ascending of part[sb][c][e], e < ne (32 for a hole, 2 for the value)
+__global__ void k_reduce_ctas(const double *part, double *q, int64_t nsb, int ctas, int ne = 32)
 {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= nsb * 32) return;
-    int64_t sb = i >> 5;
-    int e = (int)(i & 31);
-    const double *src = part + sb * ctas * 32 + e;
+    if (i >= nsb * ne) return;
+    int64_t sb = i / ne;
+    int e = (int)(i - sb * ne);
+    const double *src = part + sb * ctas * ne + e;
     double acc = 0.0;
-    for (int c = 0; c < ctas; ++c) acc += src[(int64_t)c * 32];
+    for (int c = 0; c < ctas; ++c) acc += src[(int64_t)c * ne];
     q[i] = acc;
 }
 
@@ -1958,16 +1929,25 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
     if (!(grad_like && n > 0) && p->profiling) GF_CUDA(cudaEventRecord(p->ev[2], st));
     l_asc = launches - l_fwd - l_rev;
     if (p->profiling) GF_CUDA(cudaEventRecord(p->ev[3], st));
-    if (grad_like && n > 0 && !p->fused) {
+    if (grad_like && n > 0) {
         int64_t nsb = (int64_t)n * nvec;
         int blocks = (int)((nsb * 32 + 255) / 256);
         k_reduce_ctas<<<blocks, 256, 0, st>>>(p->partD, p->qD, nsb, p->ctas);
         ++launches;
         if (flags & GF_HVP) {
-            k_reduce_ctas<<<blocks, 256, 0, st>>>(p->partHd, p->qHd, nsb, p->ctas);
-            k_reduce_ctas<<<blocks, 256, 0, st>>>(p->partHa, p->qHa, nsb, p->ctas);
-            launches += 2;
+            const int ndr = p->fused ? nd : 1;
+            const u64 hs = (u64)std::max(1, p->n) * p->max_batch * p->ctas * 32;
+            const u64 qs = (u64)std::max(1, p->n) * p->max_batch * 32;
+            for (int d = 0; d < ndr; ++d) {
+                k_reduce_ctas<<<blocks, 256, 0, st>>>(p->partHd + d * hs, p->qHd + d * qs, nsb, p->ctas);
+                k_reduce_ctas<<<blocks, 256, 0, st>>>(p->partHa + d * hs, p->qHa + d * qs, nsb, p->ctas);
+                launches += 2;
+            }
         }
+    }
+    if (p->fused && n > 0) {
+        k_reduce_ctas<<<(unsigned)((nvec * 2 + 255) / 256), 256, 0, st>>>(p->partV, p->qV, nvec, p->ctas, 2);
+        ++launches;
     }
     {
         int64_t nchunks = (nvec + p->chunk - 1) / p->chunk;
