@@ -291,6 +291,7 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                                           double *sacc, const int tpop, const unsigned T)
 {
     constexpr int NW = NT / 32;
+    constexpr int NWB = NW >= 16 ? 4 : (NW >= 8 ? 3 : (NW >= 4 ? 2 : (NW >= 2 ? 1 : 0)));  // log2(NW)
     constexpr bool HD = (OP == OP_REV_G || OP == OP_REV_GH);
     constexpr bool HH = (OP == OP_REV_GH || OP == OP_ASC_H);
     constexpr bool REV = (OP == OP_REV_G || OP == OP_REV_GH);
@@ -403,15 +404,17 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                 // Tuple -> swizzled tile index is GF(2)-linear (bit insertion +
                 // XOR swizzle), so every address is an XOR of precomputed columns.
                 const PassSlot &PS = p.ps[si];
-                auto F = [&](unsigned x) {  // = swz(ins0u(ins0u(x, llo), lhi))
-                    unsigned a = 0;
+                // F(x) = swz(ins0u(ins0u(x, llo), lhi)) is GF(2)-linear in the
+                // tuple index x: F(wbase | t) = F(wbase) ^ F(t) for t < TW
+                const int twb = 31 - __clz(TW);
+                unsigned Fw = 0;
 #pragma unroll
-                    for (int i = 0; i < FMAXM - 2; ++i)
-                        if ((x >> i) & 1u) a ^= PS.col[i];
-                    return a;
-                };
+                for (int i = 0; i < NWB; ++i)
+                    if ((warp >> i) & 1) Fw ^= PS.col[twb + i];
+                const unsigned c0 = PS.col[0], c1 = PS.col[1], c2 = PS.col[2];
                 const unsigned offA = ((tq & 2) ? PS.sh : 0u) ^ ((tq & 1) ? PS.so : 0u);
-                const unsigned baseA = F(wbase + g) ^ offA;  // gate layout: lane (g, tq) = amp tq of tuple g
+                // gate layout: lane (g, tq) = amp tq of tuple g
+                const unsigned baseA = Fw ^ ((g & 1) ? c0 : 0u) ^ ((g & 2) ? c1 : 0u) ^ ((g & 4) ? c2 : 0u) ^ offA;
                 const unsigned ngrp = TW >> 3;                // groups of 8 tuples
                 unsigned colA[4];
 #pragma unroll
@@ -457,7 +460,7 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                     __syncwarp();
                     // hole layout: lane (g, tq) = component g (amp g>>1, part g&1) of tuple tq
                     const unsigned offH = ((gi & 2) ? PS.sh : 0u) ^ ((gi & 1) ? PS.so : 0u);
-                    const unsigned baseH = F(wbase + tq) ^ offH;
+                    const unsigned baseH = Fw ^ ((tq & 1) ? c0 : 0u) ^ ((tq & 2) ? c1 : 0u) ^ offH;
                     unsigned colH[5];
 #pragma unroll
                     for (int i = 0; i < 5; ++i) colH[i] = PS.col[2 + i];
@@ -700,6 +703,9 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_fused(const FusedParams p)
     __syncthreads();
     double vre = 0.0, vim = 0.0;
     const unsigned cmask = (1u << c) - 1u;
+    // swz is GF(2)-linear and l = tid ^ (l - tid) in the tile loops below
+    const unsigned stid = swz((unsigned)tid);
+    auto sw = [&](unsigned l) { return stid ^ swz(l ^ (unsigned)tid); };
 
     for (u64 tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
         u64 base = 0;
@@ -717,7 +723,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_fused(const FusedParams p)
         }
         for (unsigned l = tid; l < T && !p.exp_noio; l += NT) {
             const u64 a = base + (l & cmask) + hiofs[l >> c];
-            const unsigned sl = swz(l);
+            const unsigned sl = sw(l);
             if constexpr (SYNTH)
                 t0[sl] = make_double2(a == jb ? 1.0 : 0.0, 0.0);  // psi_0 = |j>, no HBM read
             else
@@ -738,11 +744,12 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_fused(const FusedParams p)
             // bra_0 = w phi0; the value <phi0|psi_n> is read back from the tile
             for (unsigned l = tid; l < T; l += NT) {
                 const u64 a = base + (l & cmask) + hiofs[l >> c];
-                t1[swz(l)] = cscale(phi0[a], w);
+                t1[sw(l)] = cscale(phi0[a], w);
             }
             cp_async_wait<0>();
             for (unsigned l = tid; l < T; l += NT) {
-                const double2 x = t0[swz(l)], b = t1[swz(l)];
+                const unsigned sl = sw(l);
+                const double2 x = t0[sl], b = t1[sl];
                 vre = fma(b.x, x.x, vre);
                 vre = fma(-b.y, x.y, vre);
                 vim = fma(b.x, x.y, vim);
@@ -758,13 +765,14 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_fused(const FusedParams p)
         const int sm = p.store_mask;
         for (unsigned l = tid; l < T && !p.exp_noio; l += NT) {
             const u64 a = base + (l & cmask) + hiofs[l >> c];
-            const double2 x = t0[swz(l)];
+            const unsigned sl = sw(l);
+            const double2 x = t0[sl];
             if (sm & 1) psi[a] = x;
-            if constexpr (NV >= 2) if (sm & 2) bra[a] = t1[swz(l)];
+            if constexpr (NV >= 2) if (sm & 2) bra[a] = t1[sl];
             if constexpr (NV >= 3) {
                 if (sm & 4) {
 #pragma unroll
-                    for (int d = 0; d < ND; ++d) aux[a + d * p.auxstride] = t2[d * T + swz(l)];
+                    for (int d = 0; d < ND; ++d) aux[a + d * p.auxstride] = t2[d * T + sl];
                 }
             }
             if constexpr (OP == OP_FWD_DOT) {
@@ -805,193 +813,6 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_fused(const FusedParams p)
     // the sweeps (a last-CTA reduction here cost every CTA a memory fence)
 }
 
-
-// ---------------------------------------------------------------------------
-// Pipelined fused pass: persistent CTAs walk fixed-size segments of tiles
-// (segment s of vector b = tiles [s*segt, (s+1)*segt)), round-robin over the
-// grid, with two tile buffers: while the slots run on one buffer, cp.async
-// streams the next tile into the other, so HBM traffic overlaps the tensor-
-// core work.  Partials are per (slot, vector, segment) -- segment geometry
-// depends only on the vector size, so sums stay bit-identical for any batch.
-// All partials are scaled by the summand weight at flush time (the engine is
-// linear in the bra), so raw target columns can be copied asynchronously.
-// ---------------------------------------------------------------------------
-template <int OP, bool FIRST, int NT, bool SPX>
-__global__ void __launch_bounds__(NT, 512 / NT) k_fused_pipe(const FusedParams p)
-{
-    constexpr int NW = NT / 32;
-    constexpr int NV = (OP == OP_FWD || OP == OP_FWD_DOT) ? 1 : (OP == OP_REV_G ? 2 : 3);
-    constexpr bool HD = (OP == OP_REV_G || OP == OP_REV_GH);
-    constexpr bool HH = (OP == OP_REV_GH || OP == OP_ASC_H);
-    constexpr bool REV = (OP == OP_REV_G || OP == OP_REV_GH);
-    constexpr bool VLOAD = REV && FIRST;          // value = phi0 . psi_n on the first reverse pass
-    constexpr bool VSTORE = (OP == OP_FWD_DOT);    // value = phi0 . psi_n after the last forward pass
-    constexpr bool SYNTH = (OP == OP_FWD || OP == OP_FWD_DOT || OP == OP_ASC_H) && FIRST;
-    constexpr bool ZERO3 = (NV >= 3) && FIRST;     // chi / v start at zero
-    extern __shared__ __align__(16) unsigned char fsm[];
-    const int m = p.m, c = p.c;
-    const unsigned T = 1u << m;
-    double2 *buf = reinterpret_cast<double2 *>(fsm);                 // [2][NV][T]
-    double *scratch = reinterpret_cast<double *>(buf + 2 * NV * T);  // [2][NW][64]
-    double *sacc = scratch + 2 * NW * 64;                            // [FMAXSLOTS][2][32]
-    u64 *hiofs = reinterpret_cast<u64 *>(sacc + FMAXSLOTS * 2 * 32);
-    __shared__ double vsum[2];
-    __shared__ unsigned s_last;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int nh = 1 << (m - c);
-    for (int h = tid; h < nh; h += NT) {
-        u64 o = 0;
-        for (int i = 0; i < m - c; ++i)
-            if ((h >> i) & 1) o |= 1ull << p.lpos[c + i];
-        hiofs[h] = o;
-    }
-    const unsigned cmask = (1u << c) - 1u;
-    const u64 segt = p.seg_tiles, nseg = p.ntiles / p.seg_tiles;
-    const u64 nsegall = nseg * (u64)p.nvec;
-
-    // flat per-CTA tile sequence: segments blockIdx.x, blockIdx.x + gridDim.x, ...
-    auto tile_of = [&](u64 k, u64 &vec, u64 &seg, u64 &tile) -> bool {
-        const u64 sidx = blockIdx.x + (k / segt) * gridDim.x;
-        if (sidx >= nsegall) return false;
-        vec = sidx / nseg;
-        seg = sidx - vec * nseg;
-        tile = seg * segt + (k % segt);
-        return true;
-    };
-    auto tile_base = [&](u64 tile) {
-        u64 base = 0;
-        for (int i = 0; i < p.nglob; ++i)
-            if ((tile >> i) & 1ull) base |= 1ull << p.gpos[i];
-        return base;
-    };
-    auto issue = [&](u64 k, int sel) {
-        u64 vec, seg, tile;
-        if (tile_of(k, vec, seg, tile)) {
-            const u64 base = tile_base(tile) + vec * p.N;
-            double2 *dst = buf + (u64)sel * NV * T;
-            for (unsigned l = tid; l < T; l += NT) {
-                const u64 a = base + (l & cmask) + hiofs[l >> c];
-                const unsigned s = swz(l);
-                if constexpr (!SYNTH) cp_async16(dst + s, p.psi + a);
-                if constexpr (NV >= 2) cp_async16(dst + T + s, (REV && FIRST) ? (p.phi0 + a) : (p.bra + a));
-                if constexpr (NV >= 3 && !FIRST) cp_async16(dst + 2 * T + s, p.aux + a);
-            }
-        }
-        cp_async_commit();
-    };
-
-    for (int i = tid; i < FMAXSLOTS * 2 * 32; i += NT) sacc[i] = 0.0;
-    __syncthreads();
-    issue(0, 0);
-    double vre = 0.0, vim = 0.0;
-    int cur = 0;
-    for (u64 k = 0;; ++k) {
-        u64 vec, seg, tile;
-        if (!tile_of(k, vec, seg, tile)) break;
-        issue(k + 1, cur ^ 1);  // prefetch the next tile while this one computes
-        cp_async_wait<1>();
-        __syncthreads();
-        double2 *t0 = buf + (u64)cur * NV * T, *t1 = t0 + T, *t2 = t0 + 2 * T;
-        const u64 base = tile_base(tile) + vec * p.N;
-        if constexpr (SYNTH || ZERO3 || VLOAD) {
-            const u64 jb = SYNTH ? (u64)p.basis[vec] + vec * p.N : 0ull;
-            for (unsigned l = tid; l < T; l += NT) {
-                const unsigned s = swz(l);
-                if constexpr (SYNTH) {
-                    const u64 a = base + (l & cmask) + hiofs[l >> c];
-                    t0[s] = make_double2(a == jb ? 1.0 : 0.0, 0.0);  // psi_0 = |j>, no HBM read
-                }
-                if constexpr (ZERO3) t2[s] = czero();
-                if constexpr (VLOAD) {
-                    const double2 b = t1[s], x = t0[s];
-                    vre = fma(b.x, x.x, vre);
-                    vre = fma(-b.y, x.y, vre);
-                    vim = fma(b.x, x.y, vim);
-                    vim = fma(b.y, x.x, vim);
-                }
-            }
-            __syncthreads();
-        }
-        run_slots<OP, NT, 1, SPX>(p, t0, t1, t2, scratch, sacc, __popcll(tile), T);
-        const int sm = p.store_mask;
-        for (unsigned l = tid; l < T; l += NT) {
-            const u64 a = base + (l & cmask) + hiofs[l >> c];
-            const unsigned s = swz(l);
-            const double2 x = t0[s];
-            if (sm & 1) p.psi[a] = x;
-            if constexpr (NV >= 2) if (sm & 2) p.bra[a] = t1[s];
-            if constexpr (NV >= 3) if (sm & 4) p.aux[a] = t2[s];
-            if constexpr (VSTORE) {
-                const double2 f = p.phi0[a];
-                vre = fma(f.x, x.x, vre);
-                vre = fma(-f.y, x.y, vre);
-                vim = fma(f.x, x.y, vim);
-                vim = fma(f.y, x.x, vim);
-            }
-        }
-        // segment finished: flush its partials (scaled by the summand weight)
-        if ((k + 1) % segt == 0) {
-            const double w = p.weights ? p.weights[vec] : 1.0;
-            __syncthreads();
-            for (int i = tid; i < p.nslots * 64; i += NT) {
-                const int si = i >> 6, hole = (i >> 5) & 1, e = i & 31;
-                if ((hole == 0 && HD) || (hole == 1 && HH)) {
-                    double *dst = hole == 0 ? p.partD : p.partH;
-                    const u64 slot = (u64)p.ps[si].slot;
-                    dst[((slot * p.nvec + vec) * nseg + seg) * 32 + e] = w * sacc[(si * 2 + hole) * 32 + e];
-                }
-                sacc[i] = 0.0;
-            }
-            if constexpr (VLOAD || VSTORE) {
-                vre = warp_sum(vre);
-                vim = warp_sum(vim);
-                if (lane == 0) {
-                    scratch[warp * 2] = vre;
-                    scratch[warp * 2 + 1] = vim;
-                }
-                __syncthreads();
-                if (tid < 2) {
-                    double s = 0.0;
-                    for (int ww = 0; ww < NW; ++ww) s += scratch[ww * 2 + tid];
-                    p.partV[(vec * nseg + seg) * 2 + tid] = w * s;
-                }
-                vre = vim = 0.0;
-            }
-            // the last segment of this vector to finish reduces its partials
-            __threadfence();
-            __syncthreads();
-            if (tid == 0) s_last = (atomicAdd(&p.tickets[vec], 1u) == (unsigned)nseg - 1u);
-            __syncthreads();
-            if (s_last) {
-                __threadfence();
-                for (int i = tid; i < p.nslots * 64; i += NT) {
-                    const int si = i >> 6, hole = (i >> 5) & 1, e = i & 31;
-                    if ((hole == 0 && HD) || (hole == 1 && HH)) {
-                        const double *src = hole == 0 ? p.partD : p.partH;
-                        double *dst = hole == 0 ? p.qD : p.qH;
-                        const u64 slot = (u64)p.ps[si].slot;
-                        const double *q = src + ((slot * p.nvec + vec) * nseg) * 32 + e;
-                        double sum = 0.0;
-                        for (u64 sg = 0; sg < nseg; ++sg) sum += __ldcg(q + sg * 32);
-                        dst[(slot * p.nvec + vec) * 32 + e] = sum;
-                    }
-                }
-                if constexpr (VLOAD || VSTORE) {
-                    if (tid < 2) {
-                        double sum = 0.0;
-                        for (u64 sg = 0; sg < nseg; ++sg) sum += __ldcg(p.partV + (vec * nseg + sg) * 2 + tid);
-                        p.qV[vec * 2 + tid] = sum;
-                    }
-                }
-                if (tid == 0) p.tickets[vec] = 0u;
-            }
-        }
-        __syncthreads();  // buffer `cur` is free for the prefetch issued next iteration
-        cur ^= 1;
-    }
-    cp_async_wait<0>();
-    (void)vsum;
-}
 
 // |j> for every vector of the batch (basis index per vector).
 __global__ void k_init_basis(double2 *psi, u64 N, const int64_t *basis, int64_t nvec)
@@ -1124,16 +945,12 @@ struct gf_plan {
     double2 *psi = nullptr, *bra = nullptr, *aux = nullptr;
     double *partD = nullptr, *partHd = nullptr, *partHa = nullptr, *partV = nullptr;
     double *qD = nullptr, *qHd = nullptr, *qHa = nullptr, *qV = nullptr;
-    unsigned int *tickets = nullptr;
     int *d_lstart = nullptr, *d_lslots = nullptr, *d_swapped = nullptr;
     int64_t last_launches = 0;
     int last_flags = 0;
     // fused tile engine
     bool fused = false;
-    bool pipe = false;   // pipelined persistent variant (k_fused_pipe)
     int fm = 0, fc = 0;
-    unsigned long long seg_tiles = 1;
-    int nsm = 148;
     // geometry only (matrices filled per eval).  The ascending HVP sweep must
     // replay exactly the reverse slot order of the reverse sweep (the two HVP
     // half-sums are only order-invariant together), so asc_passes is
@@ -1250,7 +1067,7 @@ static void plan_free(gf_plan *p)
     for (auto &e : p->ev)
         if (e) cudaEventDestroy(e);
     void *ptrs[] = {p->psi, p->bra, p->aux, p->partD, p->partHd, p->partHa, p->partV,
-                    p->qD, p->qHd, p->qHa, p->qV, p->tickets, p->d_lstart, p->d_lslots, p->d_swapped};
+                    p->qD, p->qHd, p->qHa, p->qV, p->d_lstart, p->d_lslots, p->d_swapped};
     for (void *q : ptrs)
         if (q) cudaFree(q);
 }
@@ -1310,13 +1127,9 @@ extern "C" int gf_plan_create(gf_plan **out, int k, int sector, int n_slots, con
     {
         const char *eng = getenv("GF_ENGINE");
         p->fused = p->K >= 6 && !(eng && strcmp(eng, "stream") == 0);
-        const char *penv = getenv("GF_PIPE");
-        p->pipe = p->fused && (penv && strcmp(penv, "1") == 0);  // experimental, off by default
         const char *fmenv = getenv("GF_FUSED_M");
-        // pipelined kernel double-buffers 2^10 tiles (2 CTAs/SM); the classic one uses 2^11
-        int fm = fmenv ? atoi(fmenv) : 11;
+        int fm = fmenv ? atoi(fmenv) : 11;  // 2^11 tiles: three vectors fit 2 CTAs per SM
         p->fm = std::max(5, std::min(std::min(fm, FMAXM), p->K));
-        if (p->pipe && p->fm > 11) p->pipe = false;  // two 3-vector buffers must fit in shared memory
         p->fc = std::min(4, p->fm);
         if (p->fused) {
             p->fwd_passes = plan_passes(p, false);
@@ -1335,16 +1148,7 @@ extern "C" int gf_plan_create(gf_plan **out, int k, int sector, int n_slots, con
                 }
             }
             u64 ntiles = 1ull << (p->K - p->fm);
-            if (p->pipe) {
-                // partial segments: <= 4096 per vector, sized by the vector only
-                const char *senv = getenv("GF_SEG_TILES");
-                p->seg_tiles = senv ? std::max<u64>(1, std::min<u64>((u64)atoll(senv), ntiles))
-                                    : std::max<u64>(1, ntiles / 4096);
-                p->ctas = (int)(ntiles / p->seg_tiles);
-                int dev = 0, nsm = 148;
-                cudaGetDevice(&dev);
-                if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess) p->nsm = nsm;
-            } else {
+            {
                 const char *cenv = getenv("GF_FUSED_CTAS");
                 u64 want = cenv ? (u64)atoll(cenv) : (u64)(148 * 8);  // all tiles, up to 8 per SM
                 p->ctas = (int)std::max<u64>(1, std::min<u64>(want, ntiles));
@@ -1367,8 +1171,6 @@ extern "C" int gf_plan_create(gf_plan **out, int k, int sector, int n_slots, con
     if (e == cudaSuccess) e = cudaMalloc(&p->qHd, qbytes);
     if (e == cudaSuccess) e = cudaMalloc(&p->qHa, qbytes);
     if (e == cudaSuccess) e = cudaMalloc(&p->qV, sizeof(double) * 2 * (size_t)max_batch);
-    if (e == cudaSuccess) e = cudaMalloc(&p->tickets, sizeof(unsigned int) * (size_t)max_batch);
-    if (e == cudaSuccess) e = cudaMemset(p->tickets, 0, sizeof(unsigned int) * (size_t)max_batch);
     // logical -> slot CSR
     std::vector<int> lstart(n_logical + 1, 0), lslots, sw(std::max(1, n_slots), 0);
     for (int l = 0; l < n_logical; ++l) {
@@ -1604,44 +1406,6 @@ static int launch_fused_nt(const gf_plan *p, FusedParams &fp, int64_t nvec, cuda
     return GF_OK;
 }
 
-template <int OP, bool FIRST, int NT, bool SPX>
-static int launch_pipe_nt(const gf_plan *p, FusedParams &fp, int64_t nvec, cudaStream_t st)
-{
-    const int nv = (OP == OP_FWD || OP == OP_FWD_DOT) ? 1 : (OP == OP_REV_G ? 2 : 3);
-    const size_t smem = fused_smem(2 * nv, fp.m, fp.c, NT / 32);
-    static int bps = 0;
-    if (bps == 0) {
-        cudaError_t ae = cudaFuncSetAttribute(k_fused_pipe<OP, FIRST, NT, SPX>,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
-        if (ae != cudaSuccess) return gf_fail(GF_ECUDA, "k_fused_pipe smem attribute: %s", cudaGetErrorString(ae));
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_fused_pipe<OP, FIRST, NT, SPX>, NT, smem) !=
-                cudaSuccess ||
-            bps < 1)
-            bps = 1;
-    }
-    if (smem > 226 * 1024) return gf_fail(GF_EINVAL, "pipelined tile needs %zu B of shared memory", smem);
-    fp.seg_tiles = p->seg_tiles;
-    const unsigned long long nsegall = (fp.ntiles / fp.seg_tiles) * (unsigned long long)nvec;
-    const unsigned long long grid = std::min<unsigned long long>(nsegall, (unsigned long long)p->nsm * bps);
-    k_fused_pipe<OP, FIRST, NT, SPX><<<(unsigned)grid, NT, smem, st>>>(fp);
-    return GF_OK;
-}
-
-// 2^11 tiles: 512 threads, one CTA per SM holding both buffers; smaller tiles:
-// 256 threads, 2 CTAs per SM
-template <int OP, bool FIRST>
-static int launch_pipe(const gf_plan *p, FusedParams &fp, int64_t nvec, cudaStream_t st)
-{
-    bool spx = false;
-    for (int t = 0; t < fp.nslots; ++t) spx |= (fp.ps[t].mode == PM_SPARSE);
-    if (fp.m >= 11) {
-        if (spx) return launch_pipe_nt<OP, FIRST, 512, true>(p, fp, nvec, st);
-        return launch_pipe_nt<OP, FIRST, 512, false>(p, fp, nvec, st);
-    }
-    if (spx) return launch_pipe_nt<OP, FIRST, 256, true>(p, fp, nvec, st);
-    return launch_pipe_nt<OP, FIRST, 256, false>(p, fp, nvec, st);
-}
-
 // 256 threads (2 CTAs/SM) for tiles up to 2^11; 512 threads (1 CTA/SM, same 16
 // warps per SM) for 2^12 tiles and for multi-direction HVP sweeps (2 + ND
 // vectors per tile)
@@ -1665,7 +1429,6 @@ static int launch_fused_sp(const gf_plan *p, FusedParams &fp, int64_t nvec, cuda
 template <int OP, bool FIRST>
 static int launch_fused(const gf_plan *p, FusedParams &fp, int64_t nvec, cudaStream_t st, int nd = 1)
 {
-    if (nd < 2 && p->pipe) return launch_pipe<OP, FIRST>(p, fp, nvec, st);
     bool spx = false;
     for (int t = 0; t < fp.nslots; ++t) spx |= (fp.ps[t].mode == PM_SPARSE);
     if (spx) return launch_fused_sp<OP, FIRST, true>(p, fp, nvec, st, nd);
@@ -1756,7 +1519,6 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
             f.sector = p->sector < 0 ? 0 : p->sector;
             f.partV = p->partV;
             f.qV = p->qV;
-            f.tickets = p->tickets;
             f.basis = basis;
             f.store_mask = 7;
             f.auxstride = p->N * (u64)p->max_batch;

@@ -52,11 +52,9 @@ struct FusedParams {
     const int64_t *basis;      // [nvec] (first forward pass synthesises |j>)
     const double2 *frag;       // [n slots][NFK][32] per-lane DMMA B fragments (gf_plan::d_frag)
     double *partD, *partH, *partV;
-    double *qD, *qH, *qV;    // per-(slot, vector) sums written by the last CTA of each vector
-    unsigned int *tickets;   // [nvec] arrival counters, self-resetting
+    double *qD, *qH, *qV;    // per-(slot, vector) sums (k_reduce_ctas)
     unsigned long long N;
     unsigned long long ntiles;  // 2^(K-m)
-    unsigned long long seg_tiles;  // pipelined kernel: tiles per partial segment
     int nvec, ctas, sector;
     int m, c, nglob, nslots;
     int exp_noio;    // timing diagnostic (GF_EXP_NOIO): skip the tile loads and stores

@@ -253,7 +253,7 @@ def _get_plan(circuit: Circuit, sector: int, batch: int, chunk: int) -> EnginePl
     t1, t2, lid = circuit.slot_arrays()
     key = (torch.cuda.current_device(), circuit.num_qubits, sector, t1.tobytes(), t2.tobytes(), lid.tobytes(),
            circuit.num_logical, batch, chunk, os.environ.get("GF_ENGINE"), os.environ.get("GF_FUSED_M"),
-           os.environ.get("GF_FUSED_CTAS"), os.environ.get("GF_PIPE"), os.environ.get("GF_SEG_TILES"))
+           os.environ.get("GF_FUSED_CTAS"))
     plan = _PLANS.get(key)
     if plan is None:
         while len(_PLANS) >= 4:
