@@ -426,6 +426,11 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                         if ((grp >> i) & 1u) a ^= colA[i];
                     return a;
                 };
+                // offsets of group u of a block of 8 (u known at compile time in
+                // the unrolled loops: one or two XORs per address, no predicates)
+                auto gcomb = [&](unsigned u) {
+                    return ((u & 1u) ? colA[0] : 0u) ^ ((u & 2u) ? colA[1] : 0u) ^ ((u & 4u) ? colA[2] : 0u);
+                };
                 double2 *V = (OP == OP_ASC_H) ? t1 : t0;
                 // SPX: the pass has sparse slots; dense-only passes compile
                 // without the sparse branch (it costs them registers and
@@ -450,10 +455,14 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                     // constant cache)
                     const double2 fA = __ldg(&p.frag[p.ps[si].fa * 32 + lane]);
                     const double fa0 = fA.x, fa1 = fA.y;
-#pragma unroll 8
-                    for (unsigned grp = 0; grp < ngrp; ++grp) {
-                        const unsigned ad = addrA(grp);
-                        V[ad] = dmma_mv(V[ad], fa0, fa1);
+                    for (unsigned gb = 0; gb < ngrp; gb += 8) {
+                        const unsigned ab = addrA(gb);
+#pragma unroll
+                        for (unsigned u = 0; u < 8; ++u) {
+                            if (gb + u >= ngrp) break;  // ngrp < 8 only for tiny tiles
+                            const unsigned ad = ab ^ gcomb(u);
+                            V[ad] = dmma_mv(V[ad], fa0, fa1);
+                        }
                     }
                 }
                 if constexpr (HD || HH) {
@@ -475,12 +484,16 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                     // (ND == 1, hoisted out of the loop), 2 = test amask per d
                     auto hole_loop = [&](auto AC) {
                         constexpr int A = decltype(AC)::value;
-#pragma unroll 4
-                        for (unsigned q = 0; q < nq; q += 2) {
-                            unsigned a0 = baseH;
+                        for (unsigned qb = 0; qb < nq; qb += 8) {
+                          unsigned ab = baseH;
 #pragma unroll
-                            for (int i = 1; i < 5; ++i)
-                                if ((q >> i) & 1u) a0 ^= colH[i];
+                          for (int i = 3; i < 5; ++i)
+                              if ((qb >> i) & 1u) ab ^= colH[i];
+#pragma unroll
+                          for (unsigned u = 0; u < 8; u += 2) {
+                            const unsigned q = qb + u;
+                            if (q >= nq) break;  // nq < 8 only for tiny tiles
+                            const unsigned a0 = ab ^ ((u & 2u) ? colH[1] : 0u) ^ ((u & 4u) ? colH[2] : 0u);
                             const unsigned a1 = a0 ^ colH[0];
                             const unsigned o0 = 2 * a0, o1 = 2 * a1;
                             if constexpr (REV) {
@@ -504,6 +517,7 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                                     dmma(eH0[d], eH1[d], b1, d2[2 * d * T + o1]);
                                 }
                             }
+                          }
                         }
                     };
                     if constexpr (ND == 1 && HH) {
@@ -592,9 +606,12 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                     // compile time (ND == 1, hoisted), 2 = test the masks per d
                     auto grp_loop = [&](auto AC, auto ZC) {
                         constexpr int A = decltype(AC)::value, Z = decltype(ZC)::value;
-#pragma unroll 8
-                        for (unsigned grp = 0; grp < ngrp; ++grp) {
-                            const unsigned ad = addrA(grp);
+                        for (unsigned gb = 0; gb < ngrp; gb += 8) {
+                          const unsigned ab = addrA(gb);
+#pragma unroll
+                          for (unsigned u = 0; u < 8; ++u) {
+                            if (gb + u >= ngrp) break;  // ngrp < 8 only for tiny tiles
+                            const unsigned ad = ab ^ gcomb(u);
                             const double2 x = REV ? t1[ad] : t0[ad];
                             if constexpr (OP == OP_REV_GH || OP == OP_ASC_H) {
 #pragma unroll
@@ -609,6 +626,7 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                             }
                             if constexpr (REV) t1[ad] = dmma_mv(x, fb0, fb1);
                             else t0[ad] = dmma_mv(x, fb0, fb1);
+                          }
                         }
                     };
                     if constexpr (ND == 1 && (OP == OP_REV_GH || OP == OP_ASC_H)) {
