@@ -20,6 +20,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -281,14 +282,14 @@ __device__ __forceinline__ double2 dmma_mv2(double2 x, double b0, double b1, dou
 
 // The slots of one pass applied to a tile staged in shared memory (t0 = psi,
 // t1 = bra, t2 + d*T = chi_d (REV) / v_d (ASC) for ND directions); hole
-// partials accumulate into sacc[slot][1 + ND][32] (hole 0 = gradient D,
+// partials go to partD / partH[slot][vector][cta][32] (hole 0 = gradient D,
 // hole 1 + d = HVP direction d).
 template <int V>
 using IC = std::integral_constant<int, V>;
 
 template <int OP, int NT, int ND, bool SPX>
 __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, double2 *t1, double2 *t2, double *scratch,
-                                          double *sacc, const int tpop, const unsigned T)
+                                          const u64 pofs, const bool accum, const int tpop, const unsigned T)
 {
     constexpr int NW = NT / 32;
     constexpr int NWB = NW >= 16 ? 4 : (NW >= 8 ? 3 : (NW >= 4 ? 2 : (NW >= 2 ? 1 : 0)));  // log2(NW)
@@ -674,7 +675,11 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                     const int i = tid & 31;
                     double sum = 0.0;
                     for (unsigned ww = 0; ww < nwa; ++ww) sum += sbuf[(hole * NW + ww) * 32 + i];
-                    sacc[(si * NH + hole) * 32 + i] += sum;
+                    // this CTA's partial of this slot (accumulated over its tiles in
+                    // tile order; one tile per CTA by default)
+                    double *dst = (hole == 0 ? p.partD : p.partH + (u64)(hole - 1) * p.hstride) +
+                                  (u64)p.ps[si].slot * p.nvec * p.ctas * 32 + pofs + i;
+                    *dst = accum ? *dst + sum : sum;
                 }
             }
         } else {
@@ -700,8 +705,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_fused(const FusedParams p)
     double2 *t1 = t0 + T;                            // bra
     double2 *t2 = t0 + 2 * T;                        // chi_d (REV) / v_d (ASC), ND tiles
     double *scratch = reinterpret_cast<double *>(t0 + NV * T);  // [NH][NW][64]
-    double *sacc = scratch + NH * NW * 64;                      // [FMAXSLOTS][NH][32]
-    u64 *hiofs = reinterpret_cast<u64 *>(sacc + FMAXSLOTS * NH * 32);
+    u64 *hiofs = reinterpret_cast<u64 *>(scratch + NH * NW * 64);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const u64 vb = (u64)blockIdx.y * p.N;
     double2 *psi = p.psi + vb;
@@ -717,7 +721,6 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_fused(const FusedParams p)
             if ((h >> i) & 1) o |= 1ull << p.lpos[c + i];
         hiofs[h] = o;
     }
-    for (int i = tid; i < FMAXSLOTS * NH * 32; i += NT) sacc[i] = 0.0;
     __syncthreads();
     double vre = 0.0, vim = 0.0;
     const unsigned cmask = (1u << c) - 1u;
@@ -778,7 +781,8 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_fused(const FusedParams p)
         }
         __syncthreads();
 
-        run_slots<OP, NT, ND, SPX>(p, t0, t1, t2, scratch, sacc, tpop, T);
+        run_slots<OP, NT, ND, SPX>(p, t0, t1, t2, scratch, ((u64)blockIdx.y * p.ctas + blockIdx.x) * 32,
+                                   tile != blockIdx.x, tpop, T);
 
         const int sm = p.store_mask;
         for (unsigned l = tid; l < T && !p.exp_noio; l += NT) {
@@ -804,14 +808,6 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_fused(const FusedParams p)
         __syncthreads();
     }
 
-    for (int i = tid; i < p.nslots * NH * 32; i += NT) {
-        const int si = i / (NH * 32), hole = (i >> 5) % NH, e = i & 31;
-        if ((hole == 0 && HD) || (hole >= 1 && HH)) {
-            double *dst = hole == 0 ? p.partD : p.partH + (u64)(hole - 1) * p.hstride;
-            const u64 slot = (u64)p.ps[si].slot;
-            dst[((slot * p.nvec + blockIdx.y) * p.ctas + blockIdx.x) * 32 + e] = sacc[(si * NH + hole) * 32 + e];
-        }
-    }
     if constexpr (HV) {
         vre = warp_sum(vre);
         vim = warp_sum(vim);
@@ -1148,7 +1144,7 @@ extern "C" int gf_plan_create(gf_plan **out, int k, int sector, int n_slots, con
         const char *fmenv = getenv("GF_FUSED_M");
         int fm = fmenv ? atoi(fmenv) : 11;  // 2^11 tiles: three vectors fit 2 CTAs per SM
         p->fm = std::max(5, std::min(std::min(fm, FMAXM), p->K));
-        p->fc = std::min(4, p->fm);
+        p->fc = std::min(3, p->fm);  // 2^3-amplitude (128 B) contiguous runs: full DRAM lines, more planner freedom
         if (p->fused) {
             p->fwd_passes = plan_passes(p, false);
             p->rev_passes = plan_passes(p, true);
@@ -1311,10 +1307,114 @@ static unsigned swz_host(unsigned l)
                 ((__builtin_popcount(x & 0x7Fu) & 1u) << 2));
 }
 
+struct PassChoice {
+    std::vector<int> slots;    // in execution order
+    unsigned long long S = 0;  // local bit set (m bits)
+};
+
+// Exact beam over local-bit sets: a pass is fixed by its local set S (the c
+// low bits plus m - c others); it executes, in sweep order, every remaining
+// slot whose bits lie in S and that no skipped earlier slot blocks (up to
+// FMAXSLOTS).  Expands every S from the best `beam` states per depth and stops
+// at the first depth that executes all slots.  Used when the sets are few
+// (c2: C(13, 8) = 1287 at m = 11, c = 3) and the slots fit a 64-bit mask.
+static bool plan_exact(const gf_plan *p, const std::vector<int> &order, int m, int c, int max_depth,
+                       std::vector<PassChoice> &out)
+{
+    const int n = (int)order.size(), K = p->K, nf = K - c, kf = m - c;
+    if (n > 64 || nf > 40 || kf < 0 || kf > nf) return false;
+    double comb = 1.0;
+    for (int i = 0; i < kf; ++i) comb = comb * (nf - i) / (i + 1);
+    if (comb > 20000.0) return false;
+    const int VIRT = 63;
+    std::vector<unsigned long long> bits(n), dep(n);
+    for (int t = 0; t < n; ++t) {
+        const SlotInfo &si = p->slots[order[t]];
+        bits[t] = si.mode_c1q ? (1ull << si.lo) : ((1ull << si.lo) | (1ull << si.hi));
+        dep[t] = bits[t] | (si.mode_c1q ? (1ull << VIRT) : 0ull);
+    }
+    std::vector<unsigned long long> sets;
+    const unsigned long long low = (1ull << c) - 1ull;
+    if (kf == 0) {
+        sets.push_back(low);
+    } else {
+        for (unsigned long long x = (1ull << kf) - 1ull; x < (1ull << nf);) {
+            sets.push_back(low | (x << c));
+            const unsigned long long u = x & (~x + 1ull), v = x + u;  // Gosper's hack
+            x = v + (((v ^ x) / u) >> 2);
+        }
+    }
+    auto execute = [&](unsigned long long done, unsigned long long S) {
+        unsigned long long blocked = 0ull, taken = 0ull;
+        int cnt = 0;
+        for (int t = 0; t < n; ++t) {
+            if ((done >> t) & 1ull) continue;
+            if (dep[t] & blocked) {
+                blocked |= dep[t];
+                continue;
+            }
+            if (!(bits[t] & ~S) && cnt < FMAXSLOTS) {
+                taken |= 1ull << t;
+                ++cnt;
+            } else {
+                blocked |= dep[t];
+            }
+        }
+        return taken;
+    };
+    const unsigned long long all = n == 64 ? ~0ull : ((1ull << n) - 1ull);
+    struct St {
+        unsigned long long done;
+        std::vector<std::pair<unsigned long long, unsigned long long>> hist;  // (taken, S)
+    };
+    std::vector<St> cur(1);
+    cur[0].done = 0ull;
+    const size_t beam = 1500;
+    for (int depth = 1; depth <= max_depth; ++depth) {
+        std::map<unsigned long long, size_t> seen;
+        std::vector<St> nxt;
+        for (const St &s : cur) {
+            for (unsigned long long S : sets) {
+                const unsigned long long tk = execute(s.done, S);
+                if (!tk) continue;
+                const unsigned long long nd = s.done | tk;
+                if (seen.count(nd)) continue;
+                seen[nd] = nxt.size();
+                St e;
+                e.done = nd;
+                e.hist = s.hist;
+                e.hist.push_back({tk, S});
+                nxt.push_back(std::move(e));
+            }
+        }
+        if (nxt.empty()) return false;
+        std::stable_sort(nxt.begin(), nxt.end(), [](const St &a, const St &b) {
+            const int pa = __builtin_popcountll(a.done), pb = __builtin_popcountll(b.done);
+            return pa != pb ? pa > pb : a.done < b.done;
+        });
+        if (nxt[0].done == all) {
+            out.clear();
+            for (const auto &h : nxt[0].hist) {
+                PassChoice pc;
+                pc.S = h.second;
+                for (int t = 0; t < n; ++t)
+                    if ((h.first >> t) & 1ull) pc.slots.push_back(order[t]);
+                out.push_back(pc);
+            }
+            return true;
+        }
+        if (nxt.size() > beam) nxt.resize(beam);
+        cur.swap(nxt);
+    }
+    return false;
+}
+
 static std::vector<FusedParams> plan_passes(const gf_plan *p, bool reverse)
 {
     std::vector<FusedParams> out;
     const int n = p->n, K = p->K, m = p->fm, c = p->fc;
+    std::vector<PassChoice> choice;
+    {
     std::vector<int> remaining;
     for (int i = 0; i < n; ++i) remaining.push_back(reverse ? n - 1 - i : i);
     const int VIRT = 63;
@@ -1361,6 +1461,25 @@ static std::vector<FusedParams> plan_passes(const gf_plan *p, bool reverse)
             }
         }
         for (int b = 0; __builtin_popcountll(S) < m && b < K; ++b) S |= 1ull << b;  // pad with low bits
+        PassChoice pc;
+        pc.slots = taken;
+        pc.S = S;
+        choice.push_back(pc);
+        remaining = rest;
+    }
+    }
+    // fewer passes (fewer tile round trips and launches) from the exact search
+    // when it is affordable
+    {
+        std::vector<int> order;
+        for (int i = 0; i < n; ++i) order.push_back(reverse ? n - 1 - i : i);
+        std::vector<PassChoice> ex;
+        if (choice.size() > 1 && !getenv("GF_PLAN_GREEDY") && plan_exact(p, order, m, c, (int)choice.size() - 1, ex))
+            choice = ex;
+    }
+    for (const PassChoice &pc : choice) {
+        const std::vector<int> &taken = pc.slots;
+        const unsigned long long S = pc.S;
         FusedParams fp;
         memset(&fp, 0, sizeof fp);
         fp.m = m;
@@ -1394,14 +1513,13 @@ static std::vector<FusedParams> plan_passes(const gf_plan *p, bool reverse)
             fp.ps[t] = ps;
         }
         out.push_back(fp);
-        remaining = rest;
     }
     return out;
 }
 
 static size_t fused_smem(int nv, int m, int c, int nw, int nd = 1)
 {
-    return sizeof(double2) * ((size_t)nv << m) + sizeof(double) * ((1 + nd) * nw * 64 + FMAXSLOTS * (1 + nd) * 32) +
+    return sizeof(double2) * ((size_t)nv << m) + sizeof(double) * ((1 + nd) * nw * 64) +
            sizeof(unsigned long long) * ((size_t)1 << (m - c));
 }
 

@@ -20,7 +20,7 @@ namespace gf {
 
 constexpr int FT = 256;         // threads per fused CTA (8 warps)
 constexpr int FMAXM = 12;       // max local bits
-constexpr int FMAXSLOTS = 14;   // max slots per pass (2 CTAs/SM of m=11 tiles fit 14)
+constexpr int FMAXSLOTS = 16;   // max slots per pass (kernel parameter space: 16 x 5 Mat4)
 constexpr int FMAXGLOB = 40;
 constexpr int FMAXDIR = 3;      // HVP directions per sweep (full-Hessian columns)
 
