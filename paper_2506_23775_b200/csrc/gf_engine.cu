@@ -437,6 +437,18 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                 // without the sparse branch (it costs them registers and
                 // scheduling freedom even when never taken)
                 const bool sparse = SPX && (mode == PM_SPARSE);
+                // this lane's DMMA B fragments, issued before the gate phase so
+                // the update phase does not wait on them
+                double2 fB = make_double2(0.0, 0.0), fZ[ND];
+#pragma unroll
+                for (int d = 0; d < ND; ++d) fZ[d] = make_double2(0.0, 0.0);
+                if (!sparse) {
+                    if constexpr (OP != OP_FWD && OP != OP_FWD_DOT) fB = __ldg(&p.frag[PS.fb * 32 + lane]);
+                    if constexpr (OP == OP_REV_GH || OP == OP_ASC_H) {
+#pragma unroll
+                        for (int d = 0; d < ND; ++d) fZ[d] = __ldg(&p.frag[(PS.fz + d) * 32 + lane]);
+                    }
+                }
                 if (sparse) {
                     // parity-conserving gates: half of G is structural zeros, so the
                     // sparse FMA form does half the flops of the dense DMMA form
@@ -592,16 +604,11 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                     }
                 } else {
                     double fc0[ND], fc1[ND];
-                    const double2 fB = __ldg(&p.frag[p.ps[si].fb * 32 + lane]);
                     const double fb0 = fB.x, fb1 = fB.y;
 #pragma unroll
                     for (int d = 0; d < ND; ++d) {
-                        fc0[d] = fc1[d] = 0.0;
-                        if (OP == OP_REV_GH || OP == OP_ASC_H) {
-                            const double2 fZ = __ldg(&p.frag[(p.ps[si].fz + d) * 32 + lane]);
-                            fc0[d] = fZ.x;
-                            fc1[d] = fZ.y;
-                        }
+                        fc0[d] = fZ[d].x;
+                        fc1[d] = fZ[d].y;
                     }
                     // AC / ZC: 1/0 = chi_d (v_d) active / Z_d nonzero known at
                     // compile time (ND == 1, hoisted), 2 = test the masks per d
