@@ -237,16 +237,16 @@ __device__ __forceinline__ unsigned ins0u(unsigned t, int b)
 
 // XOR swizzle of the tile index (double2 granularity): l ^ f(l >> 3), f a
 // GF(2)-linear map onto the 16-byte slot within the 128-byte bank row.  Bit
-// i >= 3 of l moves the slot by v_i = {7,5,6,4,6,4,6,2,3}[i-3], chosen by
+// i >= 3 of l moves the slot by v_i = {7,5,2,7,4,6,4,3,6}[i-3], chosen by
 // tools/swizzle_search.py so that the quarter-warp of a gate access (tuples
 // t, t+1 x amplitudes {0, lo, hi, lo+hi}) and the half-warp of a hole access
 // (tuples 4q..4q+3 x {0, lo}) hit distinct slots for the target pairs the
-// pass planner emits (modelled excess wavefronts at c2: 28% -> 4% of ideal;
+// pass planner emits (modelled excess wavefronts at c2: 28% -> 3% of ideal;
 // the earlier fold (l>>3)^(l>>5)^(l>>7)^(l>>9) mapped bits 4, 6, 8, 10 alike).
 __device__ __forceinline__ unsigned swz(unsigned l)
 {
     const unsigned x = l >> 3;
-    return l ^ ((__popc(x & 0x103u) & 1u) | ((__popc(x & 0x1D5u) & 1u) << 1) | ((__popc(x & 0x7Fu) & 1u) << 2));
+    return l ^ ((__popc(x & 0x8Bu) & 1u) | ((__popc(x & 0x1ADu) & 1u) << 1) | ((__popc(x & 0x17Bu) & 1u) << 2));
 }
 
 // B fragment (two k-steps) of the real 8x8 form of a complex 4x4 gate for
@@ -1310,8 +1310,8 @@ static unsigned ins0u_host(unsigned t, int b) { return ((t >> b) << (b + 1)) | (
 static unsigned swz_host(unsigned l)
 {
     const unsigned x = l >> 3;
-    return l ^ ((__builtin_popcount(x & 0x103u) & 1u) | ((__builtin_popcount(x & 0x1D5u) & 1u) << 1) |
-                ((__builtin_popcount(x & 0x7Fu) & 1u) << 2));
+    return l ^ ((__builtin_popcount(x & 0x8Bu) & 1u) | ((__builtin_popcount(x & 0x1ADu) & 1u) << 1) |
+                ((__builtin_popcount(x & 0x17Bu) & 1u) << 2));
 }
 
 struct PassChoice {
