@@ -319,13 +319,38 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
         for (int d = 0; d < ND; ++d) cH0[d] = cH1[d] = 0.0;
         if ((unsigned)warp < nwa) {
             const unsigned wbase = warp * TW;
+            // GF(2)-linear unit addressing from the planner's columns:
+            // A(x) = XOR of col[i] over the bits of the unit index x (tuple for
+            // 2q slots, pair for c1q slots), split as A(wbase) ^ A(lane) ^ A(32k)
+            const PassSlot &PS = p.ps[si];
+            const int twb = 31 - __clz(TW);
+            unsigned Fw = 0;
+#pragma unroll
+            for (int i = 0; i < NWB; ++i)
+                if ((warp >> i) & 1) Fw ^= PS.col[twb + i];
+            auto Alane = [&]() {
+                unsigned a = 0;
+#pragma unroll
+                for (int i = 0; i < 5; ++i)
+                    if ((lane >> i) & 1) a ^= PS.col[i];
+                return a;
+            };
+            auto Ahi = [&](unsigned k) {  // A(32 k)
+                unsigned a = 0;
+#pragma unroll
+                for (int i = 0; i < FMAXM - 6; ++i)
+                    if ((k >> i) & 1u) a ^= PS.col[5 + i];
+                return a;
+            };
             if (c1q) {
                 // ---- parity-controlled 1q slot (sector implicit qubit): FMA on pairs
+                // (the parity of the pair index equals that of its low member:
+                // inserting a zero bit keeps the popcount)
                 double2 *V = (OP == OP_ASC_H) ? t1 : t0;
+                const unsigned Fl = Fw ^ Alane();
                 for (unsigned j = lane; j < TW; j += 32) {
-                    const unsigned l0r = ins0u(wbase + j, llo);
-                    const int P = (tpop + __popc(l0r)) & 1 ^ p.sector;
-                    const unsigned s0 = swz(l0r), s1 = swz(l0r | olo);
+                    const int P = (tpop + __popc(wbase + j)) & 1 ^ p.sector;
+                    const unsigned s0 = Fl ^ Ahi(j >> 5), s1 = s0 ^ PS.so;
                     double2 x[2] = {V[s0], V[s1]}, y[2];
                     mv2(MA, P, x, y);
                     V[s0] = y[0];
@@ -336,12 +361,17 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                     const double *d0 = reinterpret_cast<const double *>(t0);
                     const double *d1 = reinterpret_cast<const double *>(t1);
                     const double *d2 = reinterpret_cast<const double *>(t2);
+                    const unsigned Ft = Fw ^ ((tq & 1) ? PS.col[0] : 0u) ^ ((tq & 2) ? PS.col[1] : 0u);
                     for (unsigned q = 0; q < TW / 4; ++q) {
-                        const unsigned l0 = ins0u(wbase + 4 * q + tq, llo);
-                        const int P = (tpop + __popc(l0)) & 1 ^ p.sector;
+                        unsigned s0 = Ft;
+#pragma unroll
+                        for (int i = 0; i < FMAXM - 3; ++i)
+                            if ((q >> i) & 1u) s0 ^= PS.col[2 + i];
+                        const int P = (tpop + __popc(wbase + 4 * q + tq)) & 1 ^ p.sector;
                         const int i0 = P ? 1 : 0, i1 = P ? 2 : 3;
-                        const int li = (gi == i0) ? (int)l0 : ((gi == i1) ? (int)(l0 | olo) : -1);
-                        const int o = li >= 0 ? 2 * (int)swz((unsigned)li) + gpart : 0;
+                        const bool on = (gi == i0) || (gi == i1);
+                        const int o = on ? 2 * (int)((gi == i0) ? s0 : (s0 ^ PS.so)) + gpart : 0;
+                        const int li = on ? 0 : -1;
                         if constexpr (REV) {
                             const double k = li >= 0 ? d0[o] : 0.0;
                             dmma(cD0, cD1, li >= 0 ? d1[o] : 0.0, k);
@@ -360,9 +390,10 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                     __syncwarp();
                 }
                 if constexpr (OP != OP_FWD && OP != OP_FWD_DOT) {
+                    const unsigned Fl = Fw ^ Alane();
                     for (unsigned j = lane; j < TW; j += 32) {
-                        const unsigned l0r = ins0u(wbase + j, llo), l0 = swz(l0r), l1 = swz(l0r | olo);
-                        const int P = (tpop + __popc(l0r)) & 1 ^ p.sector;
+                        const unsigned l0 = Fl ^ Ahi(j >> 5), l1 = l0 ^ PS.so;
+                        const int P = (tpop + __popc(wbase + j)) & 1 ^ p.sector;
                         if constexpr (REV) {
                             double2 b[2] = {t1[l0], t1[l1]}, bn[2];
                             if constexpr (OP == OP_REV_GH) {
@@ -404,14 +435,8 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                 // ---- two-qubit slot, all FP64 math on the tensor cores (DMMA m8n8k4).
                 // Tuple -> swizzled tile index is GF(2)-linear (bit insertion +
                 // XOR swizzle), so every address is an XOR of precomputed columns.
-                const PassSlot &PS = p.ps[si];
                 // F(x) = swz(ins0u(ins0u(x, llo), lhi)) is GF(2)-linear in the
                 // tuple index x: F(wbase | t) = F(wbase) ^ F(t) for t < TW
-                const int twb = 31 - __clz(TW);
-                unsigned Fw = 0;
-#pragma unroll
-                for (int i = 0; i < NWB; ++i)
-                    if ((warp >> i) & 1) Fw ^= PS.col[twb + i];
                 const unsigned c0 = PS.col[0], c1 = PS.col[1], c2 = PS.col[2];
                 const unsigned offA = ((tq & 2) ? PS.sh : 0u) ^ ((tq & 1) ? PS.so : 0u);
                 // gate layout: lane (g, tq) = amp tq of tuple g
@@ -452,9 +477,10 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                 if (sparse) {
                     // parity-conserving gates: half of G is structural zeros, so the
                     // sparse FMA form does half the flops of the dense DMMA form
+                    const unsigned Fl = Fw ^ Alane();
                     for (unsigned j = lane; j < TW; j += 32) {
-                        const unsigned b0 = ins0u(ins0u(wbase + j, llo), lhi);
-                        const unsigned L[4] = {swz(b0), swz(b0 + olo), swz(b0 + ohi), swz(b0 + olo + ohi)};
+                        const unsigned b0 = Fl ^ Ahi(j >> 5);
+                        const unsigned L[4] = {b0, b0 ^ PS.so, b0 ^ PS.sh, b0 ^ PS.so ^ PS.sh};
                         double2 x[4], y[4];
 #pragma unroll
                         for (int i = 0; i < 4; ++i) x[i] = V[L[i]];
@@ -549,9 +575,10 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                     __syncwarp();
                 }
                 if constexpr (OP != OP_FWD && OP != OP_FWD_DOT) if (sparse) {
+                    const unsigned Fl = Fw ^ Alane();
                     for (unsigned j = lane; j < TW; j += 32) {
-                        const unsigned b0 = ins0u(ins0u(wbase + j, llo), lhi);
-                        const unsigned L[4] = {swz(b0), swz(b0 + olo), swz(b0 + ohi), swz(b0 + olo + ohi)};
+                        const unsigned b0 = Fl ^ Ahi(j >> 5);
+                        const unsigned L[4] = {b0, b0 ^ PS.so, b0 ^ PS.sh, b0 ^ PS.so ^ PS.sh};
                         if constexpr (REV) {
                             double2 bb[4], bn[4];
 #pragma unroll
@@ -1512,10 +1539,14 @@ static std::vector<FusedParams> plan_passes(const gf_plan *p, bool reverse)
             ps.llo = lidx[si.lo];
             ps.lhi = si.mode_c1q ? 0 : lidx[si.hi];
             if (!si.mode_c1q) {
-                for (int i = 0; i < FMAXM - 2; ++i)
+                for (int i = 0; i < FMAXM - 1; ++i)
                     ps.col[i] = swz_host(ins0u_host(ins0u_host(1u << i, ps.llo), ps.lhi));
                 ps.so = swz_host(1u << ps.llo);
                 ps.sh = swz_host(1u << ps.lhi);
+            } else {  // pair index -> swizzled tile index of the pair's low member
+                for (int i = 0; i < FMAXM - 1; ++i) ps.col[i] = swz_host(ins0u_host(1u << i, ps.llo));
+                ps.so = swz_host(1u << ps.llo);
+                ps.sh = 0;
             }
             fp.ps[t] = ps;
         }

@@ -39,9 +39,10 @@ struct PassSlot {
     int amask; // bit d: chi_d / v_d is nonzero entering this slot (else its hole and update are skipped)
     int fa, fb, fz;  // fragment-table rows of mat[0], mat[1], mat[2 + d] (fz + d)
     // 2q slots: col[i] = swz(tuple index 2^i with zeros inserted at llo, lhi),
-    // so = swz(2^llo), sh = swz(2^lhi) -- the GF(2)-linear tile addressing,
-    // precomputed on the host instead of per slot and lane in the kernel
-    unsigned col[FMAXM - 2];
+    // so = swz(2^llo), sh = swz(2^lhi); c1q slots: col[i] = swz(pair index 2^i
+    // with a zero inserted at llo), so = swz(2^llo) -- the GF(2)-linear tile
+    // addressing, precomputed on the host instead of per slot and lane
+    unsigned col[FMAXM - 1];
     unsigned so, sh;
 };
 
