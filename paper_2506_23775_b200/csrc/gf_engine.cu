@@ -1146,7 +1146,7 @@ static void plan_free(gf_plan *p)
         if (q) cudaFree(q);
 }
 
-static std::vector<FusedParams> plan_passes(const gf_plan *p, bool reverse);
+static std::vector<FusedParams> plan_passes(const gf_plan *p, bool reverse, int m);
 
 extern "C" int gf_plan_create(gf_plan **out, int k, int sector, int n_slots, const int32_t *t1, const int32_t *t2,
                               const int32_t *logical, int n_logical, int64_t max_batch, int chunk_states)
@@ -1206,8 +1206,12 @@ extern "C" int gf_plan_create(gf_plan **out, int k, int sector, int n_slots, con
         p->fm = std::max(5, std::min(std::min(fm, FMAXM), p->K));
         p->fc = std::min(3, p->fm);  // 2^3-amplitude (128 B) contiguous runs: full DRAM lines, more planner freedom
         if (p->fused) {
-            p->fwd_passes = plan_passes(p, false);
-            p->rev_passes = plan_passes(p, true);
+            // the forward sweep stages one vector per tile: GF_FWD_M may give it
+            // larger tiles (fewer passes) than the three-vector sweeps
+            const char *fwenv = getenv("GF_FWD_M");
+            const int fwm = fwenv ? std::max(p->fc, std::min(std::min(atoi(fwenv), FMAXM), p->K)) : p->fm;
+            p->fwd_passes = plan_passes(p, false, fwm);
+            p->rev_passes = plan_passes(p, true, p->fm);
             p->asc_passes.assign(p->rev_passes.rbegin(), p->rev_passes.rend());
             for (auto &f : p->asc_passes) std::reverse(f.ps, f.ps + f.nslots);
             if (getenv("GF_DUMP_PLAN")) {  // diagnostic: per-pass local bits and slot targets
@@ -1469,10 +1473,10 @@ static bool plan_exact(const gf_plan *p, const std::vector<int> &order, int m, i
     return false;
 }
 
-static std::vector<FusedParams> plan_passes(const gf_plan *p, bool reverse)
+static std::vector<FusedParams> plan_passes(const gf_plan *p, bool reverse, int m)
 {
     std::vector<FusedParams> out;
-    const int n = p->n, K = p->K, m = p->fm, c = p->fc;
+    const int n = p->n, K = p->K, c = p->fc;
     std::vector<PassChoice> choice;
     {
     std::vector<int> remaining;
