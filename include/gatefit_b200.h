@@ -157,6 +157,15 @@ int gf_plan_phase_times(gf_plan *plan, double *ms4, int64_t *launches4);
  * of fused passes per forward / reverse sweep, CTAs per summand. */
 int gf_plan_describe(const gf_plan *plan, int *fused, int *tile_bits, int *n_fwd_passes, int *n_rev_passes,
                      int *ctas);
+
+/* Host-only query of the fused pass plan (no device work): the passes the
+ * engine would run for slots (t1[s], t2[s]) on k qubits (sector -1/0/1) with
+ * 2^tile_bits-amplitude tiles; sweep 0 = forward, 1 = reverse.  Writes the
+ * pass count, the slots per pass, the slots in execution order and each
+ * pass's local bit set.  New (the reference runs one slot at a time,
+ * objective.py:255-280); used by the planner tests. */
+int gf_plan_layout(int k, int sector, int n_slots, const int32_t *t1, const int32_t *t2, int tile_bits, int sweep,
+                   int max_passes, int *n_passes, int *pass_sizes, int *slot_order, unsigned long long *pass_bits);
 int gf_plan_destroy(gf_plan *plan);
 
 /* ------------------------------------------------------------------ *

@@ -39,6 +39,7 @@ EXPORTS = (
     "gf_plan_set_profiling",
     "gf_plan_phase_times",
     "gf_plan_describe",
+    "gf_plan_layout",
     "gf_plan_destroy",
     "gf_cheb_step",
     "gf_hamiltonian_apply",
@@ -89,6 +90,7 @@ for _name, _args in {
     "gf_plan_slot_outputs": [_vp, _i64, _vp, _vp, _vp],
     "gf_plan_destroy": [_vp],
     "gf_plan_describe": [_vp, _vp, _vp, _vp, _vp, _vp],
+    "gf_plan_layout": [_i, _i, _i, _vp, _vp, _i, _i, _i, _vp, _vp, _vp, _vp],
     "gf_plan_set_profiling": [_vp, _i],
     "gf_plan_phase_times": [_vp, _vp, _vp],
     "gf_cheb_step": [_vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _i, ctypes.c_double, ctypes.c_double,

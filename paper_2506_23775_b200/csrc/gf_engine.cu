@@ -1148,6 +1148,35 @@ static void plan_free(gf_plan *p)
 
 static std::vector<FusedParams> plan_passes(const gf_plan *p, bool reverse, int m);
 
+// slot geometry (physical bit positions; qubit 0 = MSB) shared by plan
+// creation and the host-only layout query
+static int build_slots(gf_plan *p, int k, int sector, int n_slots, const int32_t *t1, const int32_t *t2,
+                       const int32_t *logical, int n_logical)
+{
+    for (int s = 0; s < n_slots; ++s) {
+        int a = t1[s], b = t2[s];
+        if (a == b || a < 0 || b < 0 || a >= k || b >= k)
+            return gf_fail(GF_EINVAL, "invalid slot targets (%d, %d) for %d qubits", a, b, k);
+        if (logical && (logical[s] < 0 || logical[s] >= n_logical))
+            return gf_fail(GF_EINVAL, "slot references unknown logical gate %d", logical[s]);
+        SlotInfo si;
+        si.swapped = a > b;
+        si.q1 = std::min(a, b);
+        si.q2 = std::max(a, b);
+        si.logical = logical ? logical[s] : 0;
+        si.mode_c1q = (sector >= 0 && si.q2 == k - 1);
+        if (si.mode_c1q) {
+            si.lo = p->K - 1 - si.q1;  // compressed position of qubit q1
+            si.hi = -1;
+        } else {
+            si.lo = p->K - 1 - si.q2;
+            si.hi = p->K - 1 - si.q1;
+        }
+        p->slots.push_back(si);
+    }
+    return GF_OK;
+}
+
 extern "C" int gf_plan_create(gf_plan **out, int k, int sector, int n_slots, const int32_t *t1, const int32_t *t2,
                               const int32_t *logical, int n_logical, int64_t max_batch, int chunk_states)
 {
@@ -1170,30 +1199,9 @@ extern "C" int gf_plan_create(gf_plan **out, int k, int sector, int n_slots, con
         delete p;
         return gf_fail(GF_EINVAL, "state space too small");
     }
-    for (int s = 0; s < n_slots; ++s) {
-        int a = t1[s], b = t2[s];
-        if (a == b || a < 0 || b < 0 || a >= k || b >= k) {
-            delete p;
-            return gf_fail(GF_EINVAL, "invalid slot targets (%d, %d) for %d qubits", a, b, k);
-        }
-        if (logical[s] < 0 || logical[s] >= n_logical) {
-            delete p;
-            return gf_fail(GF_EINVAL, "slot references unknown logical gate %d", logical[s]);
-        }
-        SlotInfo si;
-        si.swapped = a > b;
-        si.q1 = std::min(a, b);
-        si.q2 = std::max(a, b);
-        si.logical = logical[s];
-        si.mode_c1q = (sector >= 0 && si.q2 == k - 1);
-        if (si.mode_c1q) {
-            si.lo = p->K - 1 - si.q1;  // compressed position of qubit q1
-            si.hi = -1;
-        } else {
-            si.lo = p->K - 1 - si.q2;
-            si.hi = p->K - 1 - si.q1;
-        }
-        p->slots.push_back(si);
+    if (int rc = build_slots(p, k, sector, n_slots, t1, t2, logical, n_logical)) {
+        delete p;
+        return rc;
     }
     u64 units = p->N / 4;
     int64_t ctas = (int64_t)(units / (kThreads * 4));
@@ -1999,6 +2007,41 @@ extern "C" int gf_plan_destroy(gf_plan *p)
     if (!p) return GF_OK;
     plan_free(p);
     delete p;
+    return GF_OK;
+}
+
+// Host-only: the fused pass plan the engine would use for this circuit
+// (no device work).  sweep 0 = forward, 1 = reverse (the ascending sweep
+// replays the reverse plan backwards).  pass_sizes[i] = slots in pass i,
+// slot_order = the slots in execution order, pass_bits[i] = the pass's local
+// bit set (physical positions).
+extern "C" int gf_plan_layout(int k, int sector, int n_slots, const int32_t *t1, const int32_t *t2, int tile_bits,
+                              int sweep, int max_passes, int *n_passes, int *pass_sizes, int *slot_order,
+                              unsigned long long *pass_bits)
+{
+    if (!n_passes || !pass_sizes || !slot_order || !pass_bits || max_passes < 1)
+        return gf_fail(GF_EINVAL, "null output or no room for passes");
+    if (k < 2 || k > 34 || sector < -1 || sector > 1 || n_slots < 1)
+        return gf_fail(GF_EINVAL, "bad layout query sizes");
+    gf_plan tmp;
+    tmp.k = k;
+    tmp.sector = sector;
+    tmp.K = sector >= 0 ? k - 1 : k;
+    tmp.n = n_slots;
+    if (int rc = build_slots(&tmp, k, sector, n_slots, t1, t2, nullptr, 0)) return rc;
+    tmp.fm = std::max(5, std::min(std::min(tile_bits, FMAXM), tmp.K));
+    tmp.fc = std::min(3, tmp.fm);
+    std::vector<FusedParams> passes = plan_passes(&tmp, sweep != 0, tmp.fm);
+    if ((int)passes.size() > max_passes) return gf_fail(GF_EINVAL, "%zu passes exceed the output room", passes.size());
+    *n_passes = (int)passes.size();
+    int o = 0;
+    for (size_t i = 0; i < passes.size(); ++i) {
+        pass_sizes[i] = passes[i].nslots;
+        unsigned long long bits = 0;
+        for (int b = 0; b < passes[i].m; ++b) bits |= 1ull << passes[i].lpos[b];
+        pass_bits[i] = bits;
+        for (int t = 0; t < passes[i].nslots; ++t) slot_order[o++] = passes[i].ps[t].slot;
+    }
     return GF_OK;
 }
 
