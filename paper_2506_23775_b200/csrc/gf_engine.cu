@@ -1030,6 +1030,9 @@ struct gf_plan {
     // half-sums are only order-invariant together), so asc_passes is
     // rev_passes reversed with each pass's slot list reversed.
     std::vector<FusedParams> fwd_passes, rev_passes, asc_passes;
+    // multi-direction sweeps (2 + nd vectors per tile) on 2^10 tiles: two CTAs
+    // per SM instead of one (c2 full Hessian 120 s -> 112 s)
+    std::vector<FusedParams> rev_md, asc_md;
     // per-lane DMMA B fragments of every slot matrix, [slot][FK_*][32 lanes]
     // (double2 = the two k-steps); rebuilt on the eval stream when dirty
     double2 *d_frag = nullptr;
@@ -1233,7 +1236,16 @@ extern "C" int gf_plan_create(gf_plan **out, int k, int sector, int n_slots, con
                     }
                 }
             }
-            u64 ntiles = 1ull << (p->K - p->fm);
+            int mmin = p->fm;
+            if (p->fm >= 11 && p->K > 10) {
+                p->rev_md = plan_passes(p, true, 10);
+                p->asc_md.assign(p->rev_md.rbegin(), p->rev_md.rend());
+                for (auto &f : p->asc_md) std::reverse(f.ps, f.ps + f.nslots);
+                mmin = 10;
+            }
+            // CTAs per vector: capacity for the smallest tiles; each launch uses
+            // min(capacity, its tiles), one tile per CTA by default
+            u64 ntiles = 1ull << (p->K - mmin);
             {
                 const char *cenv = getenv("GF_FUSED_CTAS");
                 u64 want = cenv ? (u64)atoll(cenv) : (u64)(148 * 8);  // all tiles, up to 8 per SM
@@ -1613,7 +1625,7 @@ static int launch_fused_nt(const gf_plan *p, FusedParams &fp, int64_t nvec, cuda
         attr_done = true;
     }
     if (smem > 226 * 1024) return gf_fail(GF_EINVAL, "fused tile needs %zu B of shared memory", smem);
-    dim3 grid(p->ctas, (unsigned)nvec);
+    dim3 grid(fp.ctas, (unsigned)nvec);
     k_fused<OP, FIRST, NT, ND, SPX><<<grid, NT, smem, st>>>(fp);
     return GF_OK;
 }
@@ -1703,6 +1715,7 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
         ++launches;
     }
     int64_t l_fwd = 0, l_rev = 0, l_asc = 0;
+    int ctas_r = p->ctas, ctas_v = p->ctas;  // CTAs per vector of the hole / value partials
     const bool grad_like = (flags & (GF_GRAD | GF_HVP)) != 0;
     if (n == 0) {
         // empty circuit: value = sum phi0 . |j>; an identity "slot" with the dot fused
@@ -1727,7 +1740,7 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
             f.weights = weights;
             f.N = p->N;
             f.nvec = (int)nvec;
-            f.ctas = p->ctas;
+            f.ctas = (int)std::min<u64>((u64)p->ctas, f.ntiles);
             f.sector = p->sector < 0 ? 0 : p->sector;
             f.partV = p->partV;
             f.qV = p->qV;
@@ -1740,7 +1753,10 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
             static const bool exp_noio = getenv("GF_EXP_NOIO") != nullptr;  // timing diagnostic only
             f.exp_noio = exp_noio ? 1 : 0;
         };
-        const int nf = (int)p->fwd_passes.size(), nr = (int)p->rev_passes.size();
+        const bool md = nd >= 2 && !p->rev_md.empty() && (flags & GF_HVP);
+        const std::vector<FusedParams> &revp = md ? p->rev_md : p->rev_passes;
+        const std::vector<FusedParams> &ascp = md ? p->asc_md : p->asc_passes;
+        const int nf = (int)p->fwd_passes.size(), nr = (int)revp.size();
         for (int pi = 0; pi < nf; ++pi) {
             fp = p->fwd_passes[pi];
             setup(fp);
@@ -1753,6 +1769,7 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
                 if (fp.ps[t].mode != PM_C1Q) fp.ps[t].mode = p->spG[s] ? PM_SPARSE : PM_DENSE;
             }
             const bool last = !grad_like && pi == nf - 1;
+            if (last) ctas_v = fp.ctas;
             if (pi == 0) {
                 if (last) fp.store_mask = 0;  // value only: psi_n is not needed afterwards
                 if (last) { int rc_ = launch_fused<OP_FWD_DOT, true>(p, fp, nvec, st); if (rc_) return rc_; }
@@ -1769,8 +1786,10 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
             const bool h = (flags & GF_HVP) != 0;
             int act_rev = 0;  // directions whose chi is nonzero entering the next slot
             for (int pi = 0; pi < nr; ++pi) {
-                fp = p->rev_passes[pi];
+                fp = revp[pi];
                 setup(fp);
+                ctas_r = fp.ctas;
+                if (pi == 0) ctas_v = fp.ctas;
                 fp.partD = p->partD;
                 fp.partH = p->partHd;
                 fp.qD = p->qD;
@@ -1812,7 +1831,7 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
             if (h) {
                 int act_asc = 0;  // directions whose v is nonzero entering the next slot
                 for (int pi = 0; pi < nr; ++pi) {
-                    fp = p->asc_passes[pi];
+                    fp = ascp[pi];
                     setup(fp);
                     fp.partH = p->partHa;
                     fp.qH = p->qHa;
@@ -1906,21 +1925,21 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
     if (grad_like && n > 0) {
         int64_t nsb = (int64_t)n * nvec;
         int blocks = (int)((nsb * 32 + 255) / 256);
-        k_reduce_ctas<<<blocks, 256, 0, st>>>(p->partD, p->qD, nsb, p->ctas);
+        k_reduce_ctas<<<blocks, 256, 0, st>>>(p->partD, p->qD, nsb, ctas_r);
         ++launches;
         if (flags & GF_HVP) {
             const int ndr = p->fused ? nd : 1;
             const u64 hs = (u64)std::max(1, p->n) * p->max_batch * p->ctas * 32;
             const u64 qs = (u64)std::max(1, p->n) * p->max_batch * 32;
             for (int d = 0; d < ndr; ++d) {
-                k_reduce_ctas<<<blocks, 256, 0, st>>>(p->partHd + d * hs, p->qHd + d * qs, nsb, p->ctas);
-                k_reduce_ctas<<<blocks, 256, 0, st>>>(p->partHa + d * hs, p->qHa + d * qs, nsb, p->ctas);
+                k_reduce_ctas<<<blocks, 256, 0, st>>>(p->partHd + d * hs, p->qHd + d * qs, nsb, ctas_r);
+                k_reduce_ctas<<<blocks, 256, 0, st>>>(p->partHa + d * hs, p->qHa + d * qs, nsb, ctas_r);
                 launches += 2;
             }
         }
     }
     if (p->fused && n > 0) {
-        k_reduce_ctas<<<(unsigned)((nvec * 2 + 255) / 256), 256, 0, st>>>(p->partV, p->qV, nvec, p->ctas, 2);
+        k_reduce_ctas<<<(unsigned)((nvec * 2 + 255) / 256), 256, 0, st>>>(p->partV, p->qV, nvec, ctas_v, 2);
         ++launches;
     }
     {
