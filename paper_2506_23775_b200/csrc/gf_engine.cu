@@ -307,7 +307,6 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
     const int gi = g >> 1, gpart = g & 1;
     for (int si = 0; si < p.nslots; ++si) {
         const int mode = p.ps[si].mode;
-        const int llo = p.ps[si].llo, lhi = p.ps[si].lhi;
         const int zmask = p.ps[si].zmask, amask = p.ps[si].amask;
         const Mat4 &MA = p.mat[si][0];
         const Mat4 &MB = p.mat[si][1];
@@ -317,7 +316,6 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
         // 2q tensor path (8-tuple groups, paired hole MMAs)
         const unsigned TW = max(nunit / (unsigned)NW, c1q ? 4u : 8u);
         const unsigned nwa = nunit >> (31 - __clz(TW));  // powers of two
-        const unsigned olo = 1u << llo, ohi = 1u << lhi;
         double cD0 = 0.0, cD1 = 0.0, cH0[ND], cH1[ND];
 #pragma unroll
         for (int d = 0; d < ND; ++d) cH0[d] = cH1[d] = 0.0;
@@ -755,8 +753,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_fused(const FusedParams p)
     constexpr int NH = 1 + ND;   // hole slots: gradient + ND directions
     constexpr int NV = (OP == OP_FWD || OP == OP_FWD_DOT) ? 1 : (OP == OP_REV_G ? 2 : 2 + ND);
     constexpr bool HD = (OP == OP_REV_G || OP == OP_REV_GH);
-    constexpr bool HH = (OP == OP_REV_GH || OP == OP_ASC_H);
-    constexpr bool HV = (OP == OP_FWD_DOT) || (HD && FIRST);
+        constexpr bool HV = (OP == OP_FWD_DOT) || (HD && FIRST);
     constexpr bool REV = (OP == OP_REV_G || OP == OP_REV_GH);
     extern __shared__ __align__(16) unsigned char fsm[];
     const int m = p.m, c = p.c;
