@@ -34,7 +34,8 @@
 
 namespace gf {
 
-enum { OP_FWD = 0, OP_FWD_DOT = 1, OP_REV_G = 2, OP_REV_GH = 3, OP_ASC_H = 4 };
+// OP_REV_H: the reverse sweep of an HVP-only evaluation (no gradient hole)
+enum { OP_FWD = 0, OP_FWD_DOT = 1, OP_REV_G = 2, OP_REV_GH = 3, OP_ASC_H = 4, OP_REV_H = 5 };
 enum { MODE_DENSE = 0, MODE_SPARSE = 1, MODE_C1Q = 2 };
 
 struct SweepParams {
@@ -298,8 +299,9 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
     constexpr int NW = NT / 32;
     constexpr int NWB = NW >= 16 ? 4 : (NW >= 8 ? 3 : (NW >= 4 ? 2 : (NW >= 2 ? 1 : 0)));  // log2(NW)
     constexpr bool HD = (OP == OP_REV_G || OP == OP_REV_GH);
-    constexpr bool HH = (OP == OP_REV_GH || OP == OP_ASC_H);
-    constexpr bool REV = (OP == OP_REV_G || OP == OP_REV_GH);
+    constexpr bool HH = (OP == OP_REV_GH || OP == OP_REV_H || OP == OP_ASC_H);
+    constexpr bool REV = (OP == OP_REV_G || OP == OP_REV_GH || OP == OP_REV_H);
+    constexpr bool CHI = (OP == OP_REV_GH || OP == OP_REV_H);  // reverse sweep carrying chi_d
     constexpr int NH = 1 + ND;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, tq = lane & 3;
@@ -376,7 +378,7 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                         const int li = on ? 0 : -1;
                         if constexpr (REV) {
                             const double k = li >= 0 ? d0[o] : 0.0;
-                            dmma(cD0, cD1, li >= 0 ? d1[o] : 0.0, k);
+                            if constexpr (HD) dmma(cD0, cD1, li >= 0 ? d1[o] : 0.0, k);
                             if constexpr (HH) {
 #pragma unroll
                                 for (int d = 0; d < ND; ++d)
@@ -398,7 +400,7 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                         const int P = (tpop + __popc(wbase + j)) & 1 ^ p.sector;
                         if constexpr (REV) {
                             double2 b[2] = {t1[l0], t1[l1]}, bn[2];
-                            if constexpr (OP == OP_REV_GH) {
+                            if constexpr (CHI) {
 #pragma unroll
                                 for (int d = 0; d < ND; ++d) {
                                     const bool act = (amask >> d) & 1, zz = (zmask >> d) & 1;
@@ -471,7 +473,7 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                 for (int d = 0; d < ND; ++d) fZ[d] = make_double2(0.0, 0.0);
                 if (!sparse) {
                     if constexpr (OP != OP_FWD && OP != OP_FWD_DOT) fB = __ldg(&p.frag[PS.fb * 32 + lane]);
-                    if constexpr (OP == OP_REV_GH || OP == OP_ASC_H) {
+                    if constexpr (CHI || OP == OP_ASC_H) {
 #pragma unroll
                         for (int d = 0; d < ND; ++d) fZ[d] = __ldg(&p.frag[(PS.fz + d) * 32 + lane]);
                     }
@@ -561,8 +563,10 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                             const unsigned o0 = 2 * a0, o1 = 2 * a1;
                             if constexpr (REV) {
                                 const double k0 = d0[o0], k1 = d0[o1];
-                                dmma(cD0, cD1, d1[o0], k0);
-                                dmma(eD0, eD1, d1[o1], k1);
+                                if constexpr (HD) {
+                                    dmma(cD0, cD1, d1[o0], k0);
+                                    dmma(eD0, eD1, d1[o1], k1);
+                                }
                                 if constexpr (HH) {
 #pragma unroll
                                     for (int d = 0; d < ND; ++d) {
@@ -607,7 +611,7 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                             double2 bb[4], bn[4];
 #pragma unroll
                             for (int i = 0; i < 4; ++i) bb[i] = t1[L[i]];
-                            if constexpr (OP == OP_REV_GH) {
+                            if constexpr (CHI) {
 #pragma unroll
                                 for (int d = 0; d < ND; ++d) {
                                     const bool act = (amask >> d) & 1, zz = (zmask >> d) & 1;
@@ -672,7 +676,7 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                             if (gb + u >= ngrp) break;  // ngrp < 8 only for tiny tiles
                             const unsigned ad = ab ^ gcomb(u);
                             const double2 x = REV ? t1[ad] : t0[ad];
-                            if constexpr (OP == OP_REV_GH || OP == OP_ASC_H) {
+                            if constexpr (CHI || OP == OP_ASC_H) {
 #pragma unroll
                                 for (int d = 0; d < ND; ++d) {
                                     const bool act = A == 2 ? ((amask >> d) & 1) : A;
@@ -688,7 +692,7 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                           }
                         }
                     };
-                    if constexpr (ND == 1 && (OP == OP_REV_GH || OP == OP_ASC_H)) {
+                    if constexpr (ND == 1 && (CHI || OP == OP_ASC_H)) {
                         const bool a = amask & 1, z = zmask & 1;
                         if (a && z) grp_loop(IC<1>{}, IC<1>{});
                         else if (a) grp_loop(IC<1>{}, IC<0>{});
@@ -752,9 +756,9 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_fused(const FusedParams p)
     constexpr int NW = NT / 32;  // warps per CTA
     constexpr int NH = 1 + ND;   // hole slots: gradient + ND directions
     constexpr int NV = (OP == OP_FWD || OP == OP_FWD_DOT) ? 1 : (OP == OP_REV_G ? 2 : 2 + ND);
-    constexpr bool HD = (OP == OP_REV_G || OP == OP_REV_GH);
+    constexpr bool HD = (OP == OP_REV_G || OP == OP_REV_GH || OP == OP_REV_H);  // value on the first reverse pass
         constexpr bool HV = (OP == OP_FWD_DOT) || (HD && FIRST);
-    constexpr bool REV = (OP == OP_REV_G || OP == OP_REV_GH);
+    constexpr bool REV = (OP == OP_REV_G || OP == OP_REV_GH || OP == OP_REV_H);
     extern __shared__ __align__(16) unsigned char fsm[];
     const int m = p.m, c = p.c;
     const unsigned T = 1u << m;
@@ -1633,7 +1637,7 @@ static int launch_fused_nt(const gf_plan *p, FusedParams &fp, int64_t nvec, cuda
 template <int OP, bool FIRST, bool SPX>
 static int launch_fused_sp(const gf_plan *p, FusedParams &fp, int64_t nvec, cudaStream_t st, int nd)
 {
-    if constexpr (OP == OP_REV_GH || OP == OP_ASC_H) {
+    if constexpr (OP == OP_REV_GH || OP == OP_REV_H || OP == OP_ASC_H) {
         if (nd >= 2) {
             if (fp.m <= 10) {  // 2^10 tiles: 2 + ND vectors fit 2 CTAs/SM at 256 threads
                 if (nd == 2) return launch_fused_nt<OP, FIRST, 256, 2, SPX>(p, fp, nvec, st);
@@ -1815,8 +1819,14 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
                 // the last pass writes back only the bra (needed by the ascending sweep)
                 if (pi == nr - 1) fp.store_mask = h ? 2 : 0;
                 if (h) {
-                    if (pi == 0) { int rc_ = launch_fused<OP_REV_GH, true>(p, fp, nvec, st, nd); if (rc_) return rc_; }
-                    else { int rc_ = launch_fused<OP_REV_GH, false>(p, fp, nvec, st, nd); if (rc_) return rc_; }
+                    // HVP-only evaluations skip the gradient hole
+                    const bool g = (flags & GF_GRAD) != 0;
+                    int rc_;
+                    if (pi == 0) rc_ = g ? launch_fused<OP_REV_GH, true>(p, fp, nvec, st, nd)
+                                         : launch_fused<OP_REV_H, true>(p, fp, nvec, st, nd);
+                    else rc_ = g ? launch_fused<OP_REV_GH, false>(p, fp, nvec, st, nd)
+                                 : launch_fused<OP_REV_H, false>(p, fp, nvec, st, nd);
+                    if (rc_) return rc_;
                 } else {
                     if (pi == 0) { int rc_ = launch_fused<OP_REV_G, true>(p, fp, nvec, st); if (rc_) return rc_; }
                     else { int rc_ = launch_fused<OP_REV_G, false>(p, fp, nvec, st); if (rc_) return rc_; }
@@ -1922,8 +1932,10 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
     if (grad_like && n > 0) {
         int64_t nsb = (int64_t)n * nvec;
         int blocks = (int)((nsb * 32 + 255) / 256);
-        k_reduce_ctas<<<blocks, 256, 0, st>>>(p->partD, p->qD, nsb, ctas_r);
-        ++launches;
+        if (flags & GF_GRAD) {  // HVP-only evaluations write no gradient partials
+            k_reduce_ctas<<<blocks, 256, 0, st>>>(p->partD, p->qD, nsb, ctas_r);
+            ++launches;
+        }
         if (flags & GF_HVP) {
             const int ndr = p->fused ? nd : 1;
             const u64 hs = (u64)std::max(1, p->n) * p->max_batch * p->ctas * 32;
