@@ -28,7 +28,12 @@ enum { PM_DENSE = 0, PM_SPARSE = 1, PM_C1Q = 2 };
 
 // rows of the per-slot DMMA fragment table: G, G^dag, G^T, conj G, then Z_d^T
 // and Z_d per direction (row = slot * NFK + kind, 32 lanes per row)
-enum { FK_G = 0, FK_GD = 1, FK_GT = 2, FK_GC = 3, FK_ZT = 4, FK_Z = 4 + FMAXDIR, NFK = 4 + 2 * FMAXDIR };
+// FK_GDA / FK_GCA: G^dag and conj G as the A operand of C = G X (the fused
+// gate + hole formulation of the reverse / ascending passes)
+enum {
+    FK_G = 0, FK_GD = 1, FK_GT = 2, FK_GC = 3, FK_ZT = 4, FK_Z = 4 + FMAXDIR,
+    FK_GDA = 4 + 2 * FMAXDIR, FK_GCA = 5 + 2 * FMAXDIR, NFK = 6 + 2 * FMAXDIR
+};
 
 struct PassSlot {
     int slot;  // circuit slot index (for the partial layout)
@@ -38,6 +43,7 @@ struct PassSlot {
     int zmask; // bit d: direction d has a nonzero Z at this slot (zero Z-terms are skipped)
     int amask; // bit d: chi_d / v_d is nonzero entering this slot (else its hole and update are skipped)
     int fa, fb, fz;  // fragment-table rows of mat[0], mat[1], mat[2 + d] (fz + d)
+    int fa2;         // row of mat[0] in A-operand form (fused gate + hole passes)
     // 2q slots: col[i] = swz(tuple index 2^i with zeros inserted at llo, lhi),
     // so = swz(2^llo), sh = swz(2^lhi); c1q slots: col[i] = swz(pair index 2^i
     // with a zero inserted at llo), so = swz(2^llo) -- the GF(2)-linear tile
