@@ -143,7 +143,9 @@ int gf_plan_set_directions_multi(gf_plan *plan, int nd, const double *zmats);
 int gf_plan_eval(gf_plan *plan, int flags, int64_t nvec, const int64_t *basis_dev, const double *weights_dev,
                  const void *phi0_dev, double *out_dev, void *stream);
 /* Per-slot (normalised orientation) derivative sums of the last eval,
- * [n_slots][16] complex each for D and H (device), for tests. */
+ * [n_slots][16] complex each for D and H (device), for tests.  D is only
+ * defined when the eval requested GF_GRAD (an HVP-only eval skips the
+ * gradient holes, as the reference's _hvp_chunk does), H only with GF_HVP. */
 int gf_plan_slot_outputs(gf_plan *plan, int64_t nvec, double *d_dev, double *h_dev, void *stream);
 /* Number of this library's kernels launched by the last gf_plan_eval. */
 int64_t gf_plan_last_launches(const gf_plan *plan);
