@@ -9,9 +9,20 @@
 // The B200 engine replaces the 2(n+1)-vector pass cache with a reversible
 // 3-vector schedule (SURVEY 7 "hard parts" 2): psi is uncomputed with G^dag,
 // the bra is propagated with G^T on the way down and recovered with conj(G)
-// on the way up.  One kernel launch per slot per sweep streams every vector
-// of the batch once (read + write), fusing the gate applications, the hole
-// contractions and the Z-terms of the HVP.
+// on the way up.
+//
+// Default engine (k_fused): a sweep is a few *passes* planned on the host
+// (plan_passes: exact beam over local-bit sets when affordable).  One launch
+// per pass stages 2^m-amplitude tiles of psi / bra / chi (or v) in shared
+// memory -- one CTA per tile, two CTAs per SM -- and runs all of the pass's
+// slots on them: FP64 tensor-core (DMMA m8n8k4) gate applications and hole
+// contractions, per-slot partials written per CTA and summed in CTA order by
+// k_reduce_ctas.  The streaming engine (k_sweep, one launch per slot) serves
+// tiny state spaces and GF_ENGINE=stream.
+//
+// Compile-time switches (measured defaults): GF_FUSED_GH -- fused gate + hole
+// phase in the ascending passes; GF_FUSED_BLOCK -- its groups per load batch;
+// GF_GATE_BLOCK -- gate groups per load batch in the reverse/ascending passes.
 #include <cuda_runtime.h>
 
 #include <type_traits>
