@@ -179,8 +179,11 @@ def gate_apply_sweep(gf, peak):
     x.imag.normal_()
     rng = np.random.default_rng(0)
     st = gf._lib.stream_ptr()
-    cases = [("adj", t, t + 1) for t in range(K - 1)] + [("long", t, (t + 15) % K) for t in range(0, K, 3)]
-    cases += [("c1q", a, None) for a in (0, 10, 20, 29)]
+    # every target position: adjacent pairs, long-range pairs
+    # like the spinful interaction bonds, and the parity-controlled 1q gate on
+    # each explicit qubit (the sector's 1q path)
+    cases = [("adj", t, t + 1) for t in range(K - 1)] + [("long", t, (t + 15) % K) for t in range(K)]
+    cases += [("c1q", a, None) for a in range(K)]
     results = []
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for kind, a, b in cases:
@@ -224,6 +227,26 @@ def gate_apply_sweep(gf, peak):
         "worst_case": f"{worst[0]} ({worst[1]},{worst[2]}) {worst[4]:.0f} GB/s",
         "per_case_gbs": {f"{r[0]}:{r[1]}-{r[2]}": round(r[4], 1) for r in results},
     }
+
+
+def cpu_gate_apply(k=24):
+    """The CPU port of the reference gate kernel (oracle/gf_oracle.c restating
+    kernels.py:132-205, one thread as numba runs each call) on a 2^k vector:
+    GB/s at 32 B per amplitude for an adjacent, a strided and a long-range
+    target pair (cli.py:424-441 style)."""
+    from oracle import gf_oracle as O
+
+    rng = np.random.default_rng(3)
+    psi = (rng.standard_normal(1 << k) + 1j * rng.standard_normal(1 << k)).astype(np.complex128)
+    g = np.linalg.qr(rng.standard_normal((4, 4)) + 1j * rng.standard_normal((4, 4)))[0]
+    out = {}
+    for a, b in ((k - 2, k - 1), (0, 1), (3, k - 4)):
+        O.apply_gate(psi, g, (a, b))  # warm
+        t0 = time.perf_counter()
+        O.apply_gate(psi, g, (a, b))
+        dt = time.perf_counter() - t0
+        out[f"({a},{b})"] = round(32.0 * (1 << k) / dt / 1e9, 2)
+    return {"vector_amplitudes": 1 << k, "threads": 1, "gbs": out}
 
 
 def cpu_port_rate(circ, X, phi_host, js, workers, with_oracle_terms=None):
@@ -435,7 +458,8 @@ def run_b200(args):
             cpu = {"value": r / TOTAL, "unit": UNIT, "cores": cores, "kind": "port",
                    "sample": f"{sample} random c2 summands, gradient + HVP per summand (oracle/gf_oracle.c, "
                              f"restating reference objective.py:322-337, 432-482) on {cores} threads, phi0 "
-                             f"precomputed; extrapolated to the full 2^16 sum"}
+                             f"precomputed; extrapolated to the full 2^16 sum",
+                   "gate_apply": cpu_gate_apply()}
 
     if rank == 0:
         line = {
