@@ -151,6 +151,59 @@ __global__ void __launch_bounds__(256) k_apply2q(const double2 *__restrict__ in,
     }
 }
 
+__device__ __forceinline__ double2 shfl_xor_d2(double2 v, int m)
+{
+    return make_double2(__shfl_xor_sync(__activemask(), v.x, m), __shfl_xor_sync(__activemask(), v.y, m));
+}
+
+// K1 for a low target on bit 0: the two amplitudes of each pair are 16 B
+// apart, so one thread per tuple would fill only half of every 32 B sector
+// per load instruction.  Lane pairs share a tuple instead: lane h of the pair
+// loads amplitudes (h, 2 + h) -- a full sector per pair per instruction --
+// trades them with its partner through one shuffle, and stores its two
+// outputs.  (Measured: the (29,30) pair of the c5 space ran at 5.3 TB/s
+// against ~6.2 TB/s elsewhere.)
+template <bool SPARSE, int UNROLL>
+__global__ void __launch_bounds__(256) k_apply2q_lo0(const double2 *__restrict__ in, double2 *out, int logN,
+                                                     unsigned long long total, int hi, const Mat4 g)
+{
+    const int logU = logN - 2;
+    const u64 umask = (1ull << logU) - 1ull;
+    const u64 oh = 1ull << hi;
+    const u64 gt = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+    const int h = (int)(gt & 1ull);
+    const u64 stride = ((u64)gridDim.x * blockDim.x) >> 1;
+    for (u64 t0 = gt >> 1; t0 < total; t0 += stride * UNROLL) {
+        double2 a[UNROLL][2];
+        u64 base[UNROLL];
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) {
+            const u64 t = t0 + (u64)u * stride;
+            if (t < total) {
+                const u64 v = t >> logU, r = t & umask;
+                base[u] = ((v << logN) | ins0(ins0(r, 0), hi)) + h;
+                a[u][0] = in[base[u]];
+                a[u][1] = in[base[u] + oh];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) {
+            const u64 t = t0 + (u64)u * stride;
+            if (t < total) {
+                const double2 b0 = shfl_xor_d2(a[u][0], 1), b1 = shfl_xor_d2(a[u][1], 1);
+                double2 x[4], y[4];
+                x[0] = h ? b0 : a[u][0];
+                x[1] = h ? a[u][0] : b0;
+                x[2] = h ? b1 : a[u][1];
+                x[3] = h ? a[u][1] : b1;
+                mv4<SPARSE>(g, x, y);
+                out[base[u]] = h ? y[1] : y[0];
+                out[base[u] + oh] = h ? y[3] : y[2];
+            }
+        }
+    }
+}
+
 // parity-controlled one-qubit gate of the compressed sector space
 template <int UNROLL>
 __global__ void __launch_bounds__(256) k_apply_c1q(const double2 *__restrict__ in, double2 *out, int logN,
@@ -392,7 +445,15 @@ extern "C" int gf_apply_gate(const void *in, void *out, int k, int t1, int t2, c
     unsigned long long total = (1ull << (k - 2)) * (unsigned long long)nvec;
     int grid = grid_for(total, 256 * 2, 148 * 32);
     cudaStream_t st = (cudaStream_t)stream;
-    if (parity_sparse)
+    if (nm.lo == 0 && nm.hi == 1 && k >= 6) {  // measured: helps only the lowest adjacent pair
+        const int grid2 = grid_for(2 * total, 256 * 4, 148 * 32);
+        if (parity_sparse)
+            k_apply2q_lo0<true, 4><<<grid2, 256, 0, st>>>((const double2 *)in, (double2 *)out, log2_exact(k), total,
+                                                          nm.hi, g);
+        else
+            k_apply2q_lo0<false, 4><<<grid2, 256, 0, st>>>((const double2 *)in, (double2 *)out, log2_exact(k), total,
+                                                           nm.hi, g);
+    } else if (parity_sparse)
         k_apply2q<true, 2><<<grid, 256, 0, st>>>((const double2 *)in, (double2 *)out, log2_exact(k), total, nm.lo,
                                                  nm.hi, g);
     else
