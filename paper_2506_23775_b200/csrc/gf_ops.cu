@@ -151,18 +151,21 @@ __global__ void __launch_bounds__(256) k_apply2q(const double2 *__restrict__ in,
     }
 }
 
-__device__ __forceinline__ double2 shfl_xor_d2(double2 v, int m)
+// 256-bit global accesses (LDG/STG.E.ENL2.256 on sm_100a)
+__device__ __forceinline__ void ld256(const double2 *p, double2 &a, double2 &b)
 {
-    return make_double2(__shfl_xor_sync(__activemask(), v.x, m), __shfl_xor_sync(__activemask(), v.y, m));
+    asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a.x), "=d"(a.y), "=d"(b.x), "=d"(b.y) : "l"(p));
+}
+__device__ __forceinline__ void st256(double2 *p, double2 a, double2 b)
+{
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a.x), "d"(a.y), "d"(b.x), "d"(b.y)
+                 : "memory");
 }
 
-// K1 for a low target on bit 0: the two amplitudes of each pair are 16 B
-// apart, so one thread per tuple would fill only half of every 32 B sector
-// per load instruction.  Lane pairs share a tuple instead: lane h of the pair
-// loads amplitudes (h, 2 + h) -- a full sector per pair per instruction --
-// trades them with its partner through one shuffle, and stores its two
-// outputs.  (Measured: the (29,30) pair of the c5 space ran at 5.3 TB/s
-// against ~6.2 TB/s elsewhere.)
+// K1 for a low target on bit 0: the two amplitudes of each pair are adjacent
+// and 32 B aligned, so each thread moves them with one 256-bit access instead
+// of two 128-bit ones that each fill half of every 32 B sector.  (Measured:
+// pairs on bit 0 ran at 5.2-5.7 TB/s against ~6.2 TB/s elsewhere.)
 template <bool SPARSE, int UNROLL>
 __global__ void __launch_bounds__(256) k_apply2q_lo0(const double2 *__restrict__ in, double2 *out, int logN,
                                                      unsigned long long total, int hi, const Mat4 g)
@@ -170,35 +173,62 @@ __global__ void __launch_bounds__(256) k_apply2q_lo0(const double2 *__restrict__
     const int logU = logN - 2;
     const u64 umask = (1ull << logU) - 1ull;
     const u64 oh = 1ull << hi;
-    const u64 gt = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-    const int h = (int)(gt & 1ull);
-    const u64 stride = ((u64)gridDim.x * blockDim.x) >> 1;
-    for (u64 t0 = gt >> 1; t0 < total; t0 += stride * UNROLL) {
-        double2 a[UNROLL][2];
+    const u64 stride = (u64)gridDim.x * blockDim.x;
+    for (u64 t0 = (u64)blockIdx.x * blockDim.x + threadIdx.x; t0 < total; t0 += stride * UNROLL) {
+        double2 x[UNROLL][4];
         u64 base[UNROLL];
 #pragma unroll
         for (int u = 0; u < UNROLL; ++u) {
             const u64 t = t0 + (u64)u * stride;
             if (t < total) {
                 const u64 v = t >> logU, r = t & umask;
-                base[u] = ((v << logN) | ins0(ins0(r, 0), hi)) + h;
-                a[u][0] = in[base[u]];
-                a[u][1] = in[base[u] + oh];
+                base[u] = (v << logN) | ins0(ins0(r, 0), hi);
+                ld256(in + base[u], x[u][0], x[u][1]);
+                ld256(in + base[u] + oh, x[u][2], x[u][3]);
             }
         }
 #pragma unroll
         for (int u = 0; u < UNROLL; ++u) {
             const u64 t = t0 + (u64)u * stride;
             if (t < total) {
-                const double2 b0 = shfl_xor_d2(a[u][0], 1), b1 = shfl_xor_d2(a[u][1], 1);
-                double2 x[4], y[4];
-                x[0] = h ? b0 : a[u][0];
-                x[1] = h ? a[u][0] : b0;
-                x[2] = h ? b1 : a[u][1];
-                x[3] = h ? a[u][1] : b1;
-                mv4<SPARSE>(g, x, y);
-                out[base[u]] = h ? y[1] : y[0];
-                out[base[u] + oh] = h ? y[3] : y[2];
+                double2 y[4];
+                mv4<SPARSE>(g, x[u], y);
+                st256(out + base[u], y[0], y[1]);
+                st256(out + base[u] + oh, y[2], y[3]);
+            }
+        }
+    }
+}
+
+// the parity-controlled 1q gate on bit 0: one 256-bit access per pair
+template <int UNROLL>
+__global__ void __launch_bounds__(256) k_apply_c1q_lo0(const double2 *__restrict__ in, double2 *out, int logN,
+                                                       unsigned long long total, int sector, const Mat4 g)
+{
+    const int logU = logN - 1;
+    const u64 umask = (1ull << logU) - 1ull;
+    const u64 stride = (u64)gridDim.x * blockDim.x;
+    for (u64 t0 = (u64)blockIdx.x * blockDim.x + threadIdx.x; t0 < total; t0 += stride * UNROLL) {
+        double2 x[UNROLL][2];
+        u64 base[UNROLL];
+        int P[UNROLL];
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) {
+            const u64 t = t0 + (u64)u * stride;
+            if (t < total) {
+                const u64 v = t >> logU, r = ins0(t & umask, 0);
+                P[u] = (__popcll(r) & 1) ^ sector;
+                base[u] = (v << logN) | r;
+                ld256(in + base[u], x[u][0], x[u][1]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) {
+            const u64 t = t0 + (u64)u * stride;
+            if (t < total) {
+                double2 y[2];
+                mv2(g, P[u], x[u], y);
+                st256(out + base[u], y[0], y[1]);
             }
         }
     }
@@ -445,14 +475,13 @@ extern "C" int gf_apply_gate(const void *in, void *out, int k, int t1, int t2, c
     unsigned long long total = (1ull << (k - 2)) * (unsigned long long)nvec;
     int grid = grid_for(total, 256 * 2, 148 * 32);
     cudaStream_t st = (cudaStream_t)stream;
-    if (nm.lo == 0 && nm.hi == 1 && k >= 6) {  // measured: helps only the lowest adjacent pair
-        const int grid2 = grid_for(2 * total, 256 * 4, 148 * 32);
+    if (nm.lo == 0) {
         if (parity_sparse)
-            k_apply2q_lo0<true, 4><<<grid2, 256, 0, st>>>((const double2 *)in, (double2 *)out, log2_exact(k), total,
-                                                          nm.hi, g);
+            k_apply2q_lo0<true, 2><<<grid, 256, 0, st>>>((const double2 *)in, (double2 *)out, log2_exact(k), total,
+                                                         nm.hi, g);
         else
-            k_apply2q_lo0<false, 4><<<grid2, 256, 0, st>>>((const double2 *)in, (double2 *)out, log2_exact(k), total,
-                                                           nm.hi, g);
+            k_apply2q_lo0<false, 2><<<grid, 256, 0, st>>>((const double2 *)in, (double2 *)out, log2_exact(k), total,
+                                                          nm.hi, g);
     } else if (parity_sparse)
         k_apply2q<true, 2><<<grid, 256, 0, st>>>((const double2 *)in, (double2 *)out, log2_exact(k), total, nm.lo,
                                                  nm.hi, g);
@@ -478,7 +507,12 @@ extern "C" int gf_apply_gate_sector_c1q(const void *in, void *out, int k_full, i
     int pa = K - 1 - a;
     unsigned long long total = (1ull << (K - 1)) * (unsigned long long)nvec;
     int grid = grid_for(total, 256 * 2, 148 * 32);
-    k_apply_c1q<2><<<grid, 256, 0, (cudaStream_t)stream>>>((const double2 *)in, (double2 *)out, K, total, pa, sector, g);
+    if (pa == 0)
+        k_apply_c1q_lo0<2><<<grid, 256, 0, (cudaStream_t)stream>>>((const double2 *)in, (double2 *)out, K, total,
+                                                                   sector, g);
+    else
+        k_apply_c1q<2><<<grid, 256, 0, (cudaStream_t)stream>>>((const double2 *)in, (double2 *)out, K, total, pa,
+                                                               sector, g);
     GF_CUDA(cudaGetLastError());
     return GF_OK;
 }
