@@ -234,6 +234,84 @@ __global__ void __launch_bounds__(256) k_apply_c1q_lo0(const double2 *__restrict
     }
 }
 
+// K1 for targets above bit 0: tuples t and t + 1 (t even) have bases b and
+// b + 1, so a thread applies the gate to both and moves each amplitude pair
+// of the two tuples with one 256-bit access.
+template <bool SPARSE, int UNROLL>
+__global__ void __launch_bounds__(256) k_apply2q_x2(const double2 *__restrict__ in, double2 *out, int logN,
+                                                    unsigned long long npairs, int lo, int hi, const Mat4 g)
+{
+    const int logU = logN - 2;
+    const u64 umask = (1ull << logU) - 1ull;
+    const u64 ol = 1ull << lo, oh = 1ull << hi;
+    const u64 off[4] = {0ull, ol, oh, ol + oh};
+    const u64 stride = (u64)gridDim.x * blockDim.x;
+    for (u64 p0 = (u64)blockIdx.x * blockDim.x + threadIdx.x; p0 < npairs; p0 += stride * UNROLL) {
+        double2 xe[UNROLL][4], xo[UNROLL][4];
+        u64 base[UNROLL];
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) {
+            const u64 pp = p0 + (u64)u * stride;
+            if (pp < npairs) {
+                const u64 t = 2 * pp, v = t >> logU, r = t & umask;
+                base[u] = (v << logN) | ins0(ins0(r, lo), hi);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) ld256(in + base[u] + off[i], xe[u][i], xo[u][i]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) {
+            const u64 pp = p0 + (u64)u * stride;
+            if (pp < npairs) {
+                double2 ye[4], yo[4];
+                mv4<SPARSE>(g, xe[u], ye);
+                mv4<SPARSE>(g, xo[u], yo);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) st256(out + base[u] + off[i], ye[i], yo[i]);
+            }
+        }
+    }
+}
+
+// the parity-controlled 1q gate above bit 0: pairs r and r + 1 (r even) per
+// thread, opposite parities, 256-bit accesses
+template <int UNROLL>
+__global__ void __launch_bounds__(256) k_apply_c1q_x2(const double2 *__restrict__ in, double2 *out, int logN,
+                                                      unsigned long long npairs, int pa, int sector, const Mat4 g)
+{
+    const int logU = logN - 1;
+    const u64 umask = (1ull << logU) - 1ull;
+    const u64 o = 1ull << pa;
+    const u64 stride = (u64)gridDim.x * blockDim.x;
+    for (u64 p0 = (u64)blockIdx.x * blockDim.x + threadIdx.x; p0 < npairs; p0 += stride * UNROLL) {
+        double2 xe[UNROLL][2], xo[UNROLL][2];
+        u64 base[UNROLL];
+        int P[UNROLL];
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) {
+            const u64 pp = p0 + (u64)u * stride;
+            if (pp < npairs) {
+                const u64 t = 2 * pp, v = t >> logU, r = ins0(t & umask, pa);
+                P[u] = (__popcll(r) & 1) ^ sector;
+                base[u] = (v << logN) | r;
+                ld256(in + base[u], xe[u][0], xo[u][0]);
+                ld256(in + base[u] + o, xe[u][1], xo[u][1]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) {
+            const u64 pp = p0 + (u64)u * stride;
+            if (pp < npairs) {
+                double2 ye[2], yo[2];
+                mv2(g, P[u], xe[u], ye);
+                mv2(g, P[u] ^ 1, xo[u], yo);
+                st256(out + base[u], ye[0], yo[0]);
+                st256(out + base[u] + o, ye[1], yo[1]);
+            }
+        }
+    }
+}
+
 // parity-controlled one-qubit gate of the compressed sector space
 template <int UNROLL>
 __global__ void __launch_bounds__(256) k_apply_c1q(const double2 *__restrict__ in, double2 *out, int logN,
@@ -482,6 +560,18 @@ extern "C" int gf_apply_gate(const void *in, void *out, int k, int t1, int t2, c
         else
             k_apply2q_lo0<false, 2><<<grid, 256, 0, st>>>((const double2 *)in, (double2 *)out, log2_exact(k), total,
                                                           nm.hi, g);
+    } else if (k >= 3 && !(nm.lo == 1 && nm.hi == 2)) {
+        // (bits 1 and 2: a thread's four 256-bit accesses would be one 128 B
+        // run with lanes 128 B apart -- measured 4.8 TB/s; the plain kernel
+        // keeps ~6.2)
+        const unsigned long long np = total / 2;  // 2^(k-2) tuples per vector: even
+        const int grid2 = grid_for(np, 256 * 2, 148 * 32);
+        if (parity_sparse)
+            k_apply2q_x2<true, 2><<<grid2, 256, 0, st>>>((const double2 *)in, (double2 *)out, log2_exact(k), np,
+                                                         nm.lo, nm.hi, g);
+        else
+            k_apply2q_x2<false, 2><<<grid2, 256, 0, st>>>((const double2 *)in, (double2 *)out, log2_exact(k), np,
+                                                          nm.lo, nm.hi, g);
     } else if (parity_sparse)
         k_apply2q<true, 2><<<grid, 256, 0, st>>>((const double2 *)in, (double2 *)out, log2_exact(k), total, nm.lo,
                                                  nm.hi, g);
@@ -510,6 +600,9 @@ extern "C" int gf_apply_gate_sector_c1q(const void *in, void *out, int k_full, i
     if (pa == 0)
         k_apply_c1q_lo0<2><<<grid, 256, 0, (cudaStream_t)stream>>>((const double2 *)in, (double2 *)out, K, total,
                                                                    sector, g);
+    else if (K >= 3)
+        k_apply_c1q_x2<2><<<grid_for(total / 2, 256 * 2, 148 * 32), 256, 0, (cudaStream_t)stream>>>(
+            (const double2 *)in, (double2 *)out, K, total / 2, pa, sector, g);
     else
         k_apply_c1q<2><<<grid, 256, 0, (cudaStream_t)stream>>>((const double2 *)in, (double2 *)out, K, total, pa,
                                                                sector, g);
