@@ -1,6 +1,7 @@
 // gf_ops.cu -- kernel-level C-ABI operations (reference kernels.py public ops),
 // parity-sector index maps, translation-orbit folding, error plumbing.
 #include <cuda_runtime.h>
+#include <cstdint>
 
 #include <algorithm>
 #include <cstdarg>
@@ -553,14 +554,17 @@ extern "C" int gf_apply_gate(const void *in, void *out, int k, int t1, int t2, c
     unsigned long long total = (1ull << (k - 2)) * (unsigned long long)nvec;
     int grid = grid_for(total, 256 * 2, 148 * 32);
     cudaStream_t st = (cudaStream_t)stream;
-    if (nm.lo == 0) {
+    // 256-bit accesses need 32 B aligned vectors (a view at an odd amplitude
+    // offset falls back to the 128-bit kernel)
+    const bool a32 = ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 31u) == 0;
+    if (nm.lo == 0 && a32) {
         if (parity_sparse)
             k_apply2q_lo0<true, 2><<<grid, 256, 0, st>>>((const double2 *)in, (double2 *)out, log2_exact(k), total,
                                                          nm.hi, g);
         else
             k_apply2q_lo0<false, 2><<<grid, 256, 0, st>>>((const double2 *)in, (double2 *)out, log2_exact(k), total,
                                                           nm.hi, g);
-    } else if (k >= 3 && !(nm.lo == 1 && nm.hi == 2)) {
+    } else if (a32 && k >= 3 && !(nm.lo == 1 && nm.hi == 2)) {
         // (bits 1 and 2: a thread's four 256-bit accesses would be one 128 B
         // run with lanes 128 B apart -- measured 4.8 TB/s; the plain kernel
         // keeps ~6.2)
@@ -597,10 +601,11 @@ extern "C" int gf_apply_gate_sector_c1q(const void *in, void *out, int k_full, i
     int pa = K - 1 - a;
     unsigned long long total = (1ull << (K - 1)) * (unsigned long long)nvec;
     int grid = grid_for(total, 256 * 2, 148 * 32);
-    if (pa == 0)
+    const bool a32 = ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 31u) == 0;
+    if (pa == 0 && a32)
         k_apply_c1q_lo0<2><<<grid, 256, 0, (cudaStream_t)stream>>>((const double2 *)in, (double2 *)out, K, total,
                                                                    sector, g);
-    else if (K >= 3)
+    else if (a32 && K >= 3)
         k_apply_c1q_x2<2><<<grid_for(total / 2, 256 * 2, 148 * 32), 256, 0, (cudaStream_t)stream>>>(
             (const double2 *)in, (double2 *)out, K, total / 2, pa, sector, g);
     else
