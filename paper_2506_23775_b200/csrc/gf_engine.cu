@@ -1351,7 +1351,10 @@ extern "C" int gf_plan_create(gf_plan **out, int k, int sector, int n_slots, con
         const char *fmenv = getenv("GF_FUSED_M");
         int fm = fmenv ? atoi(fmenv) : 11;  // 2^11 tiles: three vectors fit 2 CTAs per SM
         p->fm = std::max(5, std::min(std::min(fm, FMAXM), p->K));
-        p->fc = std::min(3, p->fm);  // 2^3-amplitude (128 B) contiguous runs: full DRAM lines, more planner freedom
+        // 2^3-amplitude (128 B) contiguous runs: full DRAM lines, more planner
+        // freedom (GF_FUSED_C overrides; experiments only)
+        const char *fcenv = getenv("GF_FUSED_C");
+        p->fc = std::min(fcenv ? std::max(1, atoi(fcenv)) : 3, p->fm);
         if (p->fused) {
             // the forward sweep stages one vector per tile: GF_FWD_M may give it
             // larger tiles (fewer passes) than the three-vector sweeps
