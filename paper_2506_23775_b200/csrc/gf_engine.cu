@@ -48,6 +48,9 @@
 #ifndef GF_GATE_BLOCK
 #define GF_GATE_BLOCK 4
 #endif
+#ifndef GF_SPARSE_DMMA_DEFAULT
+#define GF_SPARSE_DMMA_DEFAULT 0
+#endif
 
 namespace gf {
 
@@ -1141,6 +1144,7 @@ struct gf_plan {
     int last_flags = 0;
     // fused tile engine
     bool fused = false;
+    bool sparse_fma = true;  // parity-sparse slots as FMA (else dense DMMA with structural zeros)
     int fm = 0, fc = 0;
     // geometry only (matrices filled per eval).  The ascending HVP sweep must
     // replay exactly the reverse slot order of the reverse sweep (the two HVP
@@ -1287,6 +1291,38 @@ static void plan_free(gf_plan *p)
 
 static std::vector<FusedParams> plan_passes(const gf_plan *p, bool reverse, int m);
 
+// Environment knobs of the plan (diagnostics / experiments; the defaults are
+// the measured best), parsed in one place for gf_plan_create and the
+// host-only gf_plan_layout query.  The Python plan cache keys on the same
+// variables (objective.py _PLAN_KNOBS).
+struct PlanKnobs {
+    bool stream;       // GF_ENGINE=stream: one launch per slot
+    int fm;            // GF_FUSED_M: tile bits of the three-vector sweeps (default 11)
+    int fc;            // GF_FUSED_C: always-local low bits (default 3 = 128 B runs)
+    int fwm;           // GF_FWD_M: tile bits of the forward sweep (default fm)
+    long long ctas;    // GF_FUSED_CTAS: CTAs per vector (default 148 x 8)
+    bool sparse_dmma;  // GF_SPARSE_DMMA: parity-sparse slots on the DMMA path
+};
+
+static PlanKnobs plan_knobs(int K, int tile_bits)
+{
+    PlanKnobs k;
+    const char *eng = getenv("GF_ENGINE");
+    k.stream = eng && strcmp(eng, "stream") == 0;
+    const char *fmenv = getenv("GF_FUSED_M");
+    const int fm = tile_bits > 0 ? tile_bits : (fmenv ? atoi(fmenv) : 11);  // 2^11: three vectors, 2 CTAs/SM
+    k.fm = std::max(5, std::min(std::min(fm, FMAXM), K));
+    const char *fcenv = getenv("GF_FUSED_C");
+    k.fc = std::min(fcenv ? std::max(1, atoi(fcenv)) : 3, k.fm);
+    const char *fwenv = getenv("GF_FWD_M");
+    k.fwm = (fwenv && tile_bits <= 0) ? std::max(k.fc, std::min(std::min(atoi(fwenv), FMAXM), K)) : k.fm;
+    const char *cenv = getenv("GF_FUSED_CTAS");
+    k.ctas = cenv ? std::max(1ll, atoll(cenv)) : 148ll * 8;  // all tiles, up to 8 per SM
+    const char *sd = getenv("GF_SPARSE_DMMA");
+    k.sparse_dmma = sd ? atoi(sd) != 0 : GF_SPARSE_DMMA_DEFAULT;
+    return k;
+}
+
 // slot geometry (physical bit positions; qubit 0 = MSB) shared by plan
 // creation and the host-only layout query
 static int build_slots(gf_plan *p, int k, int sector, int n_slots, const int32_t *t1, const int32_t *t2,
@@ -1346,21 +1382,13 @@ extern "C" int gf_plan_create(gf_plan **out, int k, int sector, int n_slots, con
     int64_t ctas = (int64_t)(units / (kThreads * 4));
     p->ctas = (int)std::max<int64_t>(1, std::min<int64_t>(ctas, 148 * 8));
     {
-        const char *eng = getenv("GF_ENGINE");
-        p->fused = p->K >= 6 && !(eng && strcmp(eng, "stream") == 0);
-        const char *fmenv = getenv("GF_FUSED_M");
-        int fm = fmenv ? atoi(fmenv) : 11;  // 2^11 tiles: three vectors fit 2 CTAs per SM
-        p->fm = std::max(5, std::min(std::min(fm, FMAXM), p->K));
-        // 2^3-amplitude (128 B) contiguous runs: full DRAM lines, more planner
-        // freedom (GF_FUSED_C overrides; experiments only)
-        const char *fcenv = getenv("GF_FUSED_C");
-        p->fc = std::min(fcenv ? std::max(1, atoi(fcenv)) : 3, p->fm);
+        const PlanKnobs kn = plan_knobs(p->K, -1);
+        p->fused = p->K >= 6 && !kn.stream;
+        p->fm = kn.fm;
+        p->fc = kn.fc;
+        p->sparse_fma = !kn.sparse_dmma;
         if (p->fused) {
-            // the forward sweep stages one vector per tile: GF_FWD_M may give it
-            // larger tiles (fewer passes) than the three-vector sweeps
-            const char *fwenv = getenv("GF_FWD_M");
-            const int fwm = fwenv ? std::max(p->fc, std::min(std::min(atoi(fwenv), FMAXM), p->K)) : p->fm;
-            p->fwd_passes = plan_passes(p, false, fwm);
+            p->fwd_passes = plan_passes(p, false, kn.fwm);
             p->rev_passes = plan_passes(p, true, p->fm);
             p->asc_passes.assign(p->rev_passes.rbegin(), p->rev_passes.rend());
             for (auto &f : p->asc_passes) std::reverse(f.ps, f.ps + f.nslots);
@@ -1385,11 +1413,7 @@ extern "C" int gf_plan_create(gf_plan **out, int k, int sector, int n_slots, con
             // CTAs per vector: capacity for the smallest tiles; each launch uses
             // min(capacity, its tiles), one tile per CTA by default
             u64 ntiles = 1ull << (p->K - mmin);
-            {
-                const char *cenv = getenv("GF_FUSED_CTAS");
-                u64 want = cenv ? (u64)atoll(cenv) : (u64)(148 * 8);  // all tiles, up to 8 per SM
-                p->ctas = (int)std::max<u64>(1, std::min<u64>(want, ntiles));
-            }
+            p->ctas = (int)std::max<u64>(1, std::min<u64>((u64)kn.ctas, ntiles));
         }
     }
     // workspace
@@ -1755,13 +1779,16 @@ static int launch_fused_nt(const gf_plan *p, FusedParams &fp, int64_t nvec, cuda
 {
     const int nv = (OP == OP_FWD || OP == OP_FWD_DOT) ? 1 : (OP == OP_REV_G ? 2 : 2 + ND);
     const size_t smem = fused_smem(nv, fp.m, fp.c, NT / 32, ND);
-    static bool attr_done = false;
-    if (!attr_done) {
+    // the attribute is per device: set it once for every device this process drives
+    static unsigned long long attr_done = 0ull;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return gf_fail(GF_ECUDA, "no current CUDA device");
+    if (!((attr_done >> (dev & 63)) & 1ull)) {
         // 226 KB: the opt-in limit (227 KB) minus the kernel's static shared memory
         cudaError_t ae = cudaFuncSetAttribute(k_fused<OP, FIRST, NT, ND, SPX>,
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
         if (ae != cudaSuccess) return gf_fail(GF_ECUDA, "k_fused smem attribute: %s", cudaGetErrorString(ae));
-        attr_done = true;
+        attr_done |= 1ull << (dev & 63);
     }
     if (smem > 226 * 1024) return gf_fail(GF_EINVAL, "fused tile needs %zu B of shared memory", smem);
     dim3 grid(fp.ctas, (unsigned)nvec);
@@ -1906,7 +1933,7 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
                 fp.ps[t].fa2 = fp.ps[t].fa;
                 fp.ps[t].fb = fp.ps[t].fa;
                 fp.ps[t].fz = fp.ps[t].fa;
-                if (fp.ps[t].mode != PM_C1Q) fp.ps[t].mode = p->spG[s] ? PM_SPARSE : PM_DENSE;
+                if (fp.ps[t].mode != PM_C1Q) fp.ps[t].mode = (p->spG[s] && p->sparse_fma) ? PM_SPARSE : PM_DENSE;
             }
             const bool last = !grad_like && pi == nf - 1;
             if (last) ctas_v = fp.ctas;
@@ -1953,7 +1980,7 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
                     }
                     fp.ps[t].amask = act_rev;
                     act_rev |= fp.ps[t].zmask;
-                    if (fp.ps[t].mode != PM_C1Q) fp.ps[t].mode = sp ? PM_SPARSE : PM_DENSE;
+                    if (fp.ps[t].mode != PM_C1Q) fp.ps[t].mode = (sp && p->sparse_fma) ? PM_SPARSE : PM_DENSE;
                 }
                 // after the reverse sweep psi_0 = |j> is known exactly and chi is dead:
                 // the last pass writes back only the bra (needed by the ascending sweep)
@@ -1999,7 +2026,7 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
                         }
                         fp.ps[t].amask = act_asc;
                         act_asc |= fp.ps[t].zmask;
-                        if (fp.ps[t].mode != PM_C1Q) fp.ps[t].mode = sp ? PM_SPARSE : PM_DENSE;
+                        if (fp.ps[t].mode != PM_C1Q) fp.ps[t].mode = (sp && p->sparse_fma) ? PM_SPARSE : PM_DENSE;
                     }
                     if (pi == nr - 1) fp.store_mask = 0;  // nothing is read after the ascending sweep
                     if (pi == 0) { int rc_ = launch_fused<OP_ASC_H, true>(p, fp, nvec, st, nd); if (rc_) return rc_; }
@@ -2198,8 +2225,9 @@ extern "C" int gf_plan_layout(int k, int sector, int n_slots, const int32_t *t1,
     tmp.K = sector >= 0 ? k - 1 : k;
     tmp.n = n_slots;
     if (int rc = build_slots(&tmp, k, sector, n_slots, t1, t2, nullptr, 0)) return rc;
-    tmp.fm = std::max(5, std::min(std::min(tile_bits, FMAXM), tmp.K));
-    tmp.fc = std::min(3, tmp.fm);
+    const PlanKnobs kn = plan_knobs(tmp.K, std::max(1, tile_bits));
+    tmp.fm = kn.fm;
+    tmp.fc = kn.fc;
     std::vector<FusedParams> passes = plan_passes(&tmp, sweep != 0, tmp.fm);
     if ((int)passes.size() > max_passes) return gf_fail(GF_EINVAL, "%zu passes exceed the output room", passes.size());
     *n_passes = (int)passes.size();

@@ -1,18 +1,24 @@
 // gf_fused.cuh -- fused k-qubit tile passes (north-star item 1).
 //
 // A pass applies a run of slots whose target bits all lie in a set S of m
-// "local" bit positions (always including the c lowest bits, so every HBM
-// access is a >= 256 B contiguous run).  One CTA stages a tile -- the 2^m
-// amplitudes sharing one assignment of the K-m global bits -- of every vector
-// the sweep touches (psi, bra, chi/v) in shared memory, runs all slots of the
-// pass on it, and writes it back: one HBM round trip per pass instead of one
-// per slot.  Gate applications are FP64 FMAs on 4-amplitude tuples; the 4x4
-// hole contractions (reference kernels.py:208-242) are FP64 tensor-core
-// MMAs (DMMA m8n8k4): with the complex 4-vectors split into 8 real
-// components, C[r][s] = sum_env bra_r ket_s is an 8x8 GEMM with the
-// environment as the K dimension, accumulated in 2 registers per lane; the
-// 8 warps' fragments are summed in a fixed order in shared memory, so the
-// result is deterministic.
+// "local" bit positions (always including the c = 3 lowest bits, so every HBM
+// access is a >= 128 B contiguous run, one full DRAM line).  One CTA stages a
+// tile -- the 2^m amplitudes sharing one assignment of the K-m global bits --
+// of every vector the sweep touches (psi, bra, chi/v) in shared memory, runs
+// all slots of the pass on it, and writes it back: one HBM round trip per pass
+// instead of one per slot.
+//
+// All dense FP64 math runs on the tensor cores (DMMA m8n8k4):
+//  * gate applications: a lane owns one complex amplitude of an 8-tuple group
+//    and y = G x is two MMA k-steps with G's real 8x8 form as the B fragment;
+//  * 4x4 hole contractions (reference kernels.py:208-242): with the complex
+//    4-vectors split into 8 real components, C[r][s] = sum_env bra_r ket_s is
+//    an 8x8 GEMM with the environment as K, accumulated in 2 registers per
+//    lane; the warps' fragments are summed in a fixed order in shared memory,
+//    so the result is deterministic.
+// Parity-controlled one-qubit slots (the sector's implicit qubit) and, unless
+// GF_SPARSE_DMMA routes them to the DMMA path, parity-sparse two-qubit slots
+// are FP64 FMAs.
 #pragma once
 #include "gf_common.cuh"
 

@@ -502,7 +502,7 @@ __device__ __forceinline__ void canon(u64 x, int L, u64 &rep, int &size)
     u64 best = x, y = x;
     int sz = period;
     for (int s = 1; s < period; ++s) {
-        y = (L % 2 == 0) ? shift2(y, L) : shift2(y, L);
+        y = shift2(y, L);
         if (y == x && sz == period) sz = s;
         best = y < best ? y : best;
     }

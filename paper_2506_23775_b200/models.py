@@ -317,6 +317,7 @@ class DenseOracle:
         if spec.num_qubits > 14:
             raise ValueError("dense oracle capped at 14 qubits")
         self.num_qubits = spec.num_qubits
+        self.spec = spec
         self._u = scipy.linalg.expm(-1j * t * dense_hamiltonian(spec))
         self._cols = None
         self._sector_cols = {}
@@ -672,6 +673,7 @@ class CachedTargetColumns:
     def __init__(self, oracle, k: int, p0: int, p1: int, sector=None, indices=None, batch: int = 256):
         self.num_qubits = oracle.num_qubits
         self.inner = oracle
+        self.spec = getattr(oracle, "spec", None)
         self.p0, self.p1 = p0, p1
         self.sector = sector
         self.indices = None if indices is None else np.asarray(indices, np.int64).copy()

@@ -59,6 +59,7 @@ __all__ = [
     "frobenius_error_squared",
     "default_workers",
     "BasisSpec",
+    "check_translation_invariant",
 ]
 
 COUNT_NAMES = (
@@ -247,13 +248,16 @@ class EnginePlan:
 
 
 _PLANS: dict = {}
+# environment knobs read by gf_plan_create (csrc/gf_engine.cu plan_knobs): part
+# of the plan cache key so a changed knob never reuses a plan built without it
+_PLAN_KNOBS = ("GF_ENGINE", "GF_FUSED_M", "GF_FWD_M", "GF_FUSED_C", "GF_FUSED_CTAS", "GF_PLAN_GREEDY",
+               "GF_SPARSE_DMMA")
 
 
 def _get_plan(circuit: Circuit, sector: int, batch: int, chunk: int) -> EnginePlan:
     t1, t2, lid = circuit.slot_arrays()
     key = (torch.cuda.current_device(), circuit.num_qubits, sector, t1.tobytes(), t2.tobytes(), lid.tobytes(),
-           circuit.num_logical, batch, chunk, os.environ.get("GF_ENGINE"), os.environ.get("GF_FUSED_M"),
-           os.environ.get("GF_FUSED_CTAS"))
+           circuit.num_logical, batch, chunk) + tuple(os.environ.get(v) for v in _PLAN_KNOBS)
     plan = _PLANS.get(key)
     if plan is None:
         while len(_PLANS) >= 4:
@@ -307,6 +311,58 @@ def fold_basis(k: int, sector: int, L: int | None = None) -> BasisSpec:
         ws.append(mark[nz].to(torch.float64).cpu().numpy())
     idx = np.concatenate(reps).astype(np.int64)
     return BasisSpec(int(idx.size), idx, np.concatenate(ws))
+
+
+def _shift2(q: int, k: int) -> int:
+    """Qubit image under the 2-site translation of both spin chains (qubit
+    c*L + s -> c*L + (s + 2) mod L, L = k/2)."""
+    L = k // 2
+    c, s = divmod(q, L)
+    return c * L + (s + 2) % L
+
+
+def check_translation_invariant(circuit: Circuit, oracle=None):
+    """Raise ValueError unless folding the basis sum by 2-site translations is
+    exact: the circuit maps onto itself under the shift (every slot's image is
+    a slot of the same logical gate with the same target order, and slots
+    sharing a qubit keep their relative order) and, when the oracle exposes
+    its Hamiltonian spec, the target is periodic and translation-invariant."""
+    k = circuit.num_qubits
+    if k % 2 or k < 4:
+        raise ValueError("translation folding needs a spinful chain (even qubit count >= 4)")
+    where = {}
+    for i, s in enumerate(circuit.slots):
+        where.setdefault((s.logical_id, s.targets), []).append(i)
+    img = []
+    for s in circuit.slots:
+        key = (s.logical_id, (_shift2(s.targets[0], k), _shift2(s.targets[1], k)))
+        cand = where.get(key)
+        if not cand:
+            raise ValueError(f"fold=True: the image of slot {s.targets} (logical {s.logical_id}) under the 2-site "
+                             "translation is not a slot of the same logical gate; the circuit is not "
+                             "translation-invariant (periodic, one gate per layer)")
+        img.append(cand[0] if len(cand) == 1 else -1)
+    if -1 in img:
+        raise ValueError("fold=True: duplicate slots make the translation image ambiguous")
+    n = circuit.num_slots
+    qs = [set(s.targets) for s in circuit.slots]
+    for a in range(n):
+        for b in range(a + 1, n):
+            if qs[a] & qs[b] and img[a] > img[b]:
+                raise ValueError("fold=True: the 2-site translation reorders non-commuting slots")
+    spec = getattr(oracle, "spec", None)
+    if spec is not None:
+        if not getattr(spec, "periodic", False):
+            raise ValueError("fold=True needs a periodic (translation-invariant) target Hamiltonian")
+        terms = {(t.operator, tuple(t.sites), float(t.coefficient)) for t in spec.terms}
+
+        def canon(op, a, b):
+            return (op, (a, b)) if op != "hop" else (op, (min(a, b), max(a, b)))
+
+        tset = {canon(o, *st) + (c,) for o, st, c in terms}
+        for o, st, c in terms:
+            if canon(o, _shift2(st[0], k), _shift2(st[1], k)) + (c,) not in tset:
+                raise ValueError("fold=True: the target Hamiltonian is not invariant under 2-site translations")
 
 
 def _resolve_basis(k, sector, fold, basis) -> BasisSpec:
@@ -389,6 +445,8 @@ class _Run:
         self.sector = _sector_code(sector)
         self.circuit = circuit
         self.flags = flags
+        if fold:
+            check_translation_invariant(circuit, oracle)
         self.spec = _resolve_basis(self.k, self.sector, fold, basis)
         self.N = 1 << (self.k - (1 if self.sector >= 0 else 0))
         total = self.spec.total
@@ -412,7 +470,7 @@ class _Run:
         lo, hi = shard_chunks(nchunks, self.rank, self.world)
         rec = self.rec
         local = torch.zeros((hi - lo, rec), dtype=torch.float64, device=dev)
-        phi0 = torch.empty((self.batch, self.N), dtype=torch.complex128, device=dev)
+        phi0 = None  # allocated on the first batch the oracle has no resident rows for
         idx_all = None if self.spec.indices is None else torch.from_numpy(self.spec.indices).to(dev)
         w_all = None if self.spec.weights is None else torch.from_numpy(self.spec.weights).to(dev)
         launches = 0
@@ -429,6 +487,8 @@ class _Run:
             rows = getattr(self.oracle, "phi0_at", None)
             cur = rows(pos, nvec, self.sector, self.spec.indices) if rows is not None else None
             if cur is None:
+                if phi0 is None:
+                    phi0 = torch.empty((self.batch, self.N), dtype=torch.complex128, device=dev)
                 self._fill_phi0(basis, phi0[:nvec])
                 cur = phi0
             c0 = (pos // chunk) - lo
@@ -536,7 +596,7 @@ def _grad_report(circuit, run, value, holo, parity_mode, kind, t0, hvp=None):
         wall_time=time.perf_counter() - t0,
         pass_counts=_ref_counts(circuit.num_slots, S, kind),
         engine={"launches": run.launches, "summands": S, "batch": run.batch, "chunk": run.chunk,
-                "seconds": run.elapsed, "world": run.world},
+                "seconds": run.elapsed, "world": run.world, "weight_sum": run.spec.weight_sum()},
     )
 
 
@@ -567,6 +627,15 @@ def gradient_and_hvp(circuit: Circuit, oracle, directions, parity_mode: bool = F
     return rep, [h[i] for i in range(circuit.num_logical)]
 
 
+def _multi_direction_ok(circuit, sector, batch, chunk, basis, fold) -> bool:
+    """True when the plan for this evaluation runs the fused engine (the only
+    one that evaluates several HVP directions per sweep)."""
+    if os.environ.get("GF_ENGINE") == "stream":
+        return False
+    K = circuit.num_qubits - (1 if _sector_code(sector) >= 0 else 0)
+    return K >= 6 and circuit.num_slots > 0
+
+
 def hessian_vector_products(circuit: Circuit, oracle, direction_sets, *, sector=None, fold=False, basis=None,
                             batch=None, chunk=None, distributed=None):
     """Several HVPs with shared forward / reverse state sweeps: up to 3
@@ -579,14 +648,11 @@ def hessian_vector_products(circuit: Circuit, oracle, direction_sets, *, sector=
     while i < len(zs):
         group = zs[i:i + 3]
         z = np.ascontiguousarray(np.stack(group)) if len(group) > 1 else group[0]
-        try:
-            run = _Run(circuit, oracle, _lib.GF_HVP, z, sector, fold, basis, batch, chunk, distributed)
-        except ValueError:
-            if len(group) == 1:
-                raise
-            # the streaming engine (tiny state spaces) evaluates one direction per sweep
+        if len(group) > 1 and not _multi_direction_ok(circuit, sector, batch, chunk, basis, fold):
+            # the streaming engine (tiny state spaces, GF_ENGINE=stream) runs one direction per sweep
             group = group[:1]
-            run = _Run(circuit, oracle, _lib.GF_HVP, group[0], sector, fold, basis, batch, chunk, distributed)
+            z = group[0]
+        run = _Run(circuit, oracle, _lib.GF_HVP, z, sector, fold, basis, batch, chunk, distributed)
         _, _, h = run.run()
         hs = [h] if len(group) == 1 else list(h)
         out += [[x[j] for j in range(circuit.num_logical)] for x in hs]
