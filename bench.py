@@ -1,14 +1,30 @@
 #!/usr/bin/env python
-"""Benchmark: full-basis-sum value + gradient + HVP evaluations of BASELINE.json
+"""Benchmark: value + gradient + HVP summand evaluations of BASELINE.json
 configs[1] (L=8 spinful Fermi-Hubbard, 16 qubits, 5 layers / 36 slots, Haar
 gates seed 1, target exp(-iHt) with J=1, U=4, t=0.25).
 
-One step = one evaluation of f, its Riemannian gradient and one Hessian-vector
-product summed over all 2^16 basis states (the reference's full_gradient +
-hessian_vector_product, objective.py:659-698 / 770-814), fused into one
-reversible 3-sweep pass per summand.  With N GPUs (torchrun) the fixed basis
-sum is sharded over ranks in contiguous chunks (strong scaling); the only
-collective is the all-gather of per-chunk records.
+A *summand* is one basis state |j> of the basis sum: its value phi0 . C|j>,
+its gradient holes (reference _gradient_chunk, objective.py:322-337) and its
+HVP holes along the seeded tangent direction (reference _hvp_chunk,
+objective.py:432-482).  The metric is summands per second; the full-sum
+figure (one evaluation = all 2^16 summands) is derived beside it
+(``full_sum_evals_per_s``).
+
+* B200 arm (default): one step = one full-sum evaluation (65536 summands),
+  fused into one reversible 3-sweep pass per summand by the engine.  With N
+  GPUs (torchrun, or self-launched by ``--gpus N``) the fixed basis sum is
+  sharded over ranks in contiguous chunks (strong scaling); the only
+  collective is the all-gather of per-chunk records.
+* ``--impl reference``: the reference algorithm's CPU implementation (the C
+  port in oracle/, restating the reference drivers) on every host thread;
+  one step = a bounded 64-summand sample of the same workload.  The circuit
+  and direction are read from tests/golden/c2_slice.npz, which the unmodified
+  reference wrote; nothing of the product package is imported.
+
+In both arms ``value`` excludes target generation (phi0 precomputed: cached
+HBM columns on the GPU, Lanczos columns on the host); the target-inclusive
+variants are reported beside it (``e2e`` on the GPU, ``with_target`` on the
+host).
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
@@ -19,8 +35,8 @@ from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
+import socket
 import subprocess
 import sys
 import tempfile
@@ -32,10 +48,21 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "gradient+HVP evals/sec at 16-site Hubbard; gate-apply HBM GB/s vs peak"
-UNIT = "evals/s"
+UNIT = "gradient+HVP summand-evals/s"
 L_SITES, LAYERS, SEED, T_EVOL = 8, 5, 1, 0.25
 K_QUBITS = 2 * L_SITES
 TOTAL = 1 << K_QUBITS
+REF_SAMPLE = 64  # summands per reference-arm step
+# identical in both arms (the driver compares them)
+CONFIG = {
+    "workload": "c2 (BASELINE configs[1]): spinful Fermi-Hubbard L=8 open, 16 qubits, J=1 U=4 t=0.25; circuit 5 "
+                "layers = 36 slots / 5 logical Haar gates (seed 1); per summand |j>: value + gradient + one HVP "
+                "along the seeded tangent direction",
+    "full_sum_summands": TOTAL,
+    "targets": "phi0 = conj(exp(-iHt)|j>) precomputed outside the timed region (target-inclusive variant reported "
+               "separately)",
+    "parallelism": "basis-sum data parallel",
+}
 
 
 def _peaks():
@@ -103,39 +130,65 @@ class Clocks:
                 "samples": len(sm)}
 
 
-def _dist():
+# ---------------------------------------------------------------------------
+# process group
+# ---------------------------------------------------------------------------
+
+
+def _self_launch(args) -> int:
+    """``--gpus N`` outside torchrun: start N ranks with torch.distributed.run
+    on 127.0.0.1 and return their exit code."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def _dist(args):
     import torch
     import torch.distributed as dist
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    ngpu = torch.cuda.device_count()
+    # --backend gloo on a one-GPU box: ranks share cuda:0 (CPU test of the multi-rank path only)
+    dev = local if args.backend == "nccl" else local % max(ngpu, 1)
+    torch.cuda.set_device(dev)
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(0)
-    return rank, world, local, (dist if world > 1 else None)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group("gloo")
+    return rank, world, dev, (dist if world > 1 else None)
+
+
+def _reduce_over_ranks(x, dist, op):
+    import torch
+
+    if dist is None:
+        return x
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=op)
+    return float(t.item())
 
 
 def _max_over_ranks(x, dist):
-    import torch
-
-    if dist is None:
-        return x
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    return x if dist is None else _reduce_over_ranks(x, dist, dist.ReduceOp.MAX)
 
 
 def _sum_over_ranks(x, dist):
-    import torch
+    return x if dist is None else _reduce_over_ranks(x, dist, dist.ReduceOp.SUM)
 
-    if dist is None:
-        return x
-    t = torch.tensor([float(x)], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.SUM)
-    return float(t.item())
+
+# ---------------------------------------------------------------------------
+# measurement helpers
+# ---------------------------------------------------------------------------
 
 
 def measure_fp64_peaks(gf):
@@ -145,6 +198,7 @@ def measure_fp64_peaks(gf):
     sink = torch.zeros(1, dtype=torch.float64, device="cuda")
     out = {}
     st = gf._lib.stream_ptr()
+    stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for which, key in ((0, "dmma_tflops"), (1, "dfma_tflops")):
         fl = np.zeros(1)
@@ -152,9 +206,9 @@ def measure_fp64_peaks(gf):
         torch.cuda.synchronize()
         best = 0.0
         for _ in range(3):
-            e0.record()
+            e0.record(stream)
             gf._lib.check(gf._lib.lib.gf_peak_fp64(which, 148 * 4, 2048, sink.data_ptr(), fl.ctypes.data, st))
-            e1.record()
+            e1.record(stream)
             torch.cuda.synchronize()
             best = max(best, fl[0] / (e0.elapsed_time(e1) * 1e-3) / 1e12)
         out[key] = round(best, 2)
@@ -164,8 +218,9 @@ def measure_fp64_peaks(gf):
 def gate_apply_sweep(gf, peak):
     """Standalone K1 bandwidth sweep on one 2^31-amplitude complex128 vector
     (the c5 compressed 31-qubit space, 32 GiB): 2q adjacent (t, t+1), 2q long
-    range (t, t+15 mod 31), and the parity-controlled 1q gate of the implicit
-    qubit; in place, 32 B per amplitude per application."""
+    range (t, t+15 mod 31), the generic 1q gate on every qubit and the
+    parity-controlled 1q gate of the implicit qubit; in place, 32 B per
+    amplitude per application."""
     import torch
 
     K = 31
@@ -179,34 +234,38 @@ def gate_apply_sweep(gf, peak):
     x.imag.normal_()
     rng = np.random.default_rng(0)
     st = gf._lib.stream_ptr()
-    # every target position: adjacent pairs, long-range pairs
-    # like the spinful interaction bonds, and the parity-controlled 1q gate on
-    # each explicit qubit (the sector's 1q path)
+    stream = torch.cuda.current_stream()
     cases = [("adj", t, t + 1) for t in range(K - 1)] + [("long", t, (t + 15) % K) for t in range(K)]
+    cases += [("1q", a, None) for a in range(K)]
     cases += [("c1q", a, None) for a in range(K)]
     results = []
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for kind, a, b in cases:
-        g = gf.manifold.random_unitary(4, rng)
         if kind == "c1q":
             g = gf.manifold.parity_join(gf.manifold.random_unitary(2, rng), gf.manifold.random_unitary(2, rng))
+        elif kind == "1q":
+            g = gf.manifold.random_unitary(2, rng)
+        else:
+            g = gf.manifold.random_unitary(4, rng)
         g = np.ascontiguousarray(g)
 
         def launch():
             if kind == "c1q":
                 gf._lib.check(gf._lib.lib.gf_apply_gate_sector_c1q(x.data_ptr(), x.data_ptr(), K + 1, a, 0,
                                                                    g.ctypes.data, 1, st))
+            elif kind == "1q":
+                gf._lib.check(gf._lib.lib.gf_apply_gate_1q(x.data_ptr(), x.data_ptr(), K, a, g.ctypes.data, 1, st))
             else:
                 gf._lib.check(gf._lib.lib.gf_apply_gate(x.data_ptr(), x.data_ptr(), K, a, b, g.ctypes.data, 0, 1,
                                                         st))
 
         launch()
         torch.cuda.synchronize()
-        e0.record()
+        e0.record(stream)
         reps = 3
         for _ in range(reps):
             launch()
-        e1.record()
+        e1.record(stream)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / reps
         gbs = 32.0 * N / (ms * 1e-3) / 1e9
@@ -249,100 +308,187 @@ def cpu_gate_apply(k=24):
     return {"vector_amplitudes": 1 << k, "threads": 1, "gbs": out}
 
 
-def cpu_port_rate(circ, X, phi_host, js, workers, with_oracle_terms=None):
-    """Oracle port (oracle/gf_oracle.c, restating the reference drivers) on
-    the host: gradient + HVP per summand, summands spread over `workers`
-    threads.  Returns summands per second."""
+def port_grad_hvp(plan, X, js, phi_rows, workers):
+    """Oracle port (oracle/gf_oracle.c, restating the reference drivers
+    _gradient_chunk + _hvp_chunk, objective.py:322-337, 432-482) on the host:
+    gradient + HVP of every summand of js, spread over `workers` threads (the
+    reference's parallel_reduce over its ThreadPoolExecutor).  Returns
+    (seconds, value sum)."""
     from concurrent.futures import ThreadPoolExecutor
 
     from oracle import gf_oracle as O
 
-    t1, t2, lid = circ.slot_arrays()
-    plan = O.Plan(circ.num_qubits, np.stack([t1, t2], 1), lid, circ.gate_stack())
-    parts = np.array_split(np.arange(len(js)), workers)
+    parts = [p for p in np.array_split(np.arange(len(js)), workers) if len(p)]
 
     def work(sel):
-        if len(sel) == 0:
-            return 0
         jj = js[sel]
-        if with_oracle_terms is not None:
-            P = O.lanczos_phi0(circ.num_qubits, with_oracle_terms, T_EVOL)(jj)
-        else:
-            P = phi_host[sel]
+        P = phi_rows[sel]
         fn = lambda q: P[np.searchsorted(jj, q)]
-        O.gradient_sum(plan, jj, fn)
+        v, _, _ = O.gradient_sum(plan, jj, fn)
         O.hvp_sum(plan, X, jj, fn)
-        return len(sel)
+        return v
 
     t0 = time.perf_counter()
     with ThreadPoolExecutor(max_workers=workers) as ex:
-        n = sum(ex.map(work, parts))
-    return n / (time.perf_counter() - t0)
+        v = sum(ex.map(work, parts))
+    return time.perf_counter() - t0, v
+
+
+def lanczos_rows(js, workers):
+    """phi0 rows of js from the oracle's restatement of the reference
+    KrylovOracle (models.py:322-384); returns (rows, seconds)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import gf_oracle as O
+
+    terms, _ = O.spinful_terms(L_SITES, 1.0, 4.0, False)
+    fn = O.lanczos_phi0(K_QUBITS, terms, T_EVOL)
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=workers) as ex:
+        rows = list(ex.map(lambda j: fn(np.array([j]))[0], js))
+    return np.ascontiguousarray(np.stack(rows)), time.perf_counter() - t0
+
+
+# ---------------------------------------------------------------------------
+# reference arm
+# ---------------------------------------------------------------------------
 
 
 def run_reference(args):
     """--impl reference: the reference algorithm's CPU implementation (the
-    oracle port; the reference itself is numba and cannot travel), including
-    its own target oracle (Lanczos, models.py:322-384) per summand, on all host
-    threads; bounded samples of the same c2 workload."""
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    oracle port; the reference itself is numba and cannot travel) on all host
+    threads.  Each step evaluates gradient + HVP of a fixed seeded sample of
+    REF_SAMPLE c2 summands; ms_per_step is the measured wall time of one step.
+    The circuit, gates and direction come from the reference-written fixture
+    tests/golden/c2_slice.npz (identical to the B200 arm's recipe, checked by
+    tests/test_host_logic.py)."""
+    if int(os.environ.get("RANK", "0")) != 0:
         return
     from oracle import gf_oracle as O
 
-    gf, spec, circ, X = workload()
-    terms, _ = O.spinful_terms(L_SITES, 1.0, 4.0, False)
+    d = np.load(os.path.join(ROOT, "tests", "golden", "c2_slice.npz"))
+    plan = O.Plan(int(d["k"]), d["targets"], d["logical"], d["gates"])
+    X = list(d["direction"])
     cores = os.cpu_count() or 1
     rng = np.random.default_rng(7)
-    sample = max(cores, 16)
-    rates = []
+    js = np.sort(rng.choice(TOTAL, size=REF_SAMPLE, replace=False)).astype(np.int64)
+    rows, lanczos_s = lanczos_rows(js, cores)  # setup: targets are outside `value` in both arms
+    times = []
     for step in range(args.warmup + args.steps):
-        js = np.sort(rng.choice(TOTAL, size=sample, replace=False))
-        r = cpu_port_rate(circ, X, None, js, cores, with_oracle_terms=terms)
+        dt, _ = port_grad_hvp(plan, X, js, rows, cores)
         if step >= args.warmup:
-            rates.append(r)
-    summ_rate = float(np.mean(rates))
-    v = summ_rate / TOTAL
+            times.append(dt)
+    tot = float(np.sum(times))
+    v = REF_SAMPLE * len(times) / tot
+    target_rate = REF_SAMPLE / lanczos_s
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 / v, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "c128", "data": "synthetic (BASELINE configs[1] recipe)",
-        "config": {"workload": "c2 full 2^16 basis sum, value+gradient+HVP (extrapolated from per-step samples)",
-                   "summands_per_step_sample": sample},
+        "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "c128",
+        "data": "synthetic: BASELINE configs[1] circuit and direction from tests/golden/c2_slice.npz (written by the "
+                "unmodified reference); targets from the Lanczos restatement of the reference KrylovOracle",
+        "config": CONFIG,
+        "step": f"gradient + HVP of a fixed seeded sample of {REF_SAMPLE} summands (reference _gradient_chunk + "
+                f"_hvp_chunk restated in oracle/gf_oracle.c) on {cores} host threads",
+        "full_sum_evals_per_s": v / TOTAL,
+        "with_target": {"value": 1.0 / (1.0 / v + 1.0 / target_rate), "unit": UNIT,
+                        "lanczos_summands_per_s": target_rate,
+                        "note": "Lanczos target column per summand included (the reference _phi_block path)"},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{sample} random c2 summands per step: Lanczos phi0 + gradient + HVP "
-                                   f"(oracle/gf_oracle.c restating reference objective.py:291-482), "
-                                   f"extrapolated x{TOTAL}/{sample}"},
+                         "sample": f"{REF_SAMPLE} seeded c2 summands per step, gradient + HVP each, phi0 "
+                                   f"precomputed"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------------------
+# c5 secondary measurement (BASELINE configs[4], one summand)
+# ---------------------------------------------------------------------------
+
+
+def c5_summand(gf, dmma_peak):
+    """One c5 summand (L=16 periodic, 32 qubits, even sector compressed to
+    2^31 amplitudes, 144 slots / 9 logical, folded orbit representative):
+    value + gradient + one HVP.  Algorithmic FP64 flops per summand: per
+    amplitude per 2q slot 9 parity-gate applications at 16 flop + 3 holes at
+    32 flop (1q parity-controlled slots: 9 x 16 + 3 x 16)."""
+    import torch
+
+    spec, circ, rng = gf.spinful_layer_circuit(16, 9, True, seed=4, parity=True)
+    X = [gf.manifold.project_tangent_gate(g.matrix, rng.normal(size=(4, 4)) + 1j * rng.normal(size=(4, 4)), True)
+         for g in circ.logical_gates]
+    k = circ.num_qubits
+    N = 1 << (k - 1)
+    srng = np.random.default_rng(5)
+    i0 = int(srng.integers(0, N))
+    x = torch.tensor([i0], dtype=torch.int64, device="cuda")
+    full, rep, size, comp = (torch.empty_like(x) for _ in range(4))
+    st = gf._lib.stream_ptr()
+    gf._lib.check(gf._lib.lib.gf_sector_unrank(x.data_ptr(), 1, 0, full.data_ptr(), st))
+    gf._lib.check(gf._lib.lib.gf_orbit_canon(full.data_ptr(), 1, 16, rep.data_ptr(), size.data_ptr(), st))
+    gf._lib.check(gf._lib.lib.gf_sector_rank(rep.data_ptr(), 1, comp.data_ptr(), st))
+    basis = (comp.cpu().numpy(), size.cpu().numpy().astype(np.float64))
+    orc = gf.NumberBlockOracle(spec, T_EVOL)
+    cache = gf.models.CachedTargetColumns(orc, k, 0, 1, sector=0, indices=basis[0], batch=1)
+    del orc
+    torch.cuda.empty_cache()
+    gf.gradient_and_hvp(circ, cache, X, parity_mode=True, sector=0, basis=basis)  # plan + warm-up
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    gf.gradient_and_hvp(circ, cache, X, parity_mode=True, sector=0, basis=basis)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    s = e0.elapsed_time(e1) * 1e-3
+    t1, t2, _ = circ.slot_arrays()
+    n1q = int(np.sum((t1 == k - 1) | (t2 == k - 1)))
+    n2q = circ.num_slots - n1q
+    flops = float(N) * (n2q * (9 * 16 + 3 * 32) + n1q * (9 * 16 + 3 * 16))
+    from paper_2506_23775_b200 import objective as obj
+
+    shape = list(obj._PLANS.values())[-1].describe()
+    obj._PLANS.clear()
+    del cache
+    torch.cuda.empty_cache()
+    return {"config": "c5 (BASELINE configs[4]): L=16 periodic, 32 qubits, even sector (2^31 amplitudes), fold, "
+                      "144 slots / 9 logical; one summand value + gradient + HVP",
+            "summand_evals_per_s": 1.0 / s, "s_per_summand": s, "fp64_tflops": flops / s / 1e12,
+            "frac_of_dmma_peak": flops / s / 1e12 / dmma_peak, "algorithmic_flops": flops,
+            "engine": shape}
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+
+
 def run_b200(args):
     import torch
 
-    rank, world, local, dist = _dist()
+    rank, world, dev, dist = _dist(args)
     gf, spec, circ, X = workload()
     from paper_2506_23775_b200 import objective as obj
 
     peak, peak_src = _peaks()
     chunk = obj.CHUNK_STATES
     N = TOTAL
-    nchunks = TOTAL // chunk
-    lo, hi = obj.shard_chunks(nchunks, rank, world)
-    p0, p1 = lo * chunk, hi * chunk
-    if args.summands:
-        p1 = min(p1, p0 + args.summands)
+    summands = min(args.summands, TOTAL) if args.summands else TOTAL
+    nchunks = (summands + chunk - 1) // chunk
+    lo, hi = obj.shard_chunks(nchunks, rank, world)  # this rank's positions of the basis sum
+    p0, p1 = lo * chunk, min(summands, hi * chunk)
     batch = args.batch or obj._default_batch(N, TOTAL)
     make_target = {"blocks": gf.NumberBlockOracle, "chebyshev": gf.ChebyshevOracle}[args.oracle]
     oracle = make_target(spec, T_EVOL)
     t_or = time.perf_counter()
-    cache = gf.models.CachedTargetColumns(oracle, K_QUBITS, p0, p1, batch=batch)
+    sel = np.arange(summands, dtype=np.int64) if args.summands else None
+    cache = gf.models.CachedTargetColumns(oracle, K_QUBITS, p0, max(p1, p0), indices=sel, batch=batch)
     torch.cuda.synchronize()
     oracle_setup_s = time.perf_counter() - t_or
     kw = dict(batch=batch, distributed=(dist is not None))
     if args.summands:
-        kw["basis"] = np.arange(min(args.summands, TOTAL), dtype=np.int64)
+        kw["basis"] = sel
     for _ in range(args.warmup):
         rep, hv = gf.gradient_and_hvp(circ, cache, X, **kw)
     torch.cuda.synchronize()
@@ -352,7 +498,7 @@ def run_b200(args):
 
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    clk = Clocks(local)
+    clk = Clocks(dev)
     clk.start()
     launches = 0
     if dist is not None:
@@ -370,7 +516,7 @@ def run_b200(args):
     ms = e0.elapsed_time(e1)
     ms_max = _max_over_ranks(ms, dist)
     launches_all = int(_sum_over_ranks(launches, dist))
-    value = args.steps / (ms_max * 1e-3)
+    value = summands * args.steps / (ms_max * 1e-3)
 
     ms4 = np.zeros(4)
     l4 = np.zeros(4, dtype=np.int64)
@@ -398,8 +544,6 @@ def run_b200(args):
         if nm in flops_phase and ms4[i] > 0:
             phases[nm]["fp64_tflops"] = round(flops_phase[nm] / (ms4[i] * 1e-3) / 1e12, 3)
             phases[nm]["hbm_gbs_pass_model"] = round(pass_bytes[nm] * l4[i] / (ms4[i] * 1e-3) / 1e9, 1)
-            phases[nm]["slot_stream_equiv_gbs"] = round(
-                {"forward": 32.0, "reverse": 96.0, "ascending": 96.0}[nm] * N * n * my_summands / (ms4[i] * 1e-3) / 1e9, 1)
     dom = max(("forward", "reverse", "ascending"), key=lambda k: ms4[names.index(k)])
     achieved = phases[dom]["fp64_tflops"]
     traffic = None
@@ -434,31 +578,39 @@ def run_b200(args):
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = _max_over_ranks(e0.elapsed_time(e1), dist)
-    e2e_val = e2e_steps / (e2e_ms * 1e-3)
+    e2e_val = summands * e2e_steps / (e2e_ms * 1e-3)
     rec_bytes = (2 + 64 * circ.num_logical) * 8 * nchunks
     h2d = gates_host.nbytes + dirs_host.nbytes
     # consistency: same objective from both paths
     assert abs(rep_e.value - rep.value) <= 1e-10 * max(1.0, abs(rep.value)), (rep_e.value, rep.value)
 
+    del cache
+    obj._PLANS.clear()
+    torch.cuda.empty_cache()
     gate_sweep = None
     cpu = None
+    c5 = None
     if rank == 0 and world == 1:
         if not args.no_sweep:
             gate_sweep = gate_apply_sweep(gf, peak)
+        if not args.no_c5:
+            c5 = c5_summand(gf, peaks64["dmma_tflops"])
         if not args.no_cpu:
+            from oracle import gf_oracle as O
+
             cores = os.cpu_count() or 1
             srng = np.random.default_rng(11)
-            sample = max(cores, 64)
-            js = np.sort(srng.choice(TOTAL, size=sample, replace=False))
-            phi = torch.empty((sample, N), dtype=torch.complex128, device="cuda")
+            js = np.sort(srng.choice(TOTAL, size=REF_SAMPLE, replace=False)).astype(np.int64)
+            phi = torch.empty((REF_SAMPLE, N), dtype=torch.complex128, device="cuda")
             oracle.phi0_into(torch.from_numpy(js).cuda(), None, phi)
             ph = phi.cpu().numpy()
             del phi
-            r = cpu_port_rate(circ, X, ph, js, cores)
-            cpu = {"value": r / TOTAL, "unit": UNIT, "cores": cores, "kind": "port",
-                   "sample": f"{sample} random c2 summands, gradient + HVP per summand (oracle/gf_oracle.c, "
-                             f"restating reference objective.py:322-337, 432-482) on {cores} threads, phi0 "
-                             f"precomputed; extrapolated to the full 2^16 sum",
+            t1, t2, lid = circ.slot_arrays()
+            oplan = O.Plan(K_QUBITS, np.stack([t1, t2], 1), lid, circ.gate_stack())
+            dt, _ = port_grad_hvp(oplan, X, js, ph, cores)
+            cpu = {"value": REF_SAMPLE / dt, "unit": UNIT, "cores": cores, "kind": "port",
+                   "sample": f"{REF_SAMPLE} seeded c2 summands, gradient + HVP each (oracle/gf_oracle.c, restating "
+                             f"reference objective.py:322-337, 432-482) on {cores} threads, phi0 precomputed",
                    "gate_apply": cpu_gate_apply()}
 
     if rank == 0:
@@ -476,15 +628,13 @@ def run_b200(args):
             "dtype": "c128",
             "data": "synthetic: BASELINE configs[1] circuit (spinful FH L=8 open, 5 layers, Haar seed 1); target "
                     "columns conj(exp(-iHt)|j>) (J=1, U=4, t=0.25) computed on device by the %s oracle" % args.oracle,
-            "config": {
-                "workload": "c2: L=8 spinful Fermi-Hubbard, 16 qubits, 36 slots / 5 logical gates; one step = value"
-                            " + Riemannian gradient + one HVP summed over all 65536 basis states",
-                "summands": TOTAL, "batch": batch, "chunk": chunk, "parallelism": f"basis-sum dp{world}",
-                "l2": "inputs larger than L2 (phi0 cache %d MiB per GPU; workspace 3 x batch x 1 MiB)" %
-                      ((p1 - p0) * N * 16 >> 20),
-                "oracle_setup_s": round(oracle_setup_s, 3),
-                "engine": plan_shape,
-            },
+            "config": CONFIG,
+            "step": f"one full-sum evaluation: {summands} summands (value + gradient + HVP each), batch {batch}, "
+                    f"chunk {chunk}, sharded over {world} rank(s) ({args.backend})",
+            "full_sum_evals_per_s": value / TOTAL,
+            "engine": dict(plan_shape, batch=batch, chunk=chunk, oracle_setup_s=round(oracle_setup_s, 3),
+                           l2="inputs larger than L2 (phi0 cache %d MiB per GPU; workspace 3 x batch x 1 MiB)" %
+                              ((p1 - p0) * N * 16 >> 20)),
             "roofline": {"bound": "tensor", "kernel": f"k_fused ({dom} sweep: fused tile passes, FP64 DMMA)",
                          "achieved": achieved, "peak": peaks64["dmma_tflops"], "unit": "TFLOP/s",
                          "frac": round(achieved / peaks64["dmma_tflops"], 4), "traffic": traffic,
@@ -500,11 +650,13 @@ def run_b200(args):
                                               "HBM-bound; the standalone gate apply is (gate_apply)"}},
             "phases": phases,
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(rec_bytes),
+                    "full_sum_evals_per_s": e2e_val / TOTAL,
                     "path": "gf.gradient_and_hvp(circuit, %s(spec, t), directions), oracle constructed per step: every "
                             "target column regenerated on device each evaluation" % type(oracle).__name__},
             "gpu_launches": launches_all,
             "clocks": clocks,
             "gate_apply": gate_sweep,
+            "c5": c5,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
@@ -519,15 +671,20 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N > 1 (gloo: CPU test of the multi-rank path on one GPU)")
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--oracle", default="blocks", choices=["blocks", "chebyshev"],
                     help="target oracle: number-block Chebyshev (default) or full-space Chebyshev")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-c5", action="store_true")
     ap.add_argument("--summands", type=int, default=None,
                     help="profiling only: restrict each step to the first S basis states")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_self_launch(args))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -54,6 +54,13 @@ int gf_abi_version(void);
 int gf_apply_gate(const void *in, void *out, int k, int t1, int t2, const double *mat, int parity_sparse,
                   int64_t nvec, void *stream);
 
+/* out = g in for a one-qubit gate g (host pointer to 4 complex = 8 doubles,
+ * row-major 2x2) on qubit q of every vector (out may equal in).  North-star
+ * item (1); the reference absorbs one-qubit gates into its two-qubit gates
+ * (SPEC.md:102), so the oracle is reference apply_gate with kron(g, I)
+ * (kernels.py:484-515).  Same 256-bit streaming paths as gf_apply_gate. */
+int gf_apply_gate_1q(const void *in, void *out, int k, int q, const double *mat, int64_t nvec, void *stream);
+
 /* Parity-controlled one-qubit gate of the parity-sector compressed space
  * (no reference counterpart): a 4x4 parity-conserving gate
  * on full-space qubits (a, k_full-1) acting on the compressed vector of

@@ -16,8 +16,11 @@
  * fixtures produced by the unmodified reference (tests/golden/make_golden.py).
  */
 #include <complex.h>
+#include <pthread.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
+#include <unistd.h>
 
 typedef double complex cplx;
 typedef int64_t i64;
@@ -395,6 +398,250 @@ void or_hamiltonian_apply(int k, const i64 *ta, const i64 *tb, const double *coe
             } else if (ba && bb) {
                 out[x] += coef[t] * psi[x];
             }
+        }
+    }
+}
+
+/* ======================================================================
+ * Large-k oracle: for k >= 20 the reference's drivers
+ * cache 2(n+1) vectors (c3: 162 x 256 MiB), which does not fit the host.
+ * The same recursions (objective.py:307-337 gradient, objective.py:432-482
+ * HVP) are run here in the reversible 3-vector schedule instead, built only
+ * from the restated numba cores (kernels.py:168-188 gate application,
+ * kernels.py:208-242 hole contraction), OpenMP-parallel over tuples:
+ *   forward     psi_{l+1} = G_l psi_l                      objective.py:310-313
+ *   descending  psi_s = G_s^dag psi_{s+1} (uncompute), bra_s = phis[n-s-1],
+ *               D_s = hole(bra_s, psi_s), H_s += hole(chi_s, psi_s),
+ *               chi_{s-1} = G_s^T chi_s + Z_s^T bra_s, bra_{s-1} = G_s^T bra_s
+ *   ascending   bra_s = conj(G_s) bra_{s-1} (recover), H_s += hole(bra_s, v_s),
+ *               v_{s+1} = G_s v_s + Z_s psi_s, psi_{s+1} = G_s psi_s
+ * It needs unitary gates (every trust-region iterate is).  Pinned against the
+ * reference's cached-pass drivers through the c1 / c2-slice fixtures
+ * (tests/test_oracle.py) before it is used at c3 size.
+ * ====================================================================== */
+
+/* Fixed partition of [0, total) into PAR_BLOCKS blocks run on the host
+ * threads (pthreads; OR_THREADS overrides the online core count).  Block b
+ * always covers the same tuples, so per-block partial sums combined in
+ * block order are deterministic for any thread count. */
+#define PAR_BLOCKS 256
+typedef void (*block_fn)(void *ctx, i64 lo, i64 hi, int blk);
+typedef struct {
+    block_fn fn;
+    void *ctx;
+    i64 total, per;
+    int first, stride;
+} par_job;
+
+static int or_threads(void)
+{
+    const char *e = getenv("OR_THREADS");
+    long n = e ? atol(e) : sysconf(_SC_NPROCESSORS_ONLN);
+    return (int)(n < 1 ? 1 : (n > PAR_BLOCKS ? PAR_BLOCKS : n));
+}
+
+static void *par_worker(void *arg)
+{
+    const par_job *j = (const par_job *)arg;
+    for (int b = j->first; b < PAR_BLOCKS; b += j->stride) {
+        const i64 lo = (i64)b * j->per, hi = lo + j->per < j->total ? lo + j->per : j->total;
+        if (lo < hi) j->fn(j->ctx, lo, hi, b);
+    }
+    return NULL;
+}
+
+static void par_for(i64 total, block_fn fn, void *ctx)
+{
+    const int nt = or_threads();
+    par_job jobs[PAR_BLOCKS];
+    pthread_t th[PAR_BLOCKS];
+    const i64 per = (total + PAR_BLOCKS - 1) / PAR_BLOCKS;
+    for (int t = 0; t < nt; ++t) {
+        jobs[t] = (par_job){fn, ctx, total, per, t, nt};
+        if (t > 0) pthread_create(&th[t], NULL, par_worker, &jobs[t]);
+    }
+    par_worker(&jobs[0]);
+    for (int t = 1; t < nt; ++t) pthread_join(th[t], NULL);
+}
+
+typedef struct {
+    const cplx *x, *g, *y, *z;
+    cplx *out;
+    i64 q, n;
+    int sparse;
+    cplx (*part)[16];
+} par_ctx;
+
+/* gate application kernels.py:168-188 over a flat tuple index; in place
+ * allowed (each tuple is read completely before it is written). */
+static void apply_blk(void *c, i64 lo, i64 hi, int blk)
+{
+    const par_ctx *a = (const par_ctx *)c;
+    const i64 q = a->q, n = a->n;
+    const cplx *g = a->g;
+    (void)blk;
+    for (i64 t = lo; t < hi; ++t) {
+        const i64 i4 = t % n, i2 = (t / n) % q, i0 = t / (n * q);
+        const i64 b0 = ((i0 * 2) * q + i2) * 2 * n + i4;
+        const i64 b1 = ((i0 * 2 + 1) * q + i2) * 2 * n + i4;
+        const cplx x0 = a->x[b0], x1 = a->x[b0 + n], x2 = a->x[b1], x3 = a->x[b1 + n];
+        if (a->sparse) {
+            a->out[b0] = g[0] * x0 + g[3] * x3;
+            a->out[b0 + n] = g[5] * x1 + g[6] * x2;
+            a->out[b1] = g[9] * x1 + g[10] * x2;
+            a->out[b1 + n] = g[12] * x0 + g[15] * x3;
+        } else {
+            a->out[b0] = g[0] * x0 + g[1] * x1 + g[2] * x2 + g[3] * x3;
+            a->out[b0 + n] = g[4] * x0 + g[5] * x1 + g[6] * x2 + g[7] * x3;
+            a->out[b1] = g[8] * x0 + g[9] * x1 + g[10] * x2 + g[11] * x3;
+            a->out[b1 + n] = g[12] * x0 + g[13] * x1 + g[14] * x2 + g[15] * x3;
+        }
+    }
+}
+
+static void par_apply(cplx *psi, const cplx *g, i64 p, i64 q, i64 n, int sparse, cplx *out)
+{
+    par_ctx c = {psi, g, NULL, NULL, out, q, n, sparse, NULL};
+    par_for(p * q * n, apply_blk, &c);
+}
+
+/* out = G x + Z y (one pass; the v / chi update of the HVP recursions) */
+static void apply2_blk(void *c, i64 lo, i64 hi, int blk)
+{
+    const par_ctx *a = (const par_ctx *)c;
+    const i64 q = a->q, n = a->n;
+    (void)blk;
+    for (i64 t = lo; t < hi; ++t) {
+        const i64 i4 = t % n, i2 = (t / n) % q, i0 = t / (n * q);
+        const i64 b0 = ((i0 * 2) * q + i2) * 2 * n + i4;
+        const i64 b1 = ((i0 * 2 + 1) * q + i2) * 2 * n + i4;
+        const i64 r[4] = {b0, b0 + n, b1, b1 + n};
+        cplx xs[4], ys[4];
+        for (int i = 0; i < 4; ++i) {
+            xs[i] = a->x[r[i]];
+            ys[i] = a->y[r[i]];
+        }
+        for (int i = 0; i < 4; ++i) {
+            cplx s = 0;
+            for (int j = 0; j < 4; ++j) s += a->g[4 * i + j] * xs[j] + a->z[4 * i + j] * ys[j];
+            a->out[r[i]] = s;
+        }
+    }
+}
+
+static void par_apply2(const cplx *x, const cplx *g, const cplx *y, const cplx *z, i64 p, i64 q, i64 n, cplx *out)
+{
+    par_ctx c = {x, g, y, z, out, q, n, 0, NULL};
+    par_for(p * q * n, apply2_blk, &c);
+}
+
+/* hole contraction kernels.py:208-242; per-block partials summed in block order */
+static void hole_blk(void *c, i64 lo, i64 hi, int blk)
+{
+    const par_ctx *a = (const par_ctx *)c;
+    const i64 q = a->q, n = a->n;
+    cplx d[16];
+    for (int e = 0; e < 16; ++e) d[e] = 0;
+    for (i64 t = lo; t < hi; ++t) {
+        const i64 i4 = t % n, i2 = (t / n) % q, i0 = t / (n * q);
+        const i64 b0 = ((i0 * 2) * q + i2) * 2 * n + i4;
+        const i64 b1 = ((i0 * 2 + 1) * q + i2) * 2 * n + i4;
+        const i64 r[4] = {b0, b0 + n, b1, b1 + n};
+        for (int i = 0; i < 4; ++i) {
+            const cplx y = a->x[r[i]];
+            for (int j = 0; j < 4; ++j) d[4 * i + j] += y * a->y[r[j]];
+        }
+    }
+    memcpy(a->part[blk], d, sizeof d);
+}
+
+static void par_hole(const cplx *bra, const cplx *ket, i64 p, i64 q, i64 n, cplx *out)
+{
+    cplx part[PAR_BLOCKS][16];
+    memset(part, 0, sizeof part);
+    par_ctx c = {bra, NULL, ket, NULL, NULL, q, n, 0, part};
+    par_for(p * q * n, hole_blk, &c);
+    cplx d[16];
+    for (int e = 0; e < 16; ++e) d[e] = 0;
+    for (int b = 0; b < PAR_BLOCKS; ++b)
+        for (int e = 0; e < 16; ++e) d[e] += part[b][e];
+    memcpy(out, d, sizeof d);
+}
+
+static void dot_blk(void *c, i64 lo, i64 hi, int blk)
+{
+    const par_ctx *a = (const par_ctx *)c;
+    cplx s = 0;
+    for (i64 i = lo; i < hi; ++i) s += a->x[i] * a->y[i];
+    a->part[blk][0] = s;
+}
+
+static cplx par_dot(const cplx *x, const cplx *y, i64 N)
+{
+    cplx part[PAR_BLOCKS][16];
+    memset(part, 0, sizeof part);
+    par_ctx c = {x, NULL, y, NULL, NULL, 1, 1, 0, part};
+    par_for(N, dot_blk, &c);
+    cplx s = 0;
+    for (int b = 0; b < PAR_BLOCKS; ++b) s += part[b][0];
+    return s;
+}
+
+static void conj_t(const cplx *m, cplx *dag, cplx *cj)
+{
+    for (int i = 0; i < 4; ++i)
+        for (int j = 0; j < 4; ++j) {
+            dag[4 * i + j] = conj(m[4 * j + i]);
+            cj[4 * i + j] = conj(m[4 * i + j]);
+        }
+}
+
+/* One summand j: value phi0 . C|j>, gradient holes dacc[n][16] and HVP holes
+ * oacc[n][16] (both accumulated), reference orientation (normalised wires).
+ * psi, bra, aux, tmp: four scratch vectors of 2^k amplitudes. */
+void or_grad_hvp_reversible(const or_plan *P, const cplx *zmats, const cplx *zmats_t, i64 j, const cplx *phi0,
+                            cplx *psi, cplx *bra, cplx *aux, cplx *tmp, cplx *dacc, cplx *oacc, cplx *value)
+{
+    const i64 N = (i64)1 << P->k, n = P->nslots;
+    cplx d16[16], gd[16], gc[16];
+    memset(psi, 0, sizeof(cplx) * N);
+    psi[j] = 1.0;
+    for (i64 l = 0; l < n; ++l) par_apply(psi, P->mats + 16 * l, P->ps[l], P->qs[l], P->ns[l], P->sparse[l], psi);
+    *value = par_dot(phi0, psi, N);
+    memcpy(bra, phi0, sizeof(cplx) * N);
+    memset(aux, 0, sizeof(cplx) * N); /* chi_{n-1} = 0 */
+    for (i64 s = n - 1; s >= 0; --s) {
+        const i64 p = P->ps[s], q = P->qs[s], nn = P->ns[s];
+        const int sp = P->sparse[s];
+        conj_t(P->mats + 16 * s, gd, gc);
+        par_apply(psi, gd, p, q, nn, sp, psi); /* psi_s */
+        par_hole(bra, psi, p, q, nn, d16);
+        for (int e = 0; e < 16; ++e) dacc[16 * s + e] += d16[e];
+        if (s < n - 1) {
+            par_hole(aux, psi, p, q, nn, d16);
+            for (int e = 0; e < 16; ++e) oacc[16 * s + e] += d16[e];
+        }
+        if (s > 0) {
+            par_apply2(aux, P->mats_t + 16 * s, bra, zmats_t + 16 * s, p, q, nn, tmp); /* chi_{s-1} */
+            cplx *sw = aux; aux = tmp; tmp = sw;
+        }
+        par_apply(bra, P->mats_t + 16 * s, p, q, nn, sp, bra);
+    }
+    /* psi = |j>, bra = phis[n]; ascending */
+    memset(aux, 0, sizeof(cplx) * N); /* v_0 = 0 */
+    for (i64 s = 0; s < n; ++s) {
+        const i64 p = P->ps[s], q = P->qs[s], nn = P->ns[s];
+        const int sp = P->sparse[s];
+        conj_t(P->mats + 16 * s, gd, gc);
+        par_apply(bra, gc, p, q, nn, sp, bra); /* phis[n-s-1] */
+        if (s >= 1) {
+            par_hole(bra, aux, p, q, nn, d16);
+            for (int e = 0; e < 16; ++e) oacc[16 * s + e] += d16[e];
+        }
+        if (s < n - 1) {
+            par_apply2(aux, P->mats + 16 * s, psi, zmats + 16 * s, p, q, nn, tmp); /* v_{s+1} */
+            cplx *sw = aux; aux = tmp; tmp = sw;
+            par_apply(psi, P->mats + 16 * s, p, q, nn, sp, psi);
         }
     }
 }

@@ -367,6 +367,26 @@ def hessian_sum(plan, js, phi0_fn, classes=None, workers=1):
     return v, dacc, {(a, b): blocks[r] for a, b, r in keys}, counts
 
 
+def grad_hvp_reversible(plan, directions, j, phi0_row):
+    """One summand j: (value, per-slot D [n,16], per-slot HVP [n,16]) of the
+    reference recursions (objective.py:307-337, 432-482) run in the reversible
+    3-vector schedule from the restated cores (oracle/gf_oracle.c
+    or_grad_hvp_reversible) -- the large-k oracle (SURVEY 8(c) item 4);
+    host-parallel over tuples, 4 scratch vectors instead of 2(n+1)."""
+    N, n = 2**plan.k, plan.n
+    zm, zt = plan.zmats(directions)
+    phi = _c(phi0_row)
+    if phi.shape != (N,):
+        raise ValueError("phi0 row must have 2**k amplitudes")
+    bufs = [np.empty(N, np.complex128) for _ in range(4)]
+    dacc = np.zeros((n, 16), np.complex128)
+    oacc = np.zeros((n, 16), np.complex128)
+    v = np.zeros(1, np.complex128)
+    _lib.or_grad_hvp_reversible(ctypes.byref(plan._c), _ptr(zm), _ptr(zt), _I(int(j)), _ptr(phi),
+                                *[_ptr(b) for b in bufs], _ptr(dacc), _ptr(oacc), _ptr(v))
+    return v[0], dacc, oacc
+
+
 # ---------------------------------------------------------------- models / targets
 
 

@@ -20,6 +20,7 @@ EXPORTS = (
     "gf_last_error",
     "gf_abi_version",
     "gf_apply_gate",
+    "gf_apply_gate_1q",
     "gf_apply_gate_sector_c1q",
     "gf_hole_contract",
     "gf_hole_apply",
@@ -74,6 +75,7 @@ lib.gf_plan_last_launches.argtypes = [_vp]
 for _name, _args in {
     "gf_apply_gate": [_vp, _vp, _i, _i, _i, _vp, _i, _i64, _vp],
     "gf_apply_gate_sector_c1q": [_vp, _vp, _i, _i, _i, _vp, _i64, _vp],
+    "gf_apply_gate_1q": [_vp, _vp, _i, _i, _vp, _i64, _vp],
     "gf_hole_contract": [_vp, _vp, _i, _i, _i, _i64, _vp, _vp],
     "gf_hole_apply": [_vp, _vp, _i, _i, _i, _vp, _i, _vp],
     "gf_apply_gate_to_array": [_vp, _vp, _i, _i, _i, _i, _vp, _i, _vp],

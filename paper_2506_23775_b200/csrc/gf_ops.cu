@@ -615,6 +615,38 @@ extern "C" int gf_apply_gate_sector_c1q(const void *in, void *out, int k_full, i
     return GF_OK;
 }
 
+// Generic one-qubit gate (north-star item 1).  The reference absorbs 1q gates
+// into its 2q gates; the engine-side kernels are the
+// parity-controlled 1q kernels with both 2x2 blocks set to the same matrix,
+// so every amplitude pair gets g whatever its parity (same 256-bit paths).
+extern "C" int gf_apply_gate_1q(const void *in, void *out, int k, int q, const double *mat, int64_t nvec,
+                                void *stream)
+{
+    if (!in || !out || !mat) return gf_fail(GF_EINVAL, "null argument");
+    if (k < 1 || k > 40 || nvec < 1) return gf_fail(GF_EINVAL, "bad sizes");
+    if (q < 0 || q >= k) return gf_fail(GF_EINVAL, "target %d out of range for %d qubits", q, k);
+    Mat4 g;
+    for (int e = 0; e < 16; ++e) g.m[e] = make_double2(0.0, 0.0);
+    const double2 a = make_double2(mat[0], mat[1]), b = make_double2(mat[2], mat[3]);
+    const double2 c = make_double2(mat[4], mat[5]), d = make_double2(mat[6], mat[7]);
+    g.m[0] = a; g.m[3] = b; g.m[12] = c; g.m[15] = d;   // parity-0 block
+    g.m[5] = a; g.m[6] = b; g.m[9] = c; g.m[10] = d;    // parity-1 block
+    const int pa = k - 1 - q;
+    const unsigned long long total = (1ull << (k - 1)) * (unsigned long long)nvec;
+    const int grid = grid_for(total, 256 * 2, 148 * 32);
+    cudaStream_t st = (cudaStream_t)stream;
+    const bool a32 = ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 31u) == 0;
+    if (pa == 0 && a32)
+        k_apply_c1q_lo0<2><<<grid, 256, 0, st>>>((const double2 *)in, (double2 *)out, k, total, 0, g);
+    else if (a32 && k >= 2 && total >= 2)
+        k_apply_c1q_x2<2><<<grid_for(total / 2, 256 * 2, 148 * 32), 256, 0, st>>>(
+            (const double2 *)in, (double2 *)out, k, total / 2, pa, 0, g);
+    else
+        k_apply_c1q<2><<<grid, 256, 0, st>>>((const double2 *)in, (double2 *)out, k, total, pa, 0, g);
+    GF_CUDA(cudaGetLastError());
+    return GF_OK;
+}
+
 extern "C" int gf_hole_contract(const void *bra, const void *ket, int k, int t1, int t2, int64_t nvec, void *out_dev,
                                 void *stream)
 {

@@ -36,6 +36,7 @@ __all__ = [
     "apply_gate_to_array",
     "hole_contract_array",
     "apply_sector_c1q",
+    "apply_gate_1q",
 ]
 
 #: wire exchange permutation of a 4x4 gate's rows / columns (kernels.py:49-50)
@@ -164,6 +165,20 @@ def apply_gate(state, gate: Gate, out=None, variant: str = "kernel"):
         else:
             out[...] = res.cpu().numpy()
         return out
+    return _finish(res, host)
+
+
+def apply_gate_1q(state, matrix, qubit: int):
+    """``g state`` for a 2x2 gate on one qubit (north-star item 1; the
+    reference embeds 1q gates in its 2q gates)."""
+    s, host = _stage(state, 1)
+    k = num_qubits(s)
+    g = np.ascontiguousarray(matrix, dtype=np.complex128)
+    if g.shape != (2, 2):
+        raise ValueError(f"one-qubit gate must be 2x2, got {g.shape}")
+    res = torch.empty_like(s)
+    _lib.check(_lib.lib.gf_apply_gate_1q(s.data_ptr(), res.data_ptr(), k, int(qubit), g.ctypes.data, 1,
+                                         _lib.stream_ptr()))
     return _finish(res, host)
 
 

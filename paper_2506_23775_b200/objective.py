@@ -408,8 +408,10 @@ def gather_records(local: torch.Tensor, lo: int, nchunks: int, rank: int, world:
         return local
     counts = [shard_chunks(nchunks, r, world) for r in range(world)]
     width = max(h - l for l, h in counts)
-    pad = torch.zeros((width, local.shape[1]), dtype=local.dtype, device=local.device)
-    pad[: local.shape[0]] = local
+    # NCCL gathers device tensors; gloo (CPU tests, one-GPU boxes) gathers host copies
+    dev = local.device if dist.get_backend() == "nccl" else torch.device("cpu")
+    pad = torch.zeros((width, local.shape[1]), dtype=local.dtype, device=dev)
+    pad[: local.shape[0]] = local.to(dev)
     bufs = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather(bufs, pad)
     return torch.cat([b[: h - l] for b, (l, h) in zip(bufs, counts)], dim=0)

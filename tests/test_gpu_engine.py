@@ -162,6 +162,37 @@ def test_c1q_sector_gate_matches_full_space():
             assert rel_err(got2, want2) < 1e-14
 
 
+@pytest.mark.parametrize("k", [1, 2, 5, 17])
+def test_apply_gate_1q_every_qubit_vs_oracle(k):
+    """Generic one-qubit gate on every qubit against the oracle's restatement
+    of reference apply_gate with kron(g, I) (the reference embeds 1q gates in
+    its 2q gates), and batched / in-place through the ABI."""
+    rng = np.random.default_rng(40 + k)
+    psi = rng.normal(size=2**k) + 1j * rng.normal(size=2**k)
+    for q in range(k):
+        g = manifold.random_unitary(2, rng)
+        got = K.apply_gate_1q(psi, g, q)
+        if k == 1:
+            want = g @ psi
+        else:
+            other = q + 1 if q + 1 < k else q - 1
+            pair = (q, other)
+            want = O.apply_gate(psi, np.kron(g, np.eye(2)), pair)
+        assert rel_err(got, want) < 1e-14
+    # batched, in place, on the device
+    x = torch.from_numpy(np.stack([psi, 2 * psi])).cuda()
+    g = manifold.random_unitary(2, rng)
+    gg = np.ascontiguousarray(g)
+    gf._lib.check(gf._lib.lib.gf_apply_gate_1q(x.data_ptr(), x.data_ptr(), k, 0, gg.ctypes.data, 2,
+                                               gf._lib.stream_ptr()))
+    want = K.apply_gate_1q(psi, g, 0)
+    assert rel_err(x[1].cpu().numpy(), 2 * want) < 1e-14 and rel_err(x[0].cpu().numpy(), want) < 1e-14
+    with pytest.raises(ValueError):
+        K.apply_gate_1q(psi, g, k)
+    with pytest.raises(ValueError):
+        K.apply_gate_1q(psi, np.eye(4), 0)
+
+
 def test_apply_gate_on_16_byte_aligned_views():
     """K1 moves aligned amplitude pairs with 256-bit accesses; a tensor view at
     an odd amplitude offset (16 B aligned only) must take the 128-bit path and

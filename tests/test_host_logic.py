@@ -9,7 +9,7 @@ import math
 import numpy as np
 import pytest
 
-from conftest import golden, rel_err
+from conftest import ROOT, golden, rel_err
 from paper_2506_23775_b200 import circuit as C
 from paper_2506_23775_b200 import manifold as M
 from paper_2506_23775_b200 import models, objective, optimizer
@@ -147,3 +147,34 @@ def test_shard_chunks_cover_exactly():
             spans = [objective.shard_chunks(nchunks, r, world) for r in range(world)]
             assert spans[0][0] == 0 and spans[-1][1] == nchunks
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+
+
+def test_bench_reference_arm_uses_the_same_c2_workload():
+    """bench.py --impl reference reads the circuit and direction from the
+    reference-written c2_slice fixture (it must not import the product); they
+    must equal the B200 arm's recipe bit for bit (same config in both arms)."""
+    import bench
+
+    gf, spec, circ, X = bench.workload()
+    g = golden("c2_slice")
+    t1, t2, lid = circ.slot_arrays()
+    assert np.array_equal(np.stack([t1, t2], 1), g["targets"])
+    assert np.array_equal(lid, g["logical"])
+    assert np.array_equal(circ.gate_stack(), g["gates"])
+    assert np.array_equal(np.stack(X), g["direction"])
+    assert int(g["k"]) == bench.K_QUBITS
+
+
+def test_bench_reference_arm_does_not_import_the_product(tmp_path):
+    """The reference arm runs the oracle port only: no paper_2506_23775_b200
+    module (and so no libgfcuda.so) may be loaded by it."""
+    import subprocess
+    import sys
+
+    code = ("import sys, runpy; sys.argv=['bench.py','--impl','reference','--steps','1','--warmup','0'];"
+            "import bench; bench.REF_SAMPLE=4; bench.run_reference(bench.argparse.Namespace(gpus=1, steps=1, "
+            "warmup=0)); assert not any(m.startswith('paper_2506_23775_b200') for m in sys.modules), "
+            "[m for m in sys.modules if m.startswith('paper')]; print('ok')")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=ROOT, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert r.stdout.strip().endswith("ok")

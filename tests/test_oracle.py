@@ -192,3 +192,39 @@ def test_c2_slice_lanczos_and_gradient():
     plan = O.Plan(k, g["targets"], g["logical"], g["gates"])
     v, d, _ = O.gradient_sum(plan, js[:4], lambda jj: P[np.searchsorted(js[:4], jj)])
     assert abs(v - g["values"][:4].sum()) < 1e-10
+
+
+def test_reversible_schedule_matches_reference_c1_full_sum():
+    """The large-k oracle (reversible 3-vector schedule) against the
+    reference's cached-pass drivers: c1 value / gradient / HVP over all 256
+    summands."""
+    g, U = _c1()
+    plan = O.Plan(8, g["targets"], g["logical"], g["gates"])
+    phi = O.dense_phi0(U)
+    v = 0j
+    d = np.zeros((plan.n, 16), complex)
+    h = np.zeros((plan.n, 16), complex)
+    for j in range(256):
+        vj, dj, hj = O.grad_hvp_reversible(plan, list(g["direction"]), j, phi([j])[0])
+        v, d, h = v + vj, d + dj, h + hj
+    assert abs(-v.real - g["value"]) < 1e-12 * abs(g["value"])
+    assert rel_err(plan.logical_sum(d), g["holo"]) < 1e-12
+    assert rel_err(plan.logical_sum(h), g["hvp"]) < 1e-12
+
+
+def test_reversible_schedule_matches_reference_c2_slice():
+    """... and on the 16-summand c2 slice the reference drivers produced with
+    Krylov targets (phi0 from the Lanczos restatement)."""
+    g = golden("c2_slice")
+    terms, _ = O.spinful_terms(8, 1.0, 4.0, False)
+    js = g["js"]
+    P = O.lanczos_phi0(16, terms, 0.25)(js)
+    plan = O.Plan(16, g["targets"], g["logical"], g["gates"])
+    d = np.zeros((plan.n, 16), complex)
+    h = np.zeros((plan.n, 16), complex)
+    for i, j in enumerate(js):
+        vj, dj, hj = O.grad_hvp_reversible(plan, list(g["direction"]), j, P[i])
+        assert abs(vj - g["values"][i]) < 1e-10
+        d, h = d + dj, h + hj
+    assert rel_err(plan.logical_sum(d), g["holo"]) < 1e-10
+    assert rel_err(plan.logical_sum(h), g["hvp"]) < 1e-10
