@@ -178,6 +178,50 @@ int gf_plan_layout(int k, int sector, int n_slots, const int32_t *t1, const int3
 int gf_plan_destroy(gf_plan *plan);
 
 /* ------------------------------------------------------------------ *
+ * Hessian chunk driver: the reference's _hessian_chunk (objective.py:340-423)
+ * with its pair CSR (_pair_csr, objective.py:209-247), as consumed by
+ * full_hessian's chunk closure (objective.py:729-744).  Full space only (the
+ * reference's semantics); cached passes [n+1] x batch x 2^k per direction.
+ * ------------------------------------------------------------------ */
+typedef struct gf_hess_plan gf_hess_plan;
+
+/* Slots as gf_plan_create.  support[arity]: flat entries 4*i+j of the hole
+ * support in logical orientation (16 = DENSE_SUPPORT, 8 = PARITY_SUPPORT,
+ * kernels.py:52-58); swapped slots use the remapped support
+ * (kernels.py:568-571) internally.  The pair CSR is exactly the reference's
+ * _pair_csr output: first_list[nfirst] ascending, first_start[nfirst + 1],
+ * and per pair (first_start[nfirst] of them) pair_second (ascending within a
+ * first slot), pair_mult (translation-class size with dedup, else 1),
+ * pair_route (upper-triangular logical-pair index a*nlog - a(a-1)/2 + (b-a)),
+ * pair_sym (same logical gate), pair_flip (first slot's logical gate is the
+ * later one).  All host arrays, copied at creation. */
+int gf_hess_plan_create(gf_hess_plan **plan, int k, int n_slots, const int32_t *t1, const int32_t *t2,
+                        const int32_t *logical, int n_logical, const int64_t *support, int arity,
+                        const int64_t *first_list, int64_t nfirst, const int64_t *first_start,
+                        const int64_t *pair_second, const double *pair_mult, const int64_t *pair_route,
+                        const int32_t *pair_sym, const int32_t *pair_flip, int64_t max_batch, int chunk_states);
+/* Logical gates as gf_plan_set_gates; parity_mode != 0 applies parity-sparse
+ * slot matrices without their structural zeros (the reference _Plan's sparse
+ * flags, objective.py:188). */
+int gf_hess_plan_set_gates(gf_hess_plan *plan, const double *mats, int parity_mode);
+/* `nvec` summands (basis_dev int64 [nvec], weights_dev double [nvec] or NULL,
+ * phi0_dev complex [nvec][2^k]).  out_dev: double [ceil(nvec/chunk)][rec],
+ * rec = 2 + 32*n_logical + 2*R*arity*arity, R = n_logical(n_logical+1)/2:
+ *   value (complex), D[n_logical][4][4] (holomorphic, logical orientation),
+ *   block_acc[R][arity][arity] (complex, the reference's routed layout);
+ * each record the deterministic sum over its chunk.  out_counts: host
+ * int64[5] incremented with the reference's counters (objective.py:65-73):
+ * gate, array-gate, hole-apply, hole-contract and pair applications. */
+int gf_hess_plan_eval(gf_hess_plan *plan, int64_t nvec, const int64_t *basis_dev, const double *weights_dev,
+                      const void *phi0_dev, double *out_dev, int64_t *out_counts, void *stream);
+/* Per-slot gradient holes of the last eval summed over its nvec summands,
+ * [n_slots][4][4] complex in normalised wire orientation (device): the
+ * reference's per-chunk dacc (objective.py:329-336). */
+int gf_hess_plan_slot_outputs(gf_hess_plan *plan, int64_t nvec, double *d_dev, void *stream);
+int64_t gf_hess_plan_last_launches(const gf_hess_plan *plan);
+int gf_hess_plan_destroy(gf_hess_plan *plan);
+
+/* ------------------------------------------------------------------ *
  * Matrix-free target oracle (replaces the CPU
  * KrylovOracle / DenseOracle of reference models.py:305-393 as the
  * producer of phi0 = conj(exp(-iHt)|j>)).  Terms are two-site operators

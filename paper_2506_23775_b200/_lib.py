@@ -42,6 +42,12 @@ EXPORTS = (
     "gf_plan_describe",
     "gf_plan_layout",
     "gf_plan_destroy",
+    "gf_hess_plan_create",
+    "gf_hess_plan_set_gates",
+    "gf_hess_plan_eval",
+    "gf_hess_plan_slot_outputs",
+    "gf_hess_plan_last_launches",
+    "gf_hess_plan_destroy",
     "gf_cheb_step",
     "gf_hamiltonian_apply",
     "gf_nb_cheb_step",
@@ -72,6 +78,8 @@ lib.gf_last_error.restype = ctypes.c_char_p
 lib.gf_abi_version.restype = _i
 lib.gf_plan_last_launches.restype = _i64
 lib.gf_plan_last_launches.argtypes = [_vp]
+lib.gf_hess_plan_last_launches.restype = _i64
+lib.gf_hess_plan_last_launches.argtypes = [_vp]
 for _name, _args in {
     "gf_apply_gate": [_vp, _vp, _i, _i, _i, _vp, _i, _i64, _vp],
     "gf_apply_gate_sector_c1q": [_vp, _vp, _i, _i, _i, _vp, _i64, _vp],
@@ -91,6 +99,12 @@ for _name, _args in {
     "gf_plan_eval": [_vp, _i, _i64, _vp, _vp, _vp, _vp, _vp],
     "gf_plan_slot_outputs": [_vp, _i64, _vp, _vp, _vp],
     "gf_plan_destroy": [_vp],
+    "gf_hess_plan_create": [ctypes.POINTER(_vp), _i, _i, _vp, _vp, _vp, _i, _vp, _i, _vp, _i64, _vp, _vp, _vp, _vp,
+                            _vp, _vp, _i64, _i],
+    "gf_hess_plan_set_gates": [_vp, _vp, _i],
+    "gf_hess_plan_eval": [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp],
+    "gf_hess_plan_slot_outputs": [_vp, _i64, _vp, _vp],
+    "gf_hess_plan_destroy": [_vp],
     "gf_plan_describe": [_vp, _vp, _vp, _vp, _vp, _vp],
     "gf_plan_layout": [_i, _i, _i, _vp, _vp, _i, _i, _i, _vp, _vp, _vp, _vp],
     "gf_plan_set_profiling": [_vp, _i],

@@ -312,7 +312,7 @@ __device__ __forceinline__ double2 dmma_mv2(double2 x, double b0, double b1, dou
 template <int V>
 using IC = std::integral_constant<int, V>;
 
-template <int OP, int NT, int ND, bool SPX>
+template <int OP, int NT, int ND, int VAR>
 __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, double2 *t1, double2 *t2, double *scratch,
                                           const u64 pofs, const bool accum, const int tpop, const unsigned T)
 {
@@ -325,6 +325,11 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
     // fused gate + hole phase (dense slots): ascending sweep 3% faster; the
     // reverse sweep measured 0.5% slower with it and keeps the split phases
     constexpr bool GH = GF_FUSED_GH && (OP == OP_ASC_H);
+    // VAR bit 0: the pass has parity-sparse FMA slots; bit 1: it has
+    // parity-controlled one-qubit slots on the DMMA path (PM_C1QD).  Passes
+    // without them compile without those branches.
+    constexpr bool SPX = (VAR & 1) != 0;
+    constexpr bool C1D = (VAR & 2) != 0;
     constexpr int NH = 1 + ND;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, tq = lane & 3;
@@ -336,6 +341,12 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
         const Mat4 &MA = p.mat[si][0];
         const Mat4 &MB = p.mat[si][1];
         const bool c1q = (mode == PM_C1Q);
+        // PM_C1QD: the sector's parity-controlled 2x2 gate on local bit llo as
+        // a dense 4x4 on (virtual bit lhi, llo): tuples pair two amplitude
+        // pairs of opposite parity, the even-parity pair first (the sh bit of
+        // odd-parity tuples is flipped), and the slot matrices are
+        // V(M) = diag(M[{0,3}], M[{1,2}]) (plan side, upload_frags)
+        const bool c1d = C1D && (mode == PM_C1QD);
         const unsigned nunit = c1q ? (T >> 1) : (T >> 2);
         // units per active warp: multiple of 4 (hole MMA K) -- and of 8 for the
         // 2q tensor path (8-tuple groups, paired hole MMAs)
@@ -466,6 +477,15 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                 // tuple index x: F(wbase | t) = F(wbase) ^ F(t) for t < TW
                 const unsigned c0 = PS.col[0], c1 = PS.col[1], c2 = PS.col[2];
                 const unsigned offA = ((tq & 2) ? PS.sh : 0u) ^ ((tq & 1) ? PS.so : 0u);
+                // C1QD parity flips: tuple index x = warp * TW + 8 grp + g (gate /
+                // update layout) or warp * TW + 4 q + tq (hole layout); a tuple's
+                // even-parity pair is its low one, so odd tuples XOR sh
+                const unsigned wpar = c1d ? (unsigned)((tpop + __popc((unsigned)warp) + p.sector) & 1) : 0u;
+                const unsigned gparA = wpar ^ ((unsigned)__popc((unsigned)g) & 1u);
+                auto flipA = [&](unsigned grp) -> unsigned {  // address XOR of group grp (gate layout)
+                    if constexpr (!C1D) return 0u;
+                    return (c1d && ((gparA ^ (unsigned)__popc(grp)) & 1u)) ? PS.sh : 0u;
+                };
                 // gate layout: lane (g, tq) = amp tq of tuple g
                 const unsigned baseA = Fw ^ ((g & 1) ? c0 : 0u) ^ ((g & 2) ? c1 : 0u) ^ ((g & 4) ? c2 : 0u) ^ offA;
                 const unsigned ngrp = TW >> 3;                // groups of 8 tuples
@@ -515,7 +535,7 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
 #pragma unroll
                         for (int i = 0; i < 4; ++i) V[L[i]] = y[i];
                     }
-                } else if constexpr (GH) {
+                } else if (GH && !c1d) {
                     // ---- fused gate + holes.  The gate is C = G X with X's
                     // components as K: lane (g, tq) loads part tq&1 of amps
                     // (tq>>1) and (tq>>1)+2 of tuple g, and receives component g
@@ -623,7 +643,7 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
 #pragma unroll
                             for (unsigned u = 0; u < 8; ++u) {
                                 if (gb + u >= ngrp) break;  // ngrp < 8 only for tiny tiles
-                                const unsigned ad = ab ^ gcomb(u);
+                                const unsigned ad = ab ^ gcomb(u) ^ flipA(gb + u);
                                 V[ad] = dmma_mv(V[ad], fa0, fa1);
                             }
                         }
@@ -641,14 +661,14 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                             double2 xv[GB];
 #pragma unroll
                             for (unsigned u = 0; u < GB; ++u)
-                                if (u < nb) xv[u] = V[ab ^ gcomb(u)];
+                                if (u < nb) xv[u] = V[ab ^ gcomb(u) ^ flipA(gb + u)];
 #pragma unroll
                             for (unsigned u = 0; u < GB; ++u)
-                                if (u < nb) V[ab ^ gcomb(u)] = dmma_mv(xv[u], fa0, fa1);
+                                if (u < nb) V[ab ^ gcomb(u) ^ flipA(gb + u)] = dmma_mv(xv[u], fa0, fa1);
                         }
                     }
                 }
-                if constexpr (HD || HH) if (!GH || sparse) {
+                if constexpr (HD || HH) if (!GH || sparse || c1d) {
                     __syncwarp();
                     // hole layout: lane (g, tq) = component g (amp g>>1, part g&1) of tuple tq
                     const unsigned offH = ((gi & 2) ? PS.sh : 0u) ^ ((gi & 1) ? PS.so : 0u);
@@ -663,6 +683,12 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
 #pragma unroll
                     for (int d = 0; d < ND; ++d) eH0[d] = eH1[d] = 0.0;
                     const unsigned nq = TW >> 2;
+                    // C1QD: parity of tuple 4q + tq is hpar ^ popc(q); a1 = tuple q + 1 (q even)
+                    const unsigned hpar = wpar ^ ((unsigned)__popc((unsigned)tq) & 1u);
+                    auto flipH = [&](unsigned q) -> unsigned {
+                        if constexpr (!C1D) return 0u;
+                        return (c1d && ((hpar ^ (unsigned)__popc(q)) & 1u)) ? PS.sh : 0u;
+                    };
                     // AC: 1/0 = direction active/inactive known at compile time
                     // (ND == 1, hoisted out of the loop), 2 = test amask per d
                     auto hole_loop = [&](auto AC) {
@@ -676,8 +702,8 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                           for (unsigned u = 0; u < 8; u += 2) {
                             const unsigned q = qb + u;
                             if (q >= nq) break;  // nq < 8 only for tiny tiles
-                            const unsigned a0 = ab ^ ((u & 2u) ? colH[1] : 0u) ^ ((u & 4u) ? colH[2] : 0u);
-                            const unsigned a1 = a0 ^ colH[0];
+                            const unsigned a0 = ab ^ ((u & 2u) ? colH[1] : 0u) ^ ((u & 4u) ? colH[2] : 0u) ^ flipH(q);
+                            const unsigned a1 = a0 ^ colH[0] ^ flipH(q) ^ flipH(q + 1);
                             const unsigned o0 = 2 * a0, o1 = 2 * a1;
                             if constexpr (REV) {
                                 const double k0 = d0[o0], k1 = d0[o1];
@@ -720,7 +746,7 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                     }
                     __syncwarp();
                 }
-                if constexpr (GH) if (!sparse) __syncwarp();  // fused phase reads precede the updates' writes
+                if constexpr (GH) if (!sparse && !c1d) __syncwarp();  // fused phase reads precede the updates' writes
                 if constexpr (OP != OP_FWD && OP != OP_FWD_DOT) if (sparse) {
                     const unsigned Fl = Fw ^ Alane();
                     for (unsigned j = lane; j < TW; j += 32) {
@@ -793,7 +819,7 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
 #pragma unroll
                           for (unsigned u = 0; u < 8; ++u) {
                             if (gb + u >= ngrp) break;  // ngrp < 8 only for tiny tiles
-                            const unsigned ad = ab ^ gcomb(u);
+                            const unsigned ad = ab ^ gcomb(u) ^ flipA(gb + u);
                             const double2 x = REV ? t1[ad] : t0[ad];
                             if constexpr (CHI || OP == OP_ASC_H) {
 #pragma unroll
@@ -833,13 +859,25 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
             // scratch[s & 1] is next written at slot s + 2, after the barrier of
             // slot s + 1, which the reducing warps pass only after reducing.
             double *sbuf = scratch + (si & 1) * (NH * NW * 32);
+            // C1QD slots: virtual entry (i', j') is full-space entry (m(i'), m(j')),
+            // m = [0, 3, 1, 2]; cross-block entries (different environments) are
+            // the exactly-zero off-pattern entries of the full-space hole
+            const bool c1dh = C1D && (mode == PM_C1QD);
             auto fold_store = [&](int hole, double c0, double c1) {
                 const double o0 = __shfl_xor_sync(0xffffffffu, c0, 4);
                 const double o1 = __shfl_xor_sync(0xffffffffu, c1, 4);
                 if (!(g & 1)) {
-                    double *dst = sbuf + (hole * NW + warp) * 32 + ((g >> 1) * 4 + tq) * 2;
-                    dst[0] = c0 - o1;
-                    dst[1] = c1 + o0;
+                    const int iv = g >> 1, jv = tq;
+                    int e = iv * 4 + jv;
+                    bool keep = true;
+                    if (c1dh) {
+                        const int mi = (0x2130 >> (4 * iv)) & 3, mj = (0x2130 >> (4 * jv)) & 3;  // m = [0,3,1,2]
+                        e = mi * 4 + mj;
+                        keep = (iv >> 1) == (jv >> 1);
+                    }
+                    double *dst = sbuf + (hole * NW + warp) * 32 + e * 2;
+                    dst[0] = keep ? c0 - o1 : 0.0;
+                    dst[1] = keep ? c1 + o0 : 0.0;
                 }
             };
             if ((unsigned)warp < nwa) {
@@ -869,7 +907,7 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
     }
 }
 
-template <int OP, bool FIRST, int NT, int ND, bool SPX>
+template <int OP, bool FIRST, int NT, int ND, int VAR>
 __global__ void __launch_bounds__(NT, 512 / NT) k_fused(const FusedParams p)
 {
     constexpr int NW = NT / 32;  // warps per CTA
@@ -961,7 +999,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_fused(const FusedParams p)
         }
         __syncthreads();
 
-        run_slots<OP, NT, ND, SPX>(p, t0, t1, t2, scratch, ((u64)blockIdx.y * p.ctas + blockIdx.x) * 32,
+        run_slots<OP, NT, ND, VAR>(p, t0, t1, t2, scratch, ((u64)blockIdx.y * p.ctas + blockIdx.x) * 32,
                                    tile != blockIdx.x, tpop, T);
 
         const int sm = p.store_mask;
@@ -1145,6 +1183,7 @@ struct gf_plan {
     // fused tile engine
     bool fused = false;
     bool sparse_fma = true;  // parity-sparse slots as FMA (else dense DMMA with structural zeros)
+    bool c1q_dmma = true;    // parity-controlled 1q slots on the DMMA path (PM_C1QD) instead of FMA pairs
     int fm = 0, fc = 0;
     // geometry only (matrices filled per eval).  The ascending HVP sweep must
     // replay exactly the reverse slot order of the reverse sweep (the two HVP
@@ -1254,16 +1293,27 @@ static int upload_frags(gf_plan *p, cudaStream_t st)
         if (e != cudaSuccess) return gf_fail(GF_ENOMEM, "fragment table: %s", cudaGetErrorString(e));
     }
     p->h_frag.assign(rows * 32, make_double2(0.0, 0.0));
+    // C1QD slots: V(M) = diag(M[{0,3}], M[{1,2}]) in the virtual (partner bit,
+    // explicit bit) basis; V commutes with transpose / conjugation
+    auto vm = [&](int s, const Mat4 &M) {
+        if (!(p->c1q_dmma && p->slots[s].mode_c1q)) return M;
+        static const int m[4] = {0, 3, 1, 2};
+        Mat4 r;
+        for (int i = 0; i < 4; ++i)
+            for (int j = 0; j < 4; ++j)
+                r.m[4 * i + j] = ((i >> 1) == (j >> 1)) ? M.m[4 * m[i] + m[j]] : make_double2(0.0, 0.0);
+        return r;
+    };
     auto put = [&](int s, int kind, const std::vector<Mat4> &v) {
-        if ((size_t)s < v.size()) frag_rows(v[s], &p->h_frag[((size_t)s * NFK + kind) * 32]);
+        if ((size_t)s < v.size()) frag_rows(vm(s, v[s]), &p->h_frag[((size_t)s * NFK + kind) * 32]);
     };
     for (int s = 0; s < p->n; ++s) {
         put(s, FK_G, p->G);
         put(s, FK_GD, p->Gd);
         put(s, FK_GT, p->Gt);
         put(s, FK_GC, p->Gc);
-        if ((size_t)s < p->Gd.size()) frag_rows_A(p->Gd[s], &p->h_frag[((size_t)s * NFK + FK_GDA) * 32]);
-        if ((size_t)s < p->Gc.size()) frag_rows_A(p->Gc[s], &p->h_frag[((size_t)s * NFK + FK_GCA) * 32]);
+        if ((size_t)s < p->Gd.size()) frag_rows_A(vm(s, p->Gd[s]), &p->h_frag[((size_t)s * NFK + FK_GDA) * 32]);
+        if ((size_t)s < p->Gc.size()) frag_rows_A(vm(s, p->Gc[s]), &p->h_frag[((size_t)s * NFK + FK_GCA) * 32]);
         for (int d = 0; d < FMAXDIR; ++d) {
             put(s, FK_ZT + d, p->Ztm[d]);
             put(s, FK_Z + d, p->Zm[d]);
@@ -1302,6 +1352,7 @@ struct PlanKnobs {
     int fwm;           // GF_FWD_M: tile bits of the forward sweep (default fm)
     long long ctas;    // GF_FUSED_CTAS: CTAs per vector (default 148 x 8)
     bool sparse_dmma;  // GF_SPARSE_DMMA: parity-sparse slots on the DMMA path
+    bool c1q_dmma;     // GF_C1Q_DMMA: parity-controlled 1q slots on the DMMA path
 };
 
 static PlanKnobs plan_knobs(int K, int tile_bits)
@@ -1320,6 +1371,8 @@ static PlanKnobs plan_knobs(int K, int tile_bits)
     k.ctas = cenv ? std::max(1ll, atoll(cenv)) : 148ll * 8;  // all tiles, up to 8 per SM
     const char *sd = getenv("GF_SPARSE_DMMA");
     k.sparse_dmma = sd ? atoi(sd) != 0 : GF_SPARSE_DMMA_DEFAULT;
+    const char *cq = getenv("GF_C1Q_DMMA");
+    k.c1q_dmma = cq ? atoi(cq) != 0 : true;
     return k;
 }
 
@@ -1387,6 +1440,7 @@ extern "C" int gf_plan_create(gf_plan **out, int k, int sector, int n_slots, con
         p->fm = kn.fm;
         p->fc = kn.fc;
         p->sparse_fma = !kn.sparse_dmma;
+        p->c1q_dmma = kn.c1q_dmma;
         if (p->fused) {
             p->fwd_passes = plan_passes(p, false, kn.fwm);
             p->rev_passes = plan_passes(p, true, p->fm);
@@ -1747,11 +1801,19 @@ static std::vector<FusedParams> plan_passes(const gf_plan *p, bool reverse, int 
         for (int t = 0; t < fp.nslots; ++t) {
             const SlotInfo &si = p->slots[taken[t]];
             PassSlot ps;
+            memset(&ps, 0, sizeof ps);
             ps.slot = taken[t];
-            ps.mode = si.mode_c1q ? PM_C1Q : PM_DENSE;  // sparse decided per eval
+            ps.mode = si.mode_c1q ? (p->c1q_dmma ? PM_C1QD : PM_C1Q) : PM_DENSE;  // sparse decided per eval
             ps.llo = lidx[si.lo];
             ps.lhi = si.mode_c1q ? 0 : lidx[si.hi];
-            if (!si.mode_c1q) {
+            if (ps.mode == PM_C1QD) {
+                // virtual partner bit: any other local bit (the lowest one)
+                const int vb = ps.llo == 0 ? 1 : 0, a0 = std::min(ps.llo, vb), a1 = std::max(ps.llo, vb);
+                ps.lhi = vb;
+                for (int i = 0; i < FMAXM - 1; ++i) ps.col[i] = swz_host(ins0u_host(ins0u_host(1u << i, a0), a1));
+                ps.so = swz_host(1u << ps.llo);
+                ps.sh = swz_host(1u << vb);
+            } else if (!si.mode_c1q) {
                 for (int i = 0; i < FMAXM - 1; ++i)
                     ps.col[i] = swz_host(ins0u_host(ins0u_host(1u << i, ps.llo), ps.lhi));
                 ps.so = swz_host(1u << ps.llo);
@@ -1774,7 +1836,7 @@ static size_t fused_smem(int nv, int m, int c, int nw, int nd = 1)
            sizeof(unsigned long long) * ((size_t)1 << (m - c));
 }
 
-template <int OP, bool FIRST, int NT, int ND, bool SPX>
+template <int OP, bool FIRST, int NT, int ND, int VAR>
 static int launch_fused_nt(const gf_plan *p, FusedParams &fp, int64_t nvec, cudaStream_t st)
 {
     const int nv = (OP == OP_FWD || OP == OP_FWD_DOT) ? 1 : (OP == OP_REV_G ? 2 : 2 + ND);
@@ -1785,44 +1847,51 @@ static int launch_fused_nt(const gf_plan *p, FusedParams &fp, int64_t nvec, cuda
     if (cudaGetDevice(&dev) != cudaSuccess) return gf_fail(GF_ECUDA, "no current CUDA device");
     if (!((attr_done >> (dev & 63)) & 1ull)) {
         // 226 KB: the opt-in limit (227 KB) minus the kernel's static shared memory
-        cudaError_t ae = cudaFuncSetAttribute(k_fused<OP, FIRST, NT, ND, SPX>,
+        cudaError_t ae = cudaFuncSetAttribute(k_fused<OP, FIRST, NT, ND, VAR>,
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
         if (ae != cudaSuccess) return gf_fail(GF_ECUDA, "k_fused smem attribute: %s", cudaGetErrorString(ae));
         attr_done |= 1ull << (dev & 63);
     }
     if (smem > 226 * 1024) return gf_fail(GF_EINVAL, "fused tile needs %zu B of shared memory", smem);
     dim3 grid(fp.ctas, (unsigned)nvec);
-    k_fused<OP, FIRST, NT, ND, SPX><<<grid, NT, smem, st>>>(fp);
+    k_fused<OP, FIRST, NT, ND, VAR><<<grid, NT, smem, st>>>(fp);
     return GF_OK;
 }
 
 // 256 threads (2 CTAs/SM) for tiles up to 2^11; 512 threads (1 CTA/SM, same 16
 // warps per SM) for 2^12 tiles and for multi-direction HVP sweeps (2 + ND
 // vectors per tile)
-template <int OP, bool FIRST, bool SPX>
+template <int OP, bool FIRST, int VAR>
 static int launch_fused_sp(const gf_plan *p, FusedParams &fp, int64_t nvec, cudaStream_t st, int nd)
 {
     if constexpr (OP == OP_REV_GH || OP == OP_REV_H || OP == OP_ASC_H) {
         if (nd >= 2) {
             if (fp.m <= 10) {  // 2^10 tiles: 2 + ND vectors fit 2 CTAs/SM at 256 threads
-                if (nd == 2) return launch_fused_nt<OP, FIRST, 256, 2, SPX>(p, fp, nvec, st);
-                return launch_fused_nt<OP, FIRST, 256, 3, SPX>(p, fp, nvec, st);
+                if (nd == 2) return launch_fused_nt<OP, FIRST, 256, 2, VAR>(p, fp, nvec, st);
+                return launch_fused_nt<OP, FIRST, 256, 3, VAR>(p, fp, nvec, st);
             }
-            if (nd == 2) return launch_fused_nt<OP, FIRST, 512, 2, SPX>(p, fp, nvec, st);
-            return launch_fused_nt<OP, FIRST, 512, 3, SPX>(p, fp, nvec, st);
+            if (nd == 2) return launch_fused_nt<OP, FIRST, 512, 2, VAR>(p, fp, nvec, st);
+            return launch_fused_nt<OP, FIRST, 512, 3, VAR>(p, fp, nvec, st);
         }
     }
-    if (fp.m >= 12) return launch_fused_nt<OP, FIRST, 512, 1, SPX>(p, fp, nvec, st);
-    return launch_fused_nt<OP, FIRST, 256, 1, SPX>(p, fp, nvec, st);
+    if (fp.m >= 12) return launch_fused_nt<OP, FIRST, 512, 1, VAR>(p, fp, nvec, st);
+    return launch_fused_nt<OP, FIRST, 256, 1, VAR>(p, fp, nvec, st);
 }
 
 template <int OP, bool FIRST>
 static int launch_fused(const gf_plan *p, FusedParams &fp, int64_t nvec, cudaStream_t st, int nd = 1)
 {
-    bool spx = false;
-    for (int t = 0; t < fp.nslots; ++t) spx |= (fp.ps[t].mode == PM_SPARSE);
-    if (spx) return launch_fused_sp<OP, FIRST, true>(p, fp, nvec, st, nd);
-    return launch_fused_sp<OP, FIRST, false>(p, fp, nvec, st, nd);
+    bool spx = false, c1d = false;
+    for (int t = 0; t < fp.nslots; ++t) {
+        spx |= (fp.ps[t].mode == PM_SPARSE);
+        c1d |= (fp.ps[t].mode == PM_C1QD);
+    }
+    switch ((spx ? 1 : 0) | (c1d ? 2 : 0)) {
+        case 1: return launch_fused_sp<OP, FIRST, 1>(p, fp, nvec, st, nd);
+        case 2: return launch_fused_sp<OP, FIRST, 2>(p, fp, nvec, st, nd);
+        case 3: return launch_fused_sp<OP, FIRST, 3>(p, fp, nvec, st, nd);
+        default: return launch_fused_sp<OP, FIRST, 0>(p, fp, nvec, st, nd);
+    }
 }
 
 static int collect_phases(gf_plan *p);
@@ -1933,7 +2002,7 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
                 fp.ps[t].fa2 = fp.ps[t].fa;
                 fp.ps[t].fb = fp.ps[t].fa;
                 fp.ps[t].fz = fp.ps[t].fa;
-                if (fp.ps[t].mode != PM_C1Q) fp.ps[t].mode = (p->spG[s] && p->sparse_fma) ? PM_SPARSE : PM_DENSE;
+                if (fp.ps[t].mode != PM_C1Q && fp.ps[t].mode != PM_C1QD) fp.ps[t].mode = (p->spG[s] && p->sparse_fma) ? PM_SPARSE : PM_DENSE;
             }
             const bool last = !grad_like && pi == nf - 1;
             if (last) ctas_v = fp.ctas;
@@ -1980,7 +2049,7 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
                     }
                     fp.ps[t].amask = act_rev;
                     act_rev |= fp.ps[t].zmask;
-                    if (fp.ps[t].mode != PM_C1Q) fp.ps[t].mode = (sp && p->sparse_fma) ? PM_SPARSE : PM_DENSE;
+                    if (fp.ps[t].mode != PM_C1Q && fp.ps[t].mode != PM_C1QD) fp.ps[t].mode = (sp && p->sparse_fma) ? PM_SPARSE : PM_DENSE;
                 }
                 // after the reverse sweep psi_0 = |j> is known exactly and chi is dead:
                 // the last pass writes back only the bra (needed by the ascending sweep)
@@ -2026,7 +2095,7 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
                         }
                         fp.ps[t].amask = act_asc;
                         act_asc |= fp.ps[t].zmask;
-                        if (fp.ps[t].mode != PM_C1Q) fp.ps[t].mode = (sp && p->sparse_fma) ? PM_SPARSE : PM_DENSE;
+                        if (fp.ps[t].mode != PM_C1Q && fp.ps[t].mode != PM_C1QD) fp.ps[t].mode = (sp && p->sparse_fma) ? PM_SPARSE : PM_DENSE;
                     }
                     if (pi == nr - 1) fp.store_mask = 0;  // nothing is read after the ascending sweep
                     if (pi == 0) { int rc_ = launch_fused<OP_ASC_H, true>(p, fp, nvec, st, nd); if (rc_) return rc_; }
@@ -2228,6 +2297,7 @@ extern "C" int gf_plan_layout(int k, int sector, int n_slots, const int32_t *t1,
     const PlanKnobs kn = plan_knobs(tmp.K, std::max(1, tile_bits));
     tmp.fm = kn.fm;
     tmp.fc = kn.fc;
+    tmp.c1q_dmma = kn.c1q_dmma;
     std::vector<FusedParams> passes = plan_passes(&tmp, sweep != 0, tmp.fm);
     if ((int)passes.size() > max_passes) return gf_fail(GF_EINVAL, "%zu passes exceed the output room", passes.size());
     *n_passes = (int)passes.size();

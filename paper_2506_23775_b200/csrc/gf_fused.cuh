@@ -30,7 +30,7 @@ constexpr int FMAXSLOTS = 16;   // max slots per pass (kernel parameter space: 1
 constexpr int FMAXGLOB = 40;
 constexpr int FMAXDIR = 3;      // HVP directions per sweep (full-Hessian columns)
 
-enum { PM_DENSE = 0, PM_SPARSE = 1, PM_C1Q = 2 };
+enum { PM_DENSE = 0, PM_SPARSE = 1, PM_C1Q = 2, PM_C1QD = 3 };
 
 // rows of the per-slot DMMA fragment table: G, G^dag, G^T, conj G, then Z_d^T
 // and Z_d per direction (row = slot * NFK + kind, 32 lanes per row)

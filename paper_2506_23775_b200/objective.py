@@ -251,7 +251,7 @@ _PLANS: dict = {}
 # environment knobs read by gf_plan_create (csrc/gf_engine.cu plan_knobs): part
 # of the plan cache key so a changed knob never reuses a plan built without it
 _PLAN_KNOBS = ("GF_ENGINE", "GF_FUSED_M", "GF_FWD_M", "GF_FUSED_C", "GF_FUSED_CTAS", "GF_PLAN_GREEDY",
-               "GF_SPARSE_DMMA")
+               "GF_SPARSE_DMMA", "GF_C1Q_DMMA")
 
 
 def _get_plan(circuit: Circuit, sector: int, batch: int, chunk: int) -> EnginePlan:
@@ -674,6 +674,173 @@ def hessian_vector_product(circuit: Circuit, oracle, directions, workers: int | 
     return [h[i] for i in range(circuit.num_logical)]
 
 
+def _pair_csr(circuit: Circuit, dedup: bool):
+    """Slot pairs to contract, grouped by first slot, with multiplicity and
+    logical-pair routing (reference objective.py:209-247): every ordered pair
+    once, or one representative per translation class scaled by the class
+    size when ``dedup`` (circuit.py:173-211)."""
+    nlog = circuit.num_logical
+    lids = [s.logical_id for s in circuit.slots]
+
+    def route(a, b):
+        return a * nlog - a * (a - 1) // 2 + (b - a)
+
+    if dedup:
+        pairs = translation_classes(circuit)
+    else:
+        n = circuit.num_slots
+        pairs = [((a, b), 1) for a in range(n) for b in range(a + 1, n)]
+    grouped: dict = {}
+    for (a, b), mult in pairs:
+        grouped.setdefault(a, []).append((b, mult))
+    firsts = sorted(grouped)
+    starts, seconds, mults, routes, syms, flips = [0], [], [], [], [], []
+    for a in firsts:
+        for b, mult in sorted(grouped[a]):
+            la, lb = lids[a], lids[b]
+            seconds.append(b)
+            mults.append(float(mult))
+            routes.append(route(min(la, lb), max(la, lb)))
+            syms.append(la == lb)
+            flips.append(la > lb)
+        starts.append(len(seconds))
+    return (np.array(firsts, np.int64), np.array(starts, np.int64), np.array(seconds, np.int64),
+            np.array(mults, np.float64), np.array(routes, np.int64), np.array(syms, np.int32),
+            np.array(flips, np.int32))
+
+
+class HessianPlan:
+    """Owns one gf_hess_plan: the reference's _hessian_chunk on the GPU
+    (cached passes, hole arrays, pair contractions routed per the pair CSR)."""
+
+    def __init__(self, circuit: Circuit, csr, support, batch: int, chunk: int):
+        t1, t2, lid = circuit.slot_arrays()
+        self.nlog = circuit.num_logical
+        self.A = int(len(support))
+        self.R = self.nlog * (self.nlog + 1) // 2
+        self.rec = 2 + 32 * self.nlog + 2 * self.R * self.A * self.A
+        self.batch, self.chunk = batch, chunk
+        first, start, sec, mult, route, sym, flip = (np.ascontiguousarray(x) for x in csr)
+        sup = np.ascontiguousarray(support, dtype=np.int64)
+        self._keep = (t1, t2, lid, first, start, sec, mult, route, sym, flip, sup)
+        h = ctypes.c_void_p()
+        _lib.check(_lib.lib.gf_hess_plan_create(ctypes.byref(h), circuit.num_qubits, circuit.num_slots,
+                                                t1.ctypes.data, t2.ctypes.data, lid.ctypes.data, self.nlog,
+                                                sup.ctypes.data, self.A, first.ctypes.data, len(first),
+                                                start.ctypes.data, sec.ctypes.data, mult.ctypes.data,
+                                                route.ctypes.data, sym.ctypes.data, flip.ctypes.data, batch, chunk))
+        self.h = h
+        self.routes_used = sorted(set(int(r) for r in route))
+
+    def set_gates(self, mats, parity_mode: bool):
+        m = np.ascontiguousarray(mats, dtype=np.complex128)
+        _lib.check(_lib.lib.gf_hess_plan_set_gates(self.h, m.ctypes.data, int(bool(parity_mode))))
+
+    def eval(self, nvec, basis, weights, phi0, out, counts):
+        _lib.check(_lib.lib.gf_hess_plan_eval(self.h, nvec, basis.data_ptr(),
+                                              None if weights is None else weights.data_ptr(), phi0.data_ptr(),
+                                              out.data_ptr(), counts.ctypes.data, _lib.stream_ptr()))
+
+    def last_launches(self) -> int:
+        return int(_lib.lib.gf_hess_plan_last_launches(self.h))
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value:
+            try:
+                _lib.lib.gf_hess_plan_destroy(h)
+            except Exception:  # interpreter shutdown
+                pass
+
+
+class _RunInfo:
+    """The fields _grad_report reads from a _Run."""
+
+    def __init__(self, spec, info):
+        self.spec = spec
+        self.launches, self.batch, self.chunk = info["launches"], info["batch"], info["chunk"]
+        self.elapsed, self.world = info["seconds"], info["world"]
+
+
+def _full_hessian_pairs(circuit, oracle, dedup, parity_mode, basis, batch, chunk, distributed):
+    """full_hessian through the pair-CSR chunk driver (reference
+    objective.py:701-767): returns (value, holomorphic D per logical, blocks
+    dict, counts, support, engine info)."""
+    k = circuit.num_qubits
+    spec = _resolve_basis(k, -1, False, basis)
+    N = 1 << k
+    n = circuit.num_slots
+    sup = PARITY_SUPPORT if parity_mode else DENSE_SUPPORT
+    A = len(sup)
+    total = spec.total
+    per = 16 * N * (2 * (n + 1) + 2 * A)  # cached passes + two hole arrays per summand
+    if batch is None:
+        env = os.environ.get("GF_BATCH")
+        batch = int(env) if env else max(1, min(total, (8 << 30) // per))
+    batch = max(1, min(batch, max(total, 1)))
+    chunk = chunk or min(CHUNK_STATES, batch)
+    if batch % chunk:
+        batch = max(chunk, (batch // chunk) * chunk)
+    csr = _pair_csr(circuit, dedup)
+    hp = HessianPlan(circuit, csr, sup, batch, chunk)
+    hp.set_gates(circuit.gate_stack(), parity_mode)
+    rank, world, dist = _dist_info(distributed)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    nchunks = (total + chunk - 1) // chunk
+    lo, hi = shard_chunks(nchunks, rank, world)
+    local = torch.zeros((hi - lo, hp.rec), dtype=torch.float64, device=dev)
+    counts = np.zeros(5, np.int64)
+    idx_all = None if spec.indices is None else torch.from_numpy(spec.indices).to(dev)
+    w_all = None if spec.weights is None else torch.from_numpy(spec.weights).to(dev)
+    phi0 = None
+    launches = 0
+    t0 = time.perf_counter()
+    pos, s1 = lo * chunk, min(total, hi * chunk)
+    while pos < s1:
+        nvec = min(batch, s1 - pos)
+        basis_t = (torch.arange(pos, pos + nvec, dtype=torch.int64, device=dev) if idx_all is None
+                   else idx_all[pos:pos + nvec].contiguous())
+        weights = None if w_all is None else w_all[pos:pos + nvec].contiguous()
+        rows = getattr(oracle, "phi0_at", None)
+        cur = rows(pos, nvec, -1, spec.indices) if rows is not None else None
+        if cur is None:
+            if phi0 is None:
+                phi0 = torch.empty((batch, N), dtype=torch.complex128, device=dev)
+            fn = getattr(oracle, "phi0_into", None)
+            if fn is not None:
+                fn(basis_t, None, phi0[:nvec])
+            else:
+                host = _host_phi0(oracle, basis_t.cpu().numpy(), k, -1)
+                phi0[:nvec].copy_(torch.from_numpy(host).to(dev))
+            cur = phi0
+        c0 = (pos // chunk) - lo
+        nc = (nvec + chunk - 1) // chunk
+        hp.eval(nvec, basis_t, weights, cur, local[c0:c0 + nc], counts)
+        launches += hp.last_launches()
+        pos += nvec
+    allrec = gather_records(local, lo, nchunks, rank, world, dist)
+    host = allrec.cpu().numpy()
+    tot = ordered_sum(host) if host.shape[0] else np.zeros(hp.rec)
+    nlog = circuit.num_logical
+    value = complex(tot[0], tot[1])
+    d = tot[2:2 + 32 * nlog].view(np.complex128).reshape(nlog, 4, 4).copy()
+    blk = tot[2 + 32 * nlog:].view(np.complex128).reshape(hp.R, A, A)
+    blocks = {}
+    for a in range(nlog):
+        for b in range(a, nlog):
+            r = a * nlog - a * (a - 1) // 2 + (b - a)
+            if r in hp.routes_used:
+                blocks[(a, b)] = blk[r].copy()
+    if dist is not None:  # the counters of every rank's share
+        ct = torch.from_numpy(counts).to(dev if dist.get_backend() == "nccl" else "cpu")
+        dist.all_reduce(ct)
+        counts = ct.cpu().numpy()
+    info = {"launches": launches, "summands": total, "batch": batch, "chunk": chunk,
+            "seconds": time.perf_counter() - t0, "world": world, "weight_sum": spec.weight_sum(),
+            "hessian_method": "pairs", "pairs": int(len(csr[2])), "dedup": bool(dedup)}
+    return value, d, blocks, counts, sup, info
+
+
 def _used_routes(circuit: Circuit):
     lid = [s.logical_id for s in circuit.slots]
     used = set()
@@ -686,16 +853,43 @@ def _used_routes(circuit: Circuit):
 
 def full_hessian(circuit: Circuit, oracle, use_translation_dedup: bool = False, parity_mode: bool = False,
                  workers: int | None = None, *, sector=None, fold=False, basis=None, batch=None, chunk=None,
-                 distributed=None) -> ObjectiveReport:
+                 distributed=None, method=None) -> ObjectiveReport:
     """Value, gradient and all holomorphic Hessian blocks (reference
     objective.py:701-767).
 
-    Blocks are assembled column by column from engine HVPs with unit
-    directions on the support entries (H~_{(a,i),(b,j)} = HVP(e_{b,j})[a][i]).
-    ``use_translation_dedup`` only changes the reported pair counts: the
-    engine computes the exact sum, which the reference's dedup equals."""
+    Two engine algorithms (``method``):
+
+    * ``"pairs"`` -- the reference's own: cached passes, a hole array per
+      first slot propagated forward and contracted at every listed later slot
+      (_hessian_chunk, objective.py:340-423) on the GPU
+      (gf_hess_plan_eval).  With ``use_translation_dedup`` only one
+      representative pair per translation class is contracted and scaled by
+      the class size (the reference's work reduction).  Full space only.
+    * ``"columns"`` -- blocks assembled column by column from engine HVPs with
+      unit directions on the support entries (H~_{(a,i),(b,j)} =
+      HVP(e_{b,j})[a][i]), three directions per set of reversible sweeps;
+      supports ``sector`` / ``fold``.
+
+    Default: "pairs" with ``use_translation_dedup`` (full space), else
+    "columns" (measured faster without dedup, profiles/)."""
     _check_oracle(circuit, oracle)
     t0 = time.perf_counter()
+    if method is None:
+        method = "pairs" if (use_translation_dedup and sector is None and not fold) else "columns"
+    if method not in ("pairs", "columns"):
+        raise ValueError(f"unknown Hessian method {method!r}")
+    if method == "pairs":
+        if sector is not None or fold:
+            raise ValueError("the pair-CSR Hessian runs in the full space (no sector / fold)")
+        value, d, blocks, counts, sup, info = _full_hessian_pairs(circuit, oracle, use_translation_dedup,
+                                                                  parity_mode, basis, batch, chunk, distributed)
+        run = _RunInfo(_resolve_basis(circuit.num_qubits, -1, False, basis), info)
+        rep = _grad_report(circuit, run, value, d, parity_mode, "gradient", t0)
+        rep.engine.update(info)
+        rep.hessian = HessianBlocks(circuit.num_logical, np.asarray(sup), blocks)
+        rep.pass_counts = dict(zip(COUNT_NAMES, (int(c) for c in counts)))
+        rep.wall_time = time.perf_counter() - t0
+        return rep
     if use_translation_dedup:
         classes = translation_classes(circuit)
     rep = full_gradient(circuit, oracle, workers, parity_mode, sector=sector, fold=fold, basis=basis, batch=batch,

@@ -76,6 +76,10 @@ class MatrixOracle:
 # ------------------------------------------------------------------ kernels
 
 
+COUNTS = ("gate_applications", "array_gate_applications", "hole_applications", "hole_contractions",
+          "pair_contractions")
+
+
 def test_dense_oracle_equivalence_exhaustive_basis():
     """test_kernels.py:49-63: every ordered target pair, every basis input, k <= 4."""
     rng = np.random.default_rng(5)
@@ -248,23 +252,31 @@ def test_hessian_dedup_and_parity_blocks_vs_reference():
                       [gf.Gate(m, (0, 1)) for m in g["gates"]],
                       gf.BrickwallMeta(3, tuple(int(l) for l in g["logical"]), 2, True))
     orc = gf.DenseOracle.from_matrix(g["U"])
-    for tag, dedup in (("full_", False), ("dedup_", True)):
-        rep = gf.full_hessian(circ, orc, use_translation_dedup=dedup)
+    for tag, dedup, method in (("full_", False, "columns"), ("full_", False, "pairs"), ("dedup_", True, "pairs"),
+                               ("dedup_", True, "columns")):
+        rep = gf.full_hessian(circ, orc, use_translation_dedup=dedup, method=method)
         keys = [tuple(int(v) for v in kk) for kk in g[tag + "keys"]]
         assert sorted(rep.hessian.blocks) == keys
         sc = np.abs(g[tag + "blocks"]).max()
         for kk, ref in zip(keys, g[tag + "blocks"]):
             assert np.abs(rep.hessian.blocks[kk] - ref).max() < 1e-10 * sc
         assert rep.pass_counts["pair_contractions"] == int(g[tag + "counts"][4])
+        if method == "pairs":
+            # the reference's own algorithm: every counter equal -- with dedup
+            # that is the work actually saved (fewer arrays, hole applications
+            # and pair contractions than the full enumeration)
+            assert [rep.pass_counts[c] for c in COUNTS] == [int(x) for x in g[tag + "counts"]]
+            assert rep.engine["hessian_method"] == "pairs" and rep.engine["dedup"] == dedup
     pc = gf.Circuit(int(g["p_k"]), [gf.GateSlot(int(l), tuple(int(x) for x in t))
                                     for t, l in zip(g["p_targets"], g["p_logical"])],
                     [gf.Gate(m, (0, 1), parity_sparse=True) for m in g["p_gates"]])
-    prep = gf.full_hessian(pc, gf.DenseOracle.from_matrix(g["p_U"]), parity_mode=True)
-    assert len(prep.hessian.support) == 8
-    assert rel_err(np.stack(prep.per_logical_gradient), g["p_riem"]) < 1e-10
-    sc = np.abs(g["p_hess_blocks"]).max()
-    for kk, ref in zip([tuple(int(v) for v in x) for x in g["p_hess_keys"]], g["p_hess_blocks"]):
-        assert np.abs(prep.hessian.blocks[kk] - ref).max() < 1e-10 * sc
+    for method in ("columns", "pairs"):
+        prep = gf.full_hessian(pc, gf.DenseOracle.from_matrix(g["p_U"]), parity_mode=True, method=method)
+        assert len(prep.hessian.support) == 8
+        assert rel_err(np.stack(prep.per_logical_gradient), g["p_riem"]) < 1e-10
+        sc = np.abs(g["p_hess_blocks"]).max()
+        for kk, ref in zip([tuple(int(v) for v in x) for x in g["p_hess_keys"]], g["p_hess_blocks"]):
+            assert np.abs(prep.hessian.blocks[kk] - ref).max() < 1e-10 * sc
 
 
 def test_hvp_zero_and_column_extraction(rng):

@@ -272,6 +272,31 @@ def test_c1_full_hessian_vs_reference():
     assert [rep.pass_counts[n] for n in gf.objective.COUNT_NAMES] == list(g["hess_counts"])
 
 
+def test_c1_full_hessian_pair_csr_driver_vs_reference():
+    """The reference's own Hessian algorithm on the GPU (gf_hess_plan_eval:
+    cached passes, hole arrays, routed pair contractions): blocks, value,
+    gradient and every pass counter equal the reference's c1 run, for
+    several batch / chunk shapes (bit-identical records across them)."""
+    g, spec, circ, orc = _c1()
+    keys = [tuple(x) for x in g["hess_keys"]]
+    ref = None
+    for batch, chunk in ((256, 64), (64, 64), (32, 16)):
+        rep = gf.full_hessian(circ, orc, method="pairs", batch=batch, chunk=chunk)
+        assert rep.engine["hessian_method"] == "pairs"
+        assert sorted(rep.hessian.blocks) == keys
+        for kk, b in zip(keys, g["hess_blocks"]):
+            assert rel_err(rep.hessian.blocks[kk], b) < TOL
+        assert abs(rep.value - g["value"]) < TOL * abs(g["value"])
+        assert rel_err(np.stack(rep.holomorphic_derivatives), g["holo"]) < TOL
+        assert [rep.pass_counts[c] for c in gf.objective.COUNT_NAMES] == [int(x) for x in g["hess_counts"]]
+        if chunk == 64:
+            if ref is None:
+                ref = rep
+            else:
+                for kk in keys:
+                    assert np.array_equal(rep.hessian.blocks[kk], ref.hessian.blocks[kk])
+
+
 def test_c1_trust_region_five_iterations_vs_reference():
     g, spec, circ, orc = _c1()
     final, trace = gf.trust_region_optimize(circ, orc, gf.TrustRegionParams(max_iterations=5))
@@ -521,6 +546,40 @@ def test_integration_stub_matches_reference_chunk_drivers():
         dsum = dsum + dacc
     assert abs(-vals.real - g["value"]) < TOL * abs(g["value"])
     assert rel_err(plan.logical_sum(dsum.reshape(-1, 16)), g["holo"]) < TOL
+
+
+def test_integration_stub_hessian_chunk_with_dedup_vs_reference():
+    """INTEGRATION.md section B, Hessian: the ctypes stub's
+    GpuHessianChunkEvaluator (gf_hess_plan_*) fed the reference's dedup pair
+    CSR (translation classes from the reference fixture) returns the
+    reference's blocks, dacc and counters for full_hessian's chunk closure
+    (objective.py:729-744)."""
+    import integration_stub as S
+
+    g = golden("dedup")
+    k = int(g["k"])
+    circ = gf.Circuit(k, [gf.GateSlot(int(l), tuple(int(x) for x in t)) for t, l in zip(g["targets"], g["logical"])],
+                      [gf.Gate(m, (0, 1)) for m in g["gates"]],
+                      gf.BrickwallMeta(3, tuple(int(l) for l in g["logical"]), 2, True))
+    classes = [((int(a), int(b)), int(m)) for a, b, m in g["classes"]]
+    csr = O.pair_csr(g["targets"], g["logical"], len(g["gates"]), classes)
+    ev = S.GpuHessianChunkEvaluator(circ, O.DENSE_SUPPORT, csr, max_chunk=64)
+    phi = O.dense_phi0(g["U"])
+    tot_v, tot_d, tot_b, tot_c = 0j, 0, 0, 0
+    for j0 in range(0, 64, 32):
+        v, dacc, blocks, counts = ev(j0, j0 + 32, phi(np.arange(j0, j0 + 32)))
+        tot_v, tot_d, tot_b, tot_c = tot_v + v, tot_d + dacc, tot_b + blocks, tot_c + counts
+    assert np.array_equal(tot_c, g["dedup_counts"])
+    keys = [tuple(int(x) for x in kk) for kk in g["dedup_keys"]]
+    nlog = len(g["gates"])
+    sc = np.abs(g["dedup_blocks"]).max()
+    for (a, b), ref in zip(keys, g["dedup_blocks"]):
+        r = a * nlog - a * (a - 1) // 2 + (b - a)
+        assert np.abs(tot_b[r] - ref).max() < TOL * sc
+    t1, t2, lid = circ.slot_arrays()
+    plan = O.Plan(k, np.stack([t1, t2], 1), lid, circ.gate_stack())
+    assert rel_err(plan.logical_sum(tot_d.reshape(-1, 16)), g["holo"]) < TOL
+    assert abs(-tot_v.real - g["value"]) < TOL * abs(g["value"])
 
 
 @pytest.mark.parametrize("sector,m", [(None, None), (0, None), (None, "7")])
