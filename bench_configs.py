@@ -31,6 +31,9 @@ CONFIGS = {
     "c5": (16, 9, True, True, 0, True, 4, 1),
     "c2h": (8, 5, False, False, None, False, 1, None),   # configs[1]: full Hessian assembly, full 2^16 sum
     "c3tr": (12, 7, False, True, 0, False, 2, 64),       # configs[2]: one TR step, gradient + 10 tCG HVPs
+    "c5h": (16, 9, True, True, 0, True, 4, 1),            # configs[4]: one full gradient + 20 HVPs
+    "c2hp": (8, 5, False, False, None, False, 1, 1024),   # configs[1] Hessian: pair-CSR vs HVP-column engines
+    "bw16d": (8, 5, True, False, None, False, 5, 1024),   # 16-qubit periodic brick wall: translation dedup
 }
 
 
@@ -69,6 +72,47 @@ def run(name):
         diag = [rep.hessian.blocks[(a, a)] for a in range(circ.num_logical) if (a, a) in rep.hessian.blocks]
         out["diag_block_symmetry_max_rel_dev"] = float(max(np.abs(b - b.T).max() / np.abs(b).max() for b in diag))
         out["reference_cpu_estimate_h"] = 149.0  # 8.2 s per summand x 2^16, single core
+        return out
+    if name in ("c2hp", "bw16d"):
+        # full_hessian on a contiguous 1024-summand sample, both engine
+        # algorithms (objective.full_hessian method=): the reference's pair-CSR
+        # driver (gf_hess_plan_eval) and the HVP-column sweeps; bw16d is a
+        # periodic spinless-style brick wall where translation dedup applies
+        if name == "bw16d":
+            from bench_v1 import IdentityOracle
+
+            grng = np.random.default_rng(seed)
+            circ = gf.build_brickwall(16, layers, [gf.manifold.random_unitary(4, grng) for _ in range(layers)],
+                                      periodic=True)
+            k = 16
+            cache = IdentityOracle(k)
+            out.update(slots=circ.num_slots, logical=circ.num_logical, qubits=k)
+        else:
+            cache = gf.models.CachedTargetColumns(gf.NumberBlockOracle(spec, 0.25), k, 0, sample, batch=512)
+        basis = (np.arange(sample, dtype=np.int64), None)
+        variants = [("columns", False), ("pairs", False)] + ([("pairs", True)] if name == "bw16d" else [])
+        ref = None
+        for method, dedup in variants:
+            kw = dict(method=method, use_translation_dedup=dedup, basis=basis)
+            gf.full_hessian(circ, cache, **kw)  # plan + warm-up
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            rep = gf.full_hessian(circ, cache, **kw)
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+            tag = method + ("_dedup" if dedup else "")
+            out[f"{tag}_s_per_summand"] = dt / sample
+            out[f"{tag}_full_sum_extrapolated_s"] = dt / sample * 2**k
+            out[f"{tag}_pass_counts"] = rep.pass_counts
+            if ref is None:
+                ref = rep
+            else:
+                sc = max(np.abs(b).max() for b in ref.hessian.blocks.values())
+                out[f"{tag}_vs_columns_max_rel_dev"] = float(max(
+                    np.abs(rep.hessian.blocks[kk] - ref.hessian.blocks[kk]).max() for kk in ref.hessian.blocks) / sc)
+            obj._PLANS.clear()
+            torch.cuda.empty_cache()
+        out["sample_summands"] = sample
         return out
     if name == "c1":
         orc = gf.DenseOracle(spec, 0.25)
@@ -143,7 +187,42 @@ def run(name):
     total = out.get("orbit_reps_total_burnside") or sect_size
     out["full_sum_summands"] = total
     out["extrapolated_full_sum_grad_hvp_hours_1gpu"] = total * dt / idx.size / 3600
+    if name == "c5h":
+        # configs[4] as stated: one gradient + 20 HVPs per summand, the HVPs in
+        # multi-direction sweeps (as many directions per sweep as fit in HBM)
+        dirs = []
+        for _ in range(20):
+            dirs.append([gf.manifold.project_tangent_gate(g.matrix, rng.normal(size=(4, 4)) +
+                                                          1j * rng.normal(size=(4, 4)), True)
+                         for g in circ.logical_gates])
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        gf.full_gradient(circ, cache, parity_mode=True, sector=0, basis=basis)
+        torch.cuda.synchronize()
+        out["gradient_s_per_summand"] = (time.perf_counter() - t0) / idx.size
+        t0 = time.perf_counter()
+        hv20 = gf.hessian_vector_products(circ, cache, dirs, sector=0, basis=basis)
+        torch.cuda.synchronize()
+        out["hvp20_s_per_summand"] = (time.perf_counter() - t0) / idx.size
+        out["directions_per_sweep"] = obj._directions_per_sweep(circ, 0)
+        out["gradient_plus_20_hvp_s_per_summand"] = out["gradient_s_per_summand"] + out["hvp20_s_per_summand"]
+        # consistency: direction 0 of the batched sweeps equals the single-direction HVP
+        single = gf.hessian_vector_product(circ, cache, dirs[0], sector=0, basis=basis)
+        sc = max(np.abs(np.stack(single)).max(), 1e-300)
+        out["multi_vs_single_hvp_max_rel_dev"] = float(np.abs(np.stack(hv20[0]) - np.stack(single)).max() / sc)
+        return out
     if name == "c3tr":
+        # configs[2] as stated: gradient + 10 HVPs per TR step, timed directly
+        # (the tCG of a real step may stop earlier at the boundary / negative
+        # curvature; the TR step below reports its own inner count)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        gf.full_gradient(circ, cache, parity_mode=True, sector=0, basis=basis)
+        for _ in range(10):
+            gf.hessian_vector_product(circ, cache, X, sector=0, basis=basis)
+        torch.cuda.synchronize()
+        out["gradient_plus_10_hvp_s"] = time.perf_counter() - t0
+        out["gradient_plus_10_hvp_s_per_summand"] = out["gradient_plus_10_hvp_s"] / idx.size
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         params = gf.TrustRegionParams(max_iterations=1, use_hvp=True, tcg=gf.TcgParams(max_inner=10))

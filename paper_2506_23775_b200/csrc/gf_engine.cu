@@ -1549,6 +1549,11 @@ extern "C" int gf_plan_set_directions_multi(gf_plan *p, int nd, const double *zm
         const size_t qbytes = sizeof(double) * 32 * (size_t)p->max_batch * std::max(1, p->n);
         double2 *aux = nullptr;
         double *phd = nullptr, *pha = nullptr, *qhd = nullptr, *qha = nullptr;
+        // release the old per-direction workspace first: at 2^31 amplitudes the
+        // old and new chi / v vectors do not fit side by side
+        cudaFree(p->aux); cudaFree(p->partHd); cudaFree(p->partHa); cudaFree(p->qHd); cudaFree(p->qHa);
+        p->aux = nullptr; p->partHd = p->partHa = p->qHd = p->qHa = nullptr;
+        p->aux_dirs = 0;
         cudaError_t e = cudaMalloc(&aux, vbytes * nd);
         if (e == cudaSuccess) e = cudaMalloc(&phd, pbytes * nd);
         if (e == cudaSuccess) e = cudaMalloc(&pha, pbytes * nd);
@@ -1557,9 +1562,17 @@ extern "C" int gf_plan_set_directions_multi(gf_plan *p, int nd, const double *zm
         if (e != cudaSuccess) {
             cudaFree(aux); cudaFree(phd); cudaFree(pha); cudaFree(qhd); cudaFree(qha);
             cudaGetLastError();
-            return gf_fail(GF_ENOMEM, "direction workspace: %s", cudaGetErrorString(e));
+            // restore one direction's workspace so the plan stays usable
+            cudaError_t r = cudaMalloc(&p->aux, vbytes);
+            if (r == cudaSuccess) r = cudaMalloc(&p->partHd, pbytes);
+            if (r == cudaSuccess) r = cudaMalloc(&p->partHa, pbytes);
+            if (r == cudaSuccess) r = cudaMalloc(&p->qHd, qbytes);
+            if (r == cudaSuccess) r = cudaMalloc(&p->qHa, qbytes);
+            if (r == cudaSuccess) p->aux_dirs = 1;
+            cudaGetLastError();
+            p->have_z = false;
+            return gf_fail(GF_ENOMEM, "direction workspace for %d directions: %s", nd, cudaGetErrorString(e));
         }
-        cudaFree(p->aux); cudaFree(p->partHd); cudaFree(p->partHa); cudaFree(p->qHd); cudaFree(p->qHa);
         p->aux = aux; p->partHd = phd; p->partHa = pha; p->qHd = qhd; p->qHa = qha;
         p->aux_dirs = nd;
     }

@@ -328,6 +328,18 @@ __global__ void kh_records(const double *qD, const double *qV, const double2 *qP
     if (lane == 0) out[w] = acc;
 }
 
+// out[a][c] = sum over CTAs of part[cta][c][a] (the public B[a, c] layout of
+// kernels.hole_contract_array, kernels.py:600-623)
+__global__ void kh_pair_reduce_T(const double2 *part, double2 *out, int ctas, int ncols, int A)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= ncols * A) return;
+    const int c = i / A, a = i - c * A;
+    double2 acc = czero();
+    for (int t = 0; t < ctas; ++t) acc = cadd(acc, part[(size_t)t * ncols * A + i]);
+    out[a * ncols + c] = acc;
+}
+
 // per-slot gradient holes summed over the batch: out[s][32] (normalised
 // wire orientation, the reference's dacc)
 __global__ void kh_slot_sums(const double *qD, int64_t nvec, int nslots, double *out)
@@ -341,6 +353,88 @@ __global__ void kh_slot_sums(const double *qD, int64_t nvec, int nslots, double 
 }
 
 }  // namespace
+
+static int grid_units(u64 units, int threads_per_unit)
+{
+    const u64 ctas = (units * threads_per_unit + HT - 1) / HT;
+    return (int)std::max<u64>(1, std::min<u64>(ctas, HMAXCTAS));
+}
+
+// ---------------------------------------------------------------------------
+// fast paths of the public kernel ops (gf_ops.cu) for arity / support sizes
+// 8 and 16: thread = (tuple, arity index), no 64-bit divisions, CTA partials
+// summed in CTA order
+// ---------------------------------------------------------------------------
+static HSupport hsupport(const int *row, const int *col, int n)
+{
+    HSupport s;
+    for (int c = 0; c < 16; ++c) {
+        s.row[c] = c < n ? row[c] : 0;
+        s.col[c] = c < n ? col[c] : 0;
+    }
+    return s;
+}
+
+int gf_fast_hole_apply(const void *psi, void *out, int k, int lo, int hi, const int *row, const int *col, int arity,
+                       void *stream)
+{
+    const u64 units = (1ull << k) >> 2;
+    const dim3 grid(grid_units(units, arity) * 8, 1);
+    const HSupport sp = hsupport(row, col, arity);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (arity == 16) kh_hole_apply<16><<<grid, HT, 0, st>>>((const double2 *)psi, (double2 *)out, k, lo, hi, sp);
+    else if (arity == 8) kh_hole_apply<8><<<grid, HT, 0, st>>>((const double2 *)psi, (double2 *)out, k, lo, hi, sp);
+    else return gf_fail(GF_EINVAL, "fast hole apply needs arity 8 or 16");
+    GF_CUDA(cudaGetLastError());
+    return GF_OK;
+}
+
+int gf_fast_array_apply(const void *in, void *out, int k, int arity, int lo, int hi, const Mat4 &g, int sparse,
+                        void *stream)
+{
+    const u64 units = (1ull << k) >> 2;
+    const dim3 grid(grid_units(units, arity) * 8, 1);
+    const HSupport sp = hsupport(nullptr, nullptr, 0);
+    cudaStream_t st = (cudaStream_t)stream;
+    const double2 *x = (const double2 *)in;
+    double2 *y = (double2 *)out;
+#define KH_ARR(A_, S_) kh_pair<A_, 8, false, true, S_><<<grid, HT, 0, st>>>(nullptr, x, y, k, lo, hi, sp, g, nullptr)
+    if (arity == 16) { if (sparse) KH_ARR(16, true); else KH_ARR(16, false); }
+    else if (arity == 8) { if (sparse) KH_ARR(8, true); else KH_ARR(8, false); }
+    else return gf_fail(GF_EINVAL, "fast array apply needs arity 8 or 16");
+#undef KH_ARR
+    GF_CUDA(cudaGetLastError());
+    return GF_OK;
+}
+
+int gf_fast_hole_array(const void *bra, const void *arr, int k, int arity, int lo, int hi, const int *row,
+                       const int *col, int ncols, void *out, void *stream)
+{
+    const u64 units = (1ull << k) >> 2;
+    const int ctas = grid_units(units, arity) * 8;
+    const dim3 grid(ctas, 1);
+    const HSupport sp = hsupport(row, col, ncols);
+    cudaStream_t st = (cudaStream_t)stream;
+    double2 *part = nullptr;
+    GF_CUDA(cudaMallocAsync((void **)&part, sizeof(double2) * (size_t)ctas * ncols * arity, st));
+    Mat4 g0;
+    memset(&g0, 0, sizeof g0);
+    const double2 *b = (const double2 *)bra, *x = (const double2 *)arr;
+#define KH_HA(A_, S_) kh_pair<A_, S_, true, false, false><<<grid, HT, 0, st>>>(b, x, nullptr, k, lo, hi, sp, g0, part)
+    if (arity == 16 && ncols == 16) KH_HA(16, 16);
+    else if (arity == 16 && ncols == 8) KH_HA(16, 8);
+    else if (arity == 8 && ncols == 16) KH_HA(8, 16);
+    else if (arity == 8 && ncols == 8) KH_HA(8, 8);
+    else {
+        cudaFreeAsync(part, st);
+        return gf_fail(GF_EINVAL, "fast array contraction needs arity / support 8 or 16");
+    }
+#undef KH_HA
+    kh_pair_reduce_T<<<(ncols * arity + 255) / 256, 256, 0, st>>>(part, (double2 *)out, ctas, ncols, arity);
+    GF_CUDA(cudaFreeAsync(part, st));
+    GF_CUDA(cudaGetLastError());
+    return GF_OK;
+}
 
 // ---------------------------------------------------------------------------
 // handle
@@ -376,11 +470,6 @@ static void hess_free(gf_hess_plan *h)
         if (p) cudaFree(p);
 }
 
-static int grid_units(u64 units, int threads_per_unit)
-{
-    const u64 ctas = (units * threads_per_unit + HT - 1) / HT;
-    return (int)std::max<u64>(1, std::min<u64>(ctas, HMAXCTAS));
-}
 
 extern "C" int gf_hess_plan_create(gf_hess_plan **out, int k, int n_slots, const int32_t *t1, const int32_t *t2,
                                    const int32_t *logical, int n_logical, const int64_t *support, int arity,

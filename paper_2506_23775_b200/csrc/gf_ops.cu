@@ -678,6 +678,7 @@ extern "C" int gf_hole_apply(const void *psi, void *out, int k, int t1, int t2, 
     Support s;
     rc = make_support(support, arity, nm.swapped, s);
     if (rc) return rc;
+    if (arity == 16 || arity == 8) return gf_fast_hole_apply(psi, out, k, nm.lo, nm.hi, s.row, s.col, arity, stream);
     SupportDev sd;
     sd.n = s.n;
     memcpy(sd.row, s.row, sizeof sd.row);
@@ -699,6 +700,7 @@ extern "C" int gf_apply_gate_to_array(const void *in, void *out, int k, int arit
     int rc = normalise(k, t1, t2, nm);
     if (rc) return rc;
     Mat4 g = load_mat(mat, nm.swapped);
+    if (arity == 16 || arity == 8) return gf_fast_array_apply(in, out, k, arity, nm.lo, nm.hi, g, parity_sparse, stream);
     unsigned long long total = (1ull << (k - 2)) * (unsigned long long)arity;
     cudaStream_t st = (cudaStream_t)stream;
     if (parity_sparse)
@@ -722,6 +724,8 @@ extern "C" int gf_hole_contract_array(const void *bra, const void *arr, int k, i
     Support s;
     rc = make_support(support, ncols, nm.swapped, s);
     if (rc) return rc;
+    if ((arity == 16 || arity == 8) && (ncols == 16 || ncols == 8))
+        return gf_fast_hole_array(bra, arr, k, arity, nm.lo, nm.hi, s.row, s.col, ncols, out_dev, stream);
     SupportDev sd;
     sd.n = s.n;
     memcpy(sd.row, s.row, sizeof sd.row);

@@ -629,6 +629,18 @@ def gradient_and_hvp(circuit: Circuit, oracle, directions, parity_mode: bool = F
     return rep, [h[i] for i in range(circuit.num_logical)]
 
 
+def _directions_per_sweep(circuit, sector) -> int:
+    """HVP directions per set of sweeps (<= 3): each needs one more resident
+    chi / v vector; at 2^31 amplitudes (32 GiB vectors) the device holds
+    psi, bra, phi0 and at most two of them."""
+    K = circuit.num_qubits - (1 if _sector_code(sector) >= 0 else 0)
+    vec = 16 * (1 << K)
+    if vec < (1 << 30):
+        return 3
+    free, total = torch.cuda.mem_get_info()
+    return int(max(1, min(3, total // vec - 3)))
+
+
 def _multi_direction_ok(circuit, sector, batch, chunk, basis, fold) -> bool:
     """True when the plan for this evaluation runs the fused engine (the only
     one that evaluates several HVP directions per sweep)."""
@@ -647,8 +659,9 @@ def hessian_vector_products(circuit: Circuit, oracle, direction_sets, *, sector=
     zs = [_slot_directions(circuit, d) for d in direction_sets]
     out = []
     i = 0
+    gmax = _directions_per_sweep(circuit, sector)
     while i < len(zs):
-        group = zs[i:i + 3]
+        group = zs[i:i + gmax]
         z = np.ascontiguousarray(np.stack(group)) if len(group) > 1 else group[0]
         if len(group) > 1 and not _multi_direction_ok(circuit, sector, batch, chunk, basis, fold):
             # the streaming engine (tiny state spaces, GF_ENGINE=stream) runs one direction per sweep
