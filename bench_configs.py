@@ -106,6 +106,13 @@ def run(name):
             out[f"{tag}_pass_counts"] = rep.pass_counts
             if ref is None:
                 ref = rep
+            elif dedup:
+                # translation dedup equals the full enumeration only for the full,
+                # translation-invariant basis sum -- not for this contiguous sample
+                # (checked at full sum against the reference's dedup fixture in
+                # tests/test_gpu_api.py); report the work reduction only
+                out[f"{tag}_pair_contraction_ratio"] = (rep.pass_counts["pair_contractions"] /
+                                                        ref.pass_counts["pair_contractions"])
             else:
                 sc = max(np.abs(b).max() for b in ref.hessian.blocks.values())
                 out[f"{tag}_vs_columns_max_rel_dev"] = float(max(

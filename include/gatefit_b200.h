@@ -267,6 +267,11 @@ int gf_nb_gather(const int64_t *js, int64_t nrows, const void *mats, const int64
                  const int32_t *blkdim, const int32_t *block_of, const int32_t *rank_of, const int64_t *full_of,
                  int64_t max_dim, int shift, void *out, int64_t row_len, void *stream);
 
+/* Synchronous check of n device doubles (engine records): GF_ENONFINITE if
+ * any is NaN or Inf, else GF_OK.  The reference raises FloatingPointError on
+ * non-finite results (objective.py:575-578, optimizer.py:147-149). */
+int gf_check_finite(const double *x_dev, int64_t n, void *stream);
+
 /* Device-memory helpers for bindings without a tensor library (the ctypes
  * stub of INTEGRATION.md).  gf_memcpy kind: 0 = H2D, 1 = D2H, 2 = D2D
  * (asynchronous on `stream`; pair with gf_stream_sync). */

@@ -56,6 +56,7 @@ EXPORTS = (
     "gf_nb_gather",
     "gf_nb_block_matrix",
     "gf_peak_fp64",
+    "gf_check_finite",
     "gf_set_device",
     "gf_malloc",
     "gf_free",
@@ -119,6 +120,7 @@ for _name, _args in {
     "gf_nb_rank": [_vp, _vp, _i64, _vp, _i, _vp],
     "gf_nb_block_matrix": [_vp, _vp, _i, _vp, _vp, _i, _vp, _i, ctypes.c_double, ctypes.c_double, _vp, _vp],
     "gf_nb_gather": [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i, _vp, _i64, _vp],
+    "gf_check_finite": [_vp, _i64, _vp],
     "gf_set_device": [_i],
     "gf_malloc": [ctypes.POINTER(_vp), _i64],
     "gf_free": [_vp],

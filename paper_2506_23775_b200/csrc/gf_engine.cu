@@ -52,6 +52,25 @@
 #define GF_SPARSE_DMMA_DEFAULT 1  // measured: c3 -11%, c4 -11%, c5 -11% per summand vs the FMA form
 #endif
 
+// GF_CHECKS (libgfcuda_checked.so, the bounds-checked build the GPU tests run
+// in place of compute-sanitizer, which this pool does not allow): device
+// asserts that trap on the first violated tile / global address invariant.
+#ifdef GF_CHECKS
+#include <cstdio>
+#define GF_DCHECK(c)                                                                        \
+    do {                                                                                    \
+        if (!(c)) {                                                                         \
+            printf("GF_CHECKS %s:%d block (%d,%d) thread %d: %s\n", __FILE__, __LINE__,     \
+                   blockIdx.x, blockIdx.y, threadIdx.x, #c);                                \
+            __trap();                                                                       \
+        }                                                                                   \
+    } while (0)
+#else
+#define GF_DCHECK(c) \
+    do {             \
+    } while (0)
+#endif
+
 namespace gf {
 
 // OP_REV_H: the reverse sweep of an HVP-only evaluation (no gradient hole)
@@ -352,6 +371,16 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
         // 2q tensor path (8-tuple groups, paired hole MMAs)
         const unsigned TW = max(nunit / (unsigned)NW, c1q ? 4u : 8u);
         const unsigned nwa = nunit >> (31 - __clz(TW));  // powers of two
+#ifdef GF_CHECKS
+        {
+            // every tile address below is an XOR of these columns: all < T
+            // keeps every shared-memory access inside the tile
+            const int ub = 31 - __clz(nunit);  // unit-index bits
+            for (int i = 0; i < ub; ++i) GF_DCHECK(p.ps[si].col[i] < T);
+            GF_DCHECK(p.ps[si].so < T && p.ps[si].sh < T);
+            GF_DCHECK(p.ps[si].slot >= 0 && (p.ps[si].fa >= 0) && (p.ps[si].fb >= 0));
+        }
+#endif
         double cD0 = 0.0, cD1 = 0.0, cH0[ND], cH1[ND];
 #pragma unroll
         for (int d = 0; d < ND; ++d) cH0[d] = cH1[d] = 0.0;
@@ -963,6 +992,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_fused(const FusedParams p)
         for (unsigned l = tid; l < T && !p.exp_noio; l += NT) {
             const u64 a = base + (l & cmask) + hiofs[l >> c];
             const unsigned sl = sw(l);
+            GF_DCHECK(a < p.N && sl < T);
             if constexpr (SYNTH)
                 t0[sl] = make_double2(a == jb ? 1.0 : 0.0, 0.0);  // psi_0 = |j>, no HBM read
             else

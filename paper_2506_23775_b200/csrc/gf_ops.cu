@@ -744,6 +744,33 @@ extern "C" int gf_hole_contract_array(const void *bra, const void *arr, int k, i
     return GF_OK;
 }
 
+__global__ void k_count_nonfinite(const double *x, int64_t n, unsigned long long *bad)
+{
+    unsigned long long local = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        local += isfinite(x[i]) ? 0ull : 1ull;
+    if (local) atomicAdd(bad, local);  // integer count: order-independent
+}
+
+// Synchronous: GF_ENONFINITE if any of the n doubles is NaN / Inf (the
+// reference raises FloatingPointError on non-finite results,
+// objective.py:575-578, optimizer.py:147-149).
+extern "C" int gf_check_finite(const double *x, int64_t n, void *stream)
+{
+    if (n < 0 || (n > 0 && !x)) return gf_fail(GF_EINVAL, "bad arguments");
+    if (n == 0) return GF_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned long long *bad = nullptr, host = 0;
+    GF_CUDA(cudaMallocAsync((void **)&bad, sizeof *bad, st));
+    GF_CUDA(cudaMemsetAsync(bad, 0, sizeof *bad, st));
+    k_count_nonfinite<<<grid_for((unsigned long long)n, 256), 256, 0, st>>>(x, n, bad);
+    GF_CUDA(cudaMemcpyAsync(&host, bad, sizeof host, cudaMemcpyDeviceToHost, st));
+    GF_CUDA(cudaFreeAsync(bad, st));
+    GF_CUDA(cudaStreamSynchronize(st));
+    if (host) return gf_fail(GF_ENONFINITE, "%llu non-finite values in %lld engine outputs", host, (long long)n);
+    return GF_OK;
+}
+
 extern "C" int gf_sector_unrank(const int64_t *idx, int64_t m, int sector, int64_t *out, void *stream)
 {
     if (m < 0 || (m > 0 && (!idx || !out))) return gf_fail(GF_EINVAL, "bad arguments");

@@ -498,6 +498,8 @@ class _Run:
             self.plan.eval(self.flags, nvec, basis, weights, cur, local[c0:c0 + nc])
             launches += self.plan.last_launches()
             pos += nvec
+        # non-finite engine output -> FloatingPointError (GF_ENONFINITE)
+        _lib.check(_lib.lib.gf_check_finite(local.data_ptr(), local.numel(), _lib.stream_ptr()))
         allrec = gather_records(local, lo, nchunks, self.rank, self.world, self.dist)
         host = allrec.cpu().numpy()
         self.elapsed = time.perf_counter() - t0
@@ -831,6 +833,7 @@ def _full_hessian_pairs(circuit, oracle, dedup, parity_mode, basis, batch, chunk
         hp.eval(nvec, basis_t, weights, cur, local[c0:c0 + nc], counts)
         launches += hp.last_launches()
         pos += nvec
+    _lib.check(_lib.lib.gf_check_finite(local.data_ptr(), local.numel(), _lib.stream_ptr()))
     allrec = gather_records(local, lo, nchunks, rank, world, dist)
     host = allrec.cpu().numpy()
     tot = ordered_sum(host) if host.shape[0] else np.zeros(hp.rec)

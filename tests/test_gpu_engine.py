@@ -601,3 +601,21 @@ def test_multi_direction_hvp_equals_single(monkeypatch, sector, m):
     for z, got in zip(dirs, multi):
         one = gf.hessian_vector_product(circ, orc, z, sector=sector)
         assert rel_err(np.stack(got), np.stack(one)) < 1e-12
+
+
+def test_non_finite_engine_output_raises_floating_point_error():
+    """GF_ENONFINITE: a NaN in a gate propagates into the records and is
+    reported as FloatingPointError (reference objective.py:575-578), for the
+    engine and the pair-CSR Hessian driver alike."""
+    g, spec, circ, orc = _c1()
+    bad = circ.gate_stack().copy()
+    bad[1, 2, 3] = np.nan
+    cb = circ.with_gates(list(bad))
+    with pytest.raises(FloatingPointError):
+        gf.full_gradient(cb, orc)
+    with pytest.raises(FloatingPointError):
+        gf.full_hessian(cb, orc, method="pairs")
+    x = torch.tensor([1.0, np.inf, 0.0], dtype=torch.float64, device="cuda")
+    with pytest.raises(FloatingPointError):
+        gf._lib.check(gf._lib.lib.gf_check_finite(x.data_ptr(), 3, gf._lib.stream_ptr()))
+    gf._lib.check(gf._lib.lib.gf_check_finite(x.data_ptr(), 1, gf._lib.stream_ptr()))

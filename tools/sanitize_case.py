@@ -41,4 +41,7 @@ for t in ((0, 1), (3, 11), (11, 2)):
     gf.hole_contract_array(psi, arr, (5, 6))
 gf.apply_gate_1q(psi, gf.manifold.random_unitary(2, rng), 4)
 torch.cuda.synchronize()
-print("sanitize case ok", rep.value, repp.value, len(cols))
+want = os.environ.get("GF_EXPECT_LIB")
+if want:  # the library this process actually mapped
+    assert want in open("/proc/self/maps").read(), want
+print("sanitize case ok", repr(rep.value), repr(repp.value), len(cols))
