@@ -936,8 +936,15 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
     }
 }
 
+// forward passes stage one vector per tile (~38 KB of shared memory): ask the
+// compiler for 4 CTAs per SM there (<= 64 registers), 2 for the three-vector
+// reverse / ascending passes (GF_FWD_OCC overrides the forward occupancy)
+#ifndef GF_FWD_OCC
+#define GF_FWD_OCC 4
+#endif
 template <int OP, bool FIRST, int NT, int ND, int VAR>
-__global__ void __launch_bounds__(NT, 512 / NT) k_fused(const FusedParams p)
+__global__ void __launch_bounds__(NT, ((OP == OP_FWD || OP == OP_FWD_DOT) ? GF_FWD_OCC * 256 : 512) / NT)
+    k_fused(const FusedParams p)
 {
     constexpr int NW = NT / 32;  // warps per CTA
     constexpr int NH = 1 + ND;   // hole slots: gradient + ND directions

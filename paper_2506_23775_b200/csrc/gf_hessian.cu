@@ -183,78 +183,68 @@ __global__ void __launch_bounds__(HT) kh_hole_apply(const double2 *__restrict__ 
 
 // Fused pair contraction + array update of slot l' for every summand:
 // part[b][cta][c][a] = sum over the CTA's tuples of bra(row_c) cur(col_c, a)
-// (kernels.py:417-458, stored [c][a] = out_t), and out = G cur when
-// APPLY.  Thread = (tuple, a); the A_s contraction accumulators sit in
-// registers, folded over the tuple lanes with shuffles and over warps in
-// shared memory (fixed order).
+// (kernels.py:417-458, stored [c][a] = out_t), and out = G cur when APPLY.
+// Thread = (tuple, row i, arity index a): it loads the tuple's four values of
+// its a (coalesced over a; the four i-threads of an a share the addresses),
+// accumulates bra_i cur_j for j = 0..3 and writes output row i of G cur.  Four
+// accumulators per thread instead of A_s keep the kernel register-light; the
+// CTA's tuple lanes are summed in shared memory in a fixed order.
 template <int A, int AS, bool CONTRACT, bool APPLY, bool SPARSE>
 __global__ void __launch_bounds__(HT) kh_pair(const double2 *__restrict__ bra, const double2 *__restrict__ cur,
                                               double2 *__restrict__ out, int logN, int lo, int hi,
                                               const HSupport sup, const Mat4 g, double2 *part)
 {
-    constexpr int TPW = 32 / A;  // tuples per warp (2 for A = 16, 4 for A = 8)
-    constexpr int NW = HT / 32;
+    constexpr int TL = HT / (4 * A);  // tuples per CTA iteration (4 for A = 16, 8 for A = 8)
     const u64 N = 1ull << logN, units = N >> 2;
-    const int a = threadIdx.x % A;
+    const int a = threadIdx.x % A, i = (threadIdx.x / A) & 3, tl = threadIdx.x / (4 * A);
     const u64 ol = 1ull << lo, oh = 1ull << hi;
+    const u64 oi = ((i & 1) ? ol : 0ull) + ((i & 2) ? oh : 0ull);
     const u64 vb = (u64)blockIdx.y * N;
-    double2 acc[AS];
+    double2 gi[4];
 #pragma unroll
-    for (int c = 0; c < AS; ++c) acc[c] = czero();
-    for (u64 t = ((u64)blockIdx.x * blockDim.x + threadIdx.x) / A; t < units;
-         t += (u64)gridDim.x * blockDim.x / A) {
-        const u64 b = ins0(ins0(t, lo), hi);
-        const u64 r[4] = {b, b + ol, b + oh, b + ol + oh};
+    for (int j = 0; j < 4; ++j) gi[j] = g.m[4 * i + j];
+    double2 acc[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[j] = czero();
+    for (u64 t = (u64)blockIdx.x * TL + tl; t < units; t += (u64)gridDim.x * TL) {
+        const u64 b = vb + ins0(ins0(t, lo), hi);
         double2 x[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) x[q] = cur[(vb + r[q]) * A + a];
+        x[0] = cur[b * A + a];
+        x[1] = cur[(b + ol) * A + a];
+        x[2] = cur[(b + oh) * A + a];
+        x[3] = cur[(b + ol + oh) * A + a];
         if (CONTRACT) {
-            double2 y[4];
+            const double2 y = bra[b + oi];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) y[q] = bra[vb + r[q]];
-#pragma unroll
-            for (int c = 0; c < AS; ++c) {
-                // row / col of support position c: compile-time loop, runtime table
-                double2 yv = y[0], xv = x[0];
-#pragma unroll
-                for (int q = 1; q < 4; ++q) {
-                    if (sup.row[c] == q) yv = y[q];
-                    if (sup.col[c] == q) xv = x[q];
-                }
-                acc[c] = cfma(yv, xv, acc[c]);
-            }
+            for (int j = 0; j < 4; ++j) acc[j] = cfma(y, x[j], acc[j]);
         }
         if (APPLY) {
-            double2 y[4];
-            mv4<SPARSE>(g, x, y);
+            double2 v;
+            if (SPARSE) {  // parity-conserving rows: {0,3} x {0,3} and {1,2} x {1,2}
+                const int j0 = (i == 0 || i == 3) ? 0 : 1, j1 = 3 - j0;
+                v = cfma(gi[j1], x[j1], cmul(gi[j0], x[j0]));
+            } else {
+                v = cmul(gi[0], x[0]);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) out[(vb + r[q]) * A + a] = y[q];
+                for (int j = 1; j < 4; ++j) v = cfma(gi[j], x[j], v);
+            }
+            out[(b + oi) * A + a] = v;
         }
     }
     if (CONTRACT) {
-        // fold the TPW tuple lanes of each a (lane = tuple_in_warp * A + a)
+        __shared__ double2 red[TL][4][4][A];  // [tuple lane][j][i][a]
 #pragma unroll
-        for (int s = A; s < 32; s <<= 1)
-#pragma unroll
-            for (int c = 0; c < AS; ++c) {
-                acc[c].x += __shfl_xor_sync(0xffffffffu, acc[c].x, s);
-                acc[c].y += __shfl_xor_sync(0xffffffffu, acc[c].y, s);
-            }
-        __shared__ double2 red[NW][AS * A];
-        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-        if (lane < A) {
-#pragma unroll
-            for (int c = 0; c < AS; ++c) red[warp][c * A + lane] = acc[c];
-        }
+        for (int j = 0; j < 4; ++j) red[tl][j][i][a] = acc[j];
         __syncthreads();
         const u64 slot = (u64)blockIdx.y * gridDim.x + blockIdx.x;
         for (int e = threadIdx.x; e < AS * A; e += HT) {
+            const int c = e / A, aa = e - c * A;
             double2 s = czero();
-            for (int w = 0; w < NW; ++w) s = cadd(s, red[w][e]);
+#pragma unroll
+            for (int q = 0; q < TL; ++q) s = cadd(s, red[q][sup.col[c]][sup.row[c]][aa]);
             part[slot * (AS * A) + e] = s;
         }
     }
-    (void)TPW;
 }
 
 // per-summand pair result q[b][c][a] (= out_t[c][a]) summed over CTAs
