@@ -48,6 +48,9 @@
 #ifndef GF_GATE_BLOCK
 #define GF_GATE_BLOCK 4
 #endif
+#ifndef GF_HOLE_ILP
+#define GF_HOLE_ILP 2  // independent DMMA accumulator chains per hole in the split hole phase
+#endif
 #ifndef GF_SPARSE_DMMA_DEFAULT
 #define GF_SPARSE_DMMA_DEFAULT 1  // measured: c3 -11%, c4 -11%, c5 -11% per summand vs the FMA form
 #endif
@@ -305,23 +308,44 @@ __device__ __forceinline__ void gate_frag(const Mat4 &M, int g, int t, double &b
     b1 = pi ? e.x : -e.y;
 }
 
-// y (this lane's amplitude) = sum of DMMA products over (x, fragment) pairs
+// y (this lane's amplitude) = sum of DMMA products over (x, fragment) pairs.
+// GF_SPLIT_MV: the two k-steps into independent accumulators plus two DADDs
+// (no DMMA -> DMMA dependency inside a gate application)
+#ifndef GF_SPLIT_MV
+#define GF_SPLIT_MV 0
+#endif
 __device__ __forceinline__ double2 dmma_mv(double2 x, double b0, double b1)
 {
     double c0 = 0.0, c1 = 0.0;
+#if GF_SPLIT_MV
+    double d0 = 0.0, d1 = 0.0;
+    dmma(c0, c1, x.x, b0);
+    dmma(d0, d1, x.y, b1);
+    return make_double2(c0 + d0, c1 + d1);
+#else
     dmma(c0, c1, x.x, b0);
     dmma(c0, c1, x.y, b1);
     return make_double2(c0, c1);
+#endif
 }
 
 __device__ __forceinline__ double2 dmma_mv2(double2 x, double b0, double b1, double2 z, double e0, double e1)
 {
     double c0 = 0.0, c1 = 0.0;
+#if GF_SPLIT_MV
+    double d0 = 0.0, d1 = 0.0;
+    dmma(c0, c1, x.x, b0);
+    dmma(d0, d1, z.x, e0);
+    dmma(c0, c1, x.y, b1);
+    dmma(d0, d1, z.y, e1);
+    return make_double2(c0 + d0, c1 + d1);
+#else
     dmma(c0, c1, x.x, b0);
     dmma(c0, c1, x.y, b1);
     dmma(c0, c1, z.x, e0);
     dmma(c0, c1, z.y, e1);
     return make_double2(c0, c1);
+#endif
 }
 
 // The slots of one pass applied to a tile staged in shared memory (t0 = psi,
@@ -711,6 +735,12 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                     double eD0 = 0.0, eD1 = 0.0, eH0[ND], eH1[ND];  // second accumulators (ILP)
 #pragma unroll
                     for (int d = 0; d < ND; ++d) eH0[d] = eH1[d] = 0.0;
+#if GF_HOLE_ILP >= 4
+                    // third / fourth accumulator sets for u & 2 (independent DMMA chains)
+                    double fD0 = 0.0, fD1 = 0.0, gD0 = 0.0, gD1 = 0.0, fH0[ND], fH1[ND], gH0[ND], gH1[ND];
+#pragma unroll
+                    for (int d = 0; d < ND; ++d) fH0[d] = fH1[d] = gH0[d] = gH1[d] = 0.0;
+#endif
                     const unsigned nq = TW >> 2;
                     // C1QD: parity of tuple 4q + tq is hpar ^ popc(q); a1 = tuple q + 1 (q even)
                     const unsigned hpar = wpar ^ ((unsigned)__popc((unsigned)tq) & 1u);
@@ -734,18 +764,28 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                             const unsigned a0 = ab ^ ((u & 2u) ? colH[1] : 0u) ^ ((u & 4u) ? colH[2] : 0u) ^ flipH(q);
                             const unsigned a1 = a0 ^ colH[0] ^ flipH(q) ^ flipH(q + 1);
                             const unsigned o0 = 2 * a0, o1 = 2 * a1;
+#if GF_HOLE_ILP >= 4
+                            const bool alt = (u & 2u) != 0;  // compile-time in the unrolled loop
+                            double &xD0 = alt ? fD0 : cD0, &xD1 = alt ? fD1 : cD1;
+                            double &yD0 = alt ? gD0 : eD0, &yD1 = alt ? gD1 : eD1;
+                            double *xH0 = alt ? fH0 : cH0, *xH1 = alt ? fH1 : cH1;
+                            double *yH0 = alt ? gH0 : eH0, *yH1 = alt ? gH1 : eH1;
+#else
+                            double &xD0 = cD0, &xD1 = cD1, &yD0 = eD0, &yD1 = eD1;
+                            double *xH0 = cH0, *xH1 = cH1, *yH0 = eH0, *yH1 = eH1;
+#endif
                             if constexpr (REV) {
                                 const double k0 = d0[o0], k1 = d0[o1];
                                 if constexpr (HD) {
-                                    dmma(cD0, cD1, d1[o0], k0);
-                                    dmma(eD0, eD1, d1[o1], k1);
+                                    dmma(xD0, xD1, d1[o0], k0);
+                                    dmma(yD0, yD1, d1[o1], k1);
                                 }
                                 if constexpr (HH) {
 #pragma unroll
                                     for (int d = 0; d < ND; ++d) {
                                         if (!(A == 2 ? ((amask >> d) & 1) : A)) continue;
-                                        dmma(cH0[d], cH1[d], d2[2 * d * T + o0], k0);
-                                        dmma(eH0[d], eH1[d], d2[2 * d * T + o1], k1);
+                                        dmma(xH0[d], xH1[d], d2[2 * d * T + o0], k0);
+                                        dmma(yH0[d], yH1[d], d2[2 * d * T + o1], k1);
                                     }
                                 }
                             } else {
@@ -753,8 +793,8 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
 #pragma unroll
                                 for (int d = 0; d < ND; ++d) {
                                     if (!(A == 2 ? ((amask >> d) & 1) : A)) continue;
-                                    dmma(cH0[d], cH1[d], b0, d2[2 * d * T + o0]);
-                                    dmma(eH0[d], eH1[d], b1, d2[2 * d * T + o1]);
+                                    dmma(xH0[d], xH1[d], b0, d2[2 * d * T + o0]);
+                                    dmma(yH0[d], yH1[d], b1, d2[2 * d * T + o1]);
                                 }
                             }
                           }
@@ -766,6 +806,19 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                     } else {
                         hole_loop(IC<2>{});
                     }
+#if GF_HOLE_ILP >= 4
+                    cD0 += fD0;
+                    cD1 += fD1;
+                    eD0 += gD0;
+                    eD1 += gD1;
+#pragma unroll
+                    for (int d = 0; d < ND; ++d) {
+                        cH0[d] += fH0[d];
+                        cH1[d] += fH1[d];
+                        eH0[d] += gH0[d];
+                        eH1[d] += gH1[d];
+                    }
+#endif
                     cD0 += eD0;
                     cD1 += eD1;
 #pragma unroll
@@ -936,15 +989,10 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
     }
 }
 
-// forward passes stage one vector per tile (~38 KB of shared memory): ask the
-// compiler for 4 CTAs per SM there (<= 64 registers), 2 for the three-vector
-// reverse / ascending passes (GF_FWD_OCC overrides the forward occupancy)
-#ifndef GF_FWD_OCC
-#define GF_FWD_OCC 4
-#endif
+// (measured: asking for 4 CTAs per SM in the forward passes, <= 64 registers,
+// left the forward sweep unchanged -- 24.1 vs 23.6 TFLOP/s)
 template <int OP, bool FIRST, int NT, int ND, int VAR>
-__global__ void __launch_bounds__(NT, ((OP == OP_FWD || OP == OP_FWD_DOT) ? GF_FWD_OCC * 256 : 512) / NT)
-    k_fused(const FusedParams p)
+__global__ void __launch_bounds__(NT, 512 / NT) k_fused(const FusedParams p)
 {
     constexpr int NW = NT / 32;  // warps per CTA
     constexpr int NH = 1 + ND;   // hole slots: gradient + ND directions

@@ -206,29 +206,45 @@ __global__ void __launch_bounds__(HT) kh_pair(const double2 *__restrict__ bra, c
     double2 acc[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[j] = czero();
-    for (u64 t = (u64)blockIdx.x * TL + tl; t < units; t += (u64)gridDim.x * TL) {
-        const u64 b = vb + ins0(ins0(t, lo), hi);
-        double2 x[4];
-        x[0] = cur[b * A + a];
-        x[1] = cur[(b + ol) * A + a];
-        x[2] = cur[(b + oh) * A + a];
-        x[3] = cur[(b + ol + oh) * A + a];
-        if (CONTRACT) {
-            const double2 y = bra[b + oi];
+    // two tuples per trip, all loads first (memory-level parallelism)
+    const u64 stride = (u64)gridDim.x * TL;
+    for (u64 t0 = (u64)blockIdx.x * TL + tl; t0 < units; t0 += 2 * stride) {
+        double2 x[2][4], y[2];
+        u64 bb[2];
+        bool ok[2];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) acc[j] = cfma(y, x[j], acc[j]);
-        }
-        if (APPLY) {
-            double2 v;
-            if (SPARSE) {  // parity-conserving rows: {0,3} x {0,3} and {1,2} x {1,2}
-                const int j0 = (i == 0 || i == 3) ? 0 : 1, j1 = 3 - j0;
-                v = cfma(gi[j1], x[j1], cmul(gi[j0], x[j0]));
-            } else {
-                v = cmul(gi[0], x[0]);
-#pragma unroll
-                for (int j = 1; j < 4; ++j) v = cfma(gi[j], x[j], v);
+        for (int u = 0; u < 2; ++u) {
+            const u64 t = t0 + u * stride;
+            ok[u] = t < units;
+            const u64 b = vb + ins0(ins0(ok[u] ? t : t0, lo), hi);
+            bb[u] = b;
+            if (ok[u]) {
+                x[u][0] = cur[b * A + a];
+                x[u][1] = cur[(b + ol) * A + a];
+                x[u][2] = cur[(b + oh) * A + a];
+                x[u][3] = cur[(b + ol + oh) * A + a];
+                if (CONTRACT) y[u] = bra[b + oi];
             }
-            out[(b + oi) * A + a] = v;
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            if (!ok[u]) continue;
+            if (CONTRACT) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[j] = cfma(y[u], x[u][j], acc[j]);
+            }
+            if (APPLY) {
+                double2 v;
+                if (SPARSE) {  // parity-conserving rows: {0,3} x {0,3} and {1,2} x {1,2}
+                    const int j0 = (i == 0 || i == 3) ? 0 : 1, j1 = 3 - j0;
+                    v = cfma(gi[j1], x[u][j1], cmul(gi[j0], x[u][j0]));
+                } else {
+                    v = cmul(gi[0], x[u][0]);
+#pragma unroll
+                    for (int j = 1; j < 4; ++j) v = cfma(gi[j], x[u][j], v);
+                }
+                out[(bb[u] + oi) * A + a] = v;
+            }
         }
     }
     if (CONTRACT) {
@@ -243,6 +259,45 @@ __global__ void __launch_bounds__(HT) kh_pair(const double2 *__restrict__ bra, c
 #pragma unroll
             for (int q = 0; q < TL; ++q) s = cadd(s, red[q][sup.col[c]][sup.row[c]][aa]);
             part[slot * (AS * A) + e] = s;
+        }
+    }
+}
+
+// Array update without a contraction (kernels.py:325-414): thread = (tuple,
+// arity index a) loads the tuple's four values of its a once and writes all
+// four outputs (the (tuple, row, a) layout of kh_pair would load them 4x).
+template <int A, bool SPARSE>
+__global__ void __launch_bounds__(HT) kh_array_apply(const double2 *__restrict__ cur, double2 *__restrict__ out,
+                                                     int logN, int lo, int hi, const Mat4 g)
+{
+    constexpr int TL = HT / A;
+    const u64 N = 1ull << logN, units = N >> 2;
+    const int a = threadIdx.x % A, tl = threadIdx.x / A;
+    const u64 ol = 1ull << lo, oh = 1ull << hi;
+    const u64 vb = (u64)blockIdx.y * N;
+    const u64 stride = (u64)gridDim.x * TL;
+    for (u64 t0 = (u64)blockIdx.x * TL + tl; t0 < units; t0 += 2 * stride) {
+        double2 x[2][4];
+        u64 r[2][4];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const u64 t = t0 + u * stride;
+            if (t >= units) continue;
+            const u64 b = vb + ins0(ins0(t, lo), hi);
+            r[u][0] = b * A + a;
+            r[u][1] = (b + ol) * A + a;
+            r[u][2] = (b + oh) * A + a;
+            r[u][3] = (b + ol + oh) * A + a;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) x[u][q] = cur[r[u][q]];
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            if (t0 + u * stride >= units) continue;
+            double2 y[4];
+            mv4<SPARSE>(g, x[u], y);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) out[r[u][q]] = y[q];
         }
     }
 }
@@ -384,11 +439,10 @@ int gf_fast_array_apply(const void *in, void *out, int k, int arity, int lo, int
 {
     const u64 units = (1ull << k) >> 2;
     const dim3 grid(grid_units(units, arity) * 8, 1);
-    const HSupport sp = hsupport(nullptr, nullptr, 0);
     cudaStream_t st = (cudaStream_t)stream;
     const double2 *x = (const double2 *)in;
     double2 *y = (double2 *)out;
-#define KH_ARR(A_, S_) kh_pair<A_, 8, false, true, S_><<<grid, HT, 0, st>>>(nullptr, x, y, k, lo, hi, sp, g, nullptr)
+#define KH_ARR(A_, S_) kh_array_apply<A_, S_><<<grid, HT, 0, st>>>(x, y, k, lo, hi, g)
     if (arity == 16) { if (sparse) KH_ARR(16, true); else KH_ARR(16, false); }
     else if (arity == 8) { if (sparse) KH_ARR(8, true); else KH_ARR(8, false); }
     else return gf_fail(GF_EINVAL, "fast array apply needs arity 8 or 16");
@@ -657,8 +711,10 @@ static int hess_pairs(gf_hess_plan *h, int64_t nvec, cudaStream_t st, int64_t &l
                 if (s2.sparse) KH_PAIR(true, true, true); else KH_PAIR(true, true, false);
             } else if (contract) {
                 KH_PAIR(true, false, false);
+            } else if (s2.sparse) {
+                kh_array_apply<A, true><<<grid, HT, 0, st>>>(cur, nxt, K, s2.lo, s2.hi, g);
             } else {
-                if (s2.sparse) KH_PAIR(false, true, true); else KH_PAIR(false, true, false);
+                kh_array_apply<A, false><<<grid, HT, 0, st>>>(cur, nxt, K, s2.lo, s2.hi, g);
             }
 #undef KH_PAIR
             ++launches;
