@@ -991,8 +991,13 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
 
 // (measured: asking for 4 CTAs per SM in the forward passes, <= 64 registers,
 // left the forward sweep unchanged -- 24.1 vs 23.6 TFLOP/s)
+// GF_NT512_M11 (experiment): 512-thread CTAs at two per SM for the 2^11-tile
+// passes -- 32 warps per SM instead of 16, at <= 64 registers per thread
+#ifndef GF_NT512_M11
+#define GF_NT512_M11 0
+#endif
 template <int OP, bool FIRST, int NT, int ND, int VAR>
-__global__ void __launch_bounds__(NT, 512 / NT) k_fused(const FusedParams p)
+__global__ void __launch_bounds__(NT, (GF_NT512_M11 && NT == 512) ? 2 : 512 / NT) k_fused(const FusedParams p)
 {
     constexpr int NW = NT / 32;  // warps per CTA
     constexpr int NH = 1 + ND;   // hole slots: gradient + ND directions
@@ -1972,7 +1977,7 @@ static int launch_fused_sp(const gf_plan *p, FusedParams &fp, int64_t nvec, cuda
             return launch_fused_nt<OP, FIRST, 512, 3, VAR>(p, fp, nvec, st);
         }
     }
-    if (fp.m >= 12) return launch_fused_nt<OP, FIRST, 512, 1, VAR>(p, fp, nvec, st);
+    if (fp.m >= 12 || (GF_NT512_M11 && fp.m == 11)) return launch_fused_nt<OP, FIRST, 512, 1, VAR>(p, fp, nvec, st);
     return launch_fused_nt<OP, FIRST, 256, 1, VAR>(p, fp, nvec, st);
 }
 
