@@ -919,7 +919,72 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                           }
                         }
                     };
-                    if constexpr (ND == 1 && (CHI || OP == OP_ASC_H)) {
+                    // Paired parity blocks (sector / parity circuits, one direction):
+                    // G and Z are block diagonal over amplitude pairs E, O, and
+                    // both act on the same input x (bra / psi), so one DMMA per
+                    // block with B = [M1_b | M2_b] yields x' and the Z term, and a
+                    // second with B = [0 | M1_b] adds M1 X: 4 DMMAs per group for
+                    // x' and X' instead of 6.  Lane (g, t) feeds component t&1 of
+                    // amplitude b[t>>1] and receives x' (t < 2) or X' (t >= 2) of
+                    // amplitude b[t&1].
+                    auto pair_loop = [&](auto AC, auto ZC) {
+                        constexpr int A = decltype(AC)::value, Z = decltype(ZC)::value;
+                        const double2 fE = __ldg(&p.frag[PS.fpe * 32 + lane]);
+                        const double2 fO = __ldg(&p.frag[(PS.fpe + 1) * 32 + lane]);
+                        auto offamp = [&](int a) -> unsigned {
+                            return ((a & 2) ? PS.sh : 0u) ^ ((a & 1) ? PS.so : 0u);
+                        };
+                        // block amplitudes: parity {0,3} / {1,2}; C1QD virtual {0,1} / {2,3}
+                        const int eIn = PS.pblk ? (tq >> 1) : ((tq >> 1) ? 3 : 0);
+                        const int oIn = PS.pblk ? 2 + (tq >> 1) : ((tq >> 1) ? 2 : 1);
+                        const int eOut = PS.pblk ? (tq & 1) : ((tq & 1) ? 3 : 0);
+                        const int oOut = PS.pblk ? 2 + (tq & 1) : ((tq & 1) ? 2 : 1);
+                        const unsigned dEi = offamp(eIn) ^ offA, dOi = offamp(oIn) ^ offA;
+                        const unsigned dEo = offamp(eOut) ^ offA, dOo = offamp(oOut) ^ offA;
+                        const int part = tq & 1;
+                        double2 *xt = REV ? t1 : t0;
+                        double2 *Xt = t2;
+                        const double *xd = reinterpret_cast<const double *>(xt);
+                        const double *Xd = reinterpret_cast<const double *>(Xt);
+                        double2 *dE = (tq < 2) ? xt : Xt;
+                        const bool storeX = (tq < 2) || A || Z;
+                        for (unsigned gb = 0; gb < ngrp; gb += 8) {
+                          const unsigned ab = addrA(gb);
+#pragma unroll
+                          for (unsigned u = 0; u < 8; ++u) {
+                            if (gb + u >= ngrp) break;
+                            const unsigned ad = ab ^ gcomb(u) ^ flipA(gb + u);  // lane's own amplitude
+                            const double xe = xd[2 * (ad ^ dEi) + part], xo = xd[2 * (ad ^ dOi) + part];
+                            double Xe = 0.0, Xo = 0.0;
+                            if (A) {
+                                Xe = Xd[2 * (ad ^ dEi) + part];
+                                Xo = Xd[2 * (ad ^ dOi) + part];
+                            }
+                            double e0 = 0.0, e1 = 0.0, o0 = 0.0, o1 = 0.0;
+                            dmma(e0, e1, xe, fE.x);
+                            dmma(o0, o1, xo, fO.x);
+                            if (A) {
+                                dmma(e0, e1, Xe, fE.y);
+                                dmma(o0, o1, Xo, fO.y);
+                            }
+                            if (storeX) {
+                                dE[ad ^ dEo] = make_double2(e0, e1);
+                                dE[ad ^ dOo] = make_double2(o0, o1);
+                            }
+                          }
+                        }
+                    };
+                    if constexpr (C1D && ND == 1 && (CHI || OP == OP_ASC_H)) {
+                        if (PS.pair) {
+                            const bool a = amask & 1, z = zmask & 1;
+                            if (a) pair_loop(IC<1>{}, IC<1>{});  // Z = 0 rows are zero in the fragment
+                            else if (z) pair_loop(IC<0>{}, IC<1>{});
+                            else pair_loop(IC<0>{}, IC<0>{});
+                        }
+                    }
+                    if (C1D && ND == 1 && (CHI || OP == OP_ASC_H) && PS.pair) {
+                        // done above
+                    } else if constexpr (ND == 1 && (CHI || OP == OP_ASC_H)) {
                         const bool a = amask & 1, z = zmask & 1;
                         if (a && z) grp_loop(IC<1>{}, IC<1>{});
                         else if (a) grp_loop(IC<1>{}, IC<0>{});
@@ -1274,6 +1339,7 @@ struct gf_plan {
     bool fused = false;
     bool sparse_fma = true;  // parity-sparse slots as FMA (else dense DMMA with structural zeros)
     bool c1q_dmma = true;    // parity-controlled 1q slots on the DMMA path (PM_C1QD) instead of FMA pairs
+    bool pair_blocks = false; // paired parity-block DMMAs in the update phases (PassSlot::pair; GF_PAIR_BLOCKS=1)
     int fm = 0, fc = 0;
     // geometry only (matrices filled per eval).  The ascending HVP sweep must
     // replay exactly the reverse slot order of the reverse sweep (the two HVP
@@ -1373,6 +1439,28 @@ static void frag_rows_A(const Mat4 &M, double2 *row)
     }
 }
 
+// Paired parity-block B fragments (PassSlot::pair): block b (0 = E, 1 = O) of
+// the amplitude pairs {0,3} / {1,2} (pblk 0) or {0,1} / {2,3} (pblk 1); lane
+// (g, t) holds B[k = t][n = g] for the x input (.x: [M1_b | M2_b]) and the X
+// input (.y: [0 | M1_b]), k = 2 j' + q (input amplitude j' of the block, part
+// q), n = 2 i' + p for n < 4 (x' amplitude i', part p), 4 + 2 i' + p for X'.
+static void frag_rows_pair(const Mat4 &M1, const Mat4 &M2, int pblk, int blk, double2 *row)
+{
+    const int amps[2][2][2] = {{{0, 3}, {1, 2}}, {{0, 1}, {2, 3}}};
+    const int *b = amps[pblk][blk];
+    auto real = [&](const Mat4 &M, int i, int p, int j, int q) {
+        const double2 m = M.m[4 * b[i] + b[j]];
+        return p == q ? m.x : (p == 0 ? -m.y : m.y);
+    };
+    for (int lane = 0; lane < 32; ++lane) {
+        const int n = lane >> 2, k = lane & 3, jj = k >> 1, q = k & 1;
+        const int i = (n & 3) >> 1, pp = n & 1;
+        const double bx = n < 4 ? real(M1, i, pp, jj, q) : real(M2, i, pp, jj, q);
+        const double by = n < 4 ? 0.0 : real(M1, i, pp, jj, q);
+        row[lane] = make_double2(bx, by);
+    }
+}
+
 static int upload_frags(gf_plan *p, cudaStream_t st)
 {
     if (!p->frag_dirty && p->d_frag) return GF_OK;
@@ -1404,6 +1492,13 @@ static int upload_frags(gf_plan *p, cudaStream_t st)
         put(s, FK_GC, p->Gc);
         if ((size_t)s < p->Gd.size()) frag_rows_A(vm(s, p->Gd[s]), &p->h_frag[((size_t)s * NFK + FK_GDA) * 32]);
         if ((size_t)s < p->Gc.size()) frag_rows_A(vm(s, p->Gc[s]), &p->h_frag[((size_t)s * NFK + FK_GCA) * 32]);
+        if ((size_t)s < p->G.size() && p->have_z && (size_t)s < p->Zm[0].size()) {
+            const int pblk = (p->c1q_dmma && p->slots[s].mode_c1q) ? 1 : 0;
+            frag_rows_pair(vm(s, p->Gt[s]), vm(s, p->Ztm[0][s]), pblk, 0, &p->h_frag[((size_t)s * NFK + FK_PRE) * 32]);
+            frag_rows_pair(vm(s, p->Gt[s]), vm(s, p->Ztm[0][s]), pblk, 1, &p->h_frag[((size_t)s * NFK + FK_PRO) * 32]);
+            frag_rows_pair(vm(s, p->G[s]), vm(s, p->Zm[0][s]), pblk, 0, &p->h_frag[((size_t)s * NFK + FK_PAE) * 32]);
+            frag_rows_pair(vm(s, p->G[s]), vm(s, p->Zm[0][s]), pblk, 1, &p->h_frag[((size_t)s * NFK + FK_PAO) * 32]);
+        }
         for (int d = 0; d < FMAXDIR; ++d) {
             put(s, FK_ZT + d, p->Ztm[d]);
             put(s, FK_Z + d, p->Zm[d]);
@@ -1443,6 +1538,7 @@ struct PlanKnobs {
     long long ctas;    // GF_FUSED_CTAS: CTAs per vector (default 148 x 8)
     bool sparse_dmma;  // GF_SPARSE_DMMA: parity-sparse slots on the DMMA path
     bool c1q_dmma;     // GF_C1Q_DMMA: parity-controlled 1q slots on the DMMA path
+    bool pair_blocks;  // GF_PAIR_BLOCKS: paired parity-block DMMAs in the update phases
 };
 
 static PlanKnobs plan_knobs(int K, int tile_bits)
@@ -1463,6 +1559,8 @@ static PlanKnobs plan_knobs(int K, int tile_bits)
     k.sparse_dmma = sd ? atoi(sd) != 0 : GF_SPARSE_DMMA_DEFAULT;
     const char *cq = getenv("GF_C1Q_DMMA");
     k.c1q_dmma = cq ? atoi(cq) != 0 : true;
+    const char *pb = getenv("GF_PAIR_BLOCKS");
+    k.pair_blocks = pb ? atoi(pb) != 0 : false;  // measured slower: c5 5.33 vs 5.01 s, c3 11.4 vs 10.6 ms
     return k;
 }
 
@@ -1531,6 +1629,7 @@ extern "C" int gf_plan_create(gf_plan **out, int k, int sector, int n_slots, con
         p->fc = kn.fc;
         p->sparse_fma = !kn.sparse_dmma;
         p->c1q_dmma = kn.c1q_dmma;
+        p->pair_blocks = kn.pair_blocks;
         if (p->fused) {
             p->fwd_passes = plan_passes(p, false, kn.fwm);
             p->rev_passes = plan_passes(p, true, p->fm);
@@ -1987,7 +2086,7 @@ static int launch_fused(const gf_plan *p, FusedParams &fp, int64_t nvec, cudaStr
     bool spx = false, c1d = false;
     for (int t = 0; t < fp.nslots; ++t) {
         spx |= (fp.ps[t].mode == PM_SPARSE);
-        c1d |= (fp.ps[t].mode == PM_C1QD);
+        c1d |= (fp.ps[t].mode == PM_C1QD) || fp.ps[t].pair;
     }
     switch ((spx ? 1 : 0) | (c1d ? 2 : 0)) {
         case 1: return launch_fused_sp<OP, FIRST, 1>(p, fp, nvec, st, nd);
@@ -2153,6 +2252,11 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
                     fp.ps[t].amask = act_rev;
                     act_rev |= fp.ps[t].zmask;
                     if (fp.ps[t].mode != PM_C1Q && fp.ps[t].mode != PM_C1QD) fp.ps[t].mode = (sp && p->sparse_fma) ? PM_SPARSE : PM_DENSE;
+                    // paired parity blocks: one direction, parity-structured G and Z on the DMMA path
+                    fp.ps[t].pair = h && nd == 1 && p->pair_blocks &&
+                                    (fp.ps[t].mode == PM_C1QD || (fp.ps[t].mode == PM_DENSE && sp));
+                    fp.ps[t].pblk = fp.ps[t].mode == PM_C1QD ? 1 : 0;
+                    fp.ps[t].fpe = s * NFK + FK_PRE;
                 }
                 // after the reverse sweep psi_0 = |j> is known exactly and chi is dead:
                 // the last pass writes back only the bra (needed by the ascending sweep)
@@ -2199,6 +2303,10 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
                         fp.ps[t].amask = act_asc;
                         act_asc |= fp.ps[t].zmask;
                         if (fp.ps[t].mode != PM_C1Q && fp.ps[t].mode != PM_C1QD) fp.ps[t].mode = (sp && p->sparse_fma) ? PM_SPARSE : PM_DENSE;
+                        fp.ps[t].pair = nd == 1 && p->pair_blocks &&
+                                        (fp.ps[t].mode == PM_C1QD || (fp.ps[t].mode == PM_DENSE && sp));
+                        fp.ps[t].pblk = fp.ps[t].mode == PM_C1QD ? 1 : 0;
+                        fp.ps[t].fpe = s * NFK + FK_PAE;
                     }
                     if (pi == nr - 1) fp.store_mask = 0;  // nothing is read after the ascending sweep
                     if (pi == 0) { int rc_ = launch_fused<OP_ASC_H, true>(p, fp, nvec, st, nd); if (rc_) return rc_; }

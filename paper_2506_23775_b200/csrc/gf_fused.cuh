@@ -38,7 +38,12 @@ enum { PM_DENSE = 0, PM_SPARSE = 1, PM_C1Q = 2, PM_C1QD = 3 };
 // gate + hole formulation of the reverse / ascending passes)
 enum {
     FK_G = 0, FK_GD = 1, FK_GT = 2, FK_GC = 3, FK_ZT = 4, FK_Z = 4 + FMAXDIR,
-    FK_GDA = 4 + 2 * FMAXDIR, FK_GCA = 5 + 2 * FMAXDIR, NFK = 6 + 2 * FMAXDIR
+    FK_GDA = 4 + 2 * FMAXDIR, FK_GCA = 5 + 2 * FMAXDIR,
+    // paired parity-block fragments (PassSlot::pair): per block {E, O} one row
+    // (x input, X input) = ([M1_b | M2_b], [0 | M1_b]) for the reverse sweep
+    // (M1 = G^T, M2 = Z^T) and the ascending sweep (M1 = G, M2 = Z)
+    FK_PRE = 6 + 2 * FMAXDIR, FK_PRO = 7 + 2 * FMAXDIR, FK_PAE = 8 + 2 * FMAXDIR, FK_PAO = 9 + 2 * FMAXDIR,
+    NFK = 10 + 2 * FMAXDIR
 };
 
 struct PassSlot {
@@ -50,6 +55,9 @@ struct PassSlot {
     int amask; // bit d: chi_d / v_d is nonzero entering this slot (else its hole and update are skipped)
     int fa, fb, fz;  // fragment-table rows of mat[0], mat[1], mat[2 + d] (fz + d)
     int fa2;         // row of mat[0] in A-operand form (fused gate + hole passes)
+    int pair;        // update phase as two parity-block DMMAs per input (one direction, parity-structured G, Z)
+    int fpe;         // fragment row of the even block (the odd block is fpe + 1)
+    int pblk;        // block amplitudes: 0 = {0,3} / {1,2} (parity gate), 1 = {0,1} / {2,3} (PM_C1QD virtual)
     // 2q slots: col[i] = swz(tuple index 2^i with zeros inserted at llo, lhi),
     // so = swz(2^llo), sh = swz(2^lhi); c1q slots: col[i] = swz(pair index 2^i
     // with a zero inserted at llo), so = swz(2^llo) -- the GF(2)-linear tile
