@@ -1054,6 +1054,305 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
     }
 }
 
+// ---------------------------------------------------------------------------
+// Parity-structured passes on the FP64 FMA pipe (PM_UNIT slots, VAR == 4).
+//
+// A parity-conserving 4x4 gate is two 2x2 blocks (amplitudes {0,3} and {1,2});
+// in a parity sector the gates on the implicit qubit are 2x2 blocks selected
+// by the pair's parity.  Both are *units*: two amplitudes a0, a1 = a0 ^ so and
+// a block selector b that picks the 2x2 block of every slot matrix and the
+// 2x2 sub-block of the 4x4 hole.  An m8n8k4 DMMA cannot skip the zero blocks
+// (it executes twice the algorithmic flops, and B200's DMMA and DFMA share
+// one FP64 datapath), so these passes use FMAs: a lane owns units with a fixed
+// b (lane bit 0; its 2x2 blocks live in registers for the whole slot), loads
+// the unit's amplitudes of psi / bra / chi once, does the gate, the hole
+// accumulations and the updates in registers, and stores them once -- 96 DFMA
+// and 12 conflict-free 128-bit shared accesses per unit of a reverse slot,
+// against 12 DMMAs (= 192 DFMA-equivalents) and 18 wavefronts on the dense
+// path.  B = conj(A) in both sweeps (G^T = conj(G^dag), G = conj(conj G)), so
+// only A and Z are held.
+// ---------------------------------------------------------------------------
+#ifndef GF_UNIT_PIPE
+#define GF_UNIT_PIPE 1  // 128-thread variant: two units per step, the next two loading, blocks from shared memory
+#endif
+__host__ __device__ constexpr bool unit_pipe(int nt) { return GF_UNIT_PIPE && nt <= 128; }
+// shared-memory table of the pass's 2x2 blocks: [slot][b + 2 flip][A00 A01 A10 A11 Z00 Z01 Z10 Z11]
+constexpr size_t UMAT_BYTES = (size_t)FMAXSLOTS * 4 * 8 * sizeof(double2);
+
+// c + conj(a) * b
+__device__ __forceinline__ double2 cfmac(double2 a, double2 b, double2 c)
+{
+    c.x = fma(a.x, b.x, c.x);
+    c.x = fma(a.y, b.y, c.x);
+    c.y = fma(a.x, b.y, c.y);
+    c.y = fma(-a.y, b.x, c.y);
+    return c;
+}
+// conj(a) * b
+__device__ __forceinline__ double2 cmulc(double2 a, double2 b)
+{
+    return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.x, b.y, -a.y * b.x));
+}
+
+template <int OP, int NT>
+__device__ __forceinline__ void run_units(const FusedParams &p, double2 *t0, double2 *t1, double2 *t2, double *scratch,
+                                          const double2 *umat, const u64 pofs, const bool accum, const int tpop,
+                                          const unsigned T)
+{
+    constexpr int NW = NT / 32;
+    constexpr int NWB = NW >= 16 ? 4 : (NW >= 8 ? 3 : (NW >= 4 ? 2 : (NW >= 2 ? 1 : 0)));
+    constexpr bool FWD = (OP == OP_FWD || OP == OP_FWD_DOT);
+    constexpr bool HD = (OP == OP_REV_G || OP == OP_REV_GH);
+    constexpr bool HH = (OP == OP_REV_GH || OP == OP_REV_H || OP == OP_ASC_H);
+    constexpr bool REV = (OP == OP_REV_G || OP == OP_REV_GH || OP == OP_REV_H);
+    constexpr bool CHI = (OP == OP_REV_GH || OP == OP_REV_H);
+    constexpr bool ASC = (OP == OP_ASC_H);
+    constexpr int NH = 2;
+    // 128-thread CTAs (two warps per scheduler) run two units at a time with
+    // the next two units' loads in flight (UNIT_PIPE) and read their 2x2 blocks
+    // from the shared-memory table umat
+    constexpr bool PIPE = unit_pipe(NT);
+    constexpr int NA = PIPE ? 2 : 1;  // independent hole accumulator sets
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int b = lane & 1;
+    // lanes with bit 4 set hold their unit in swapped amplitude order (a0 <-> a1,
+    // the 2x2 blocks permuted to match): their local accumulator (r', s') is
+    // hole entry (r' ^ 1, s' ^ 1), so the first reduce-scatter stage keeps
+    // r' = 0 and sends r' = 1 on every lane -- no selects
+    const int flip = (lane >> 4) & 1;
+    const unsigned nunit = T >> 1;
+    const unsigned TW = max(nunit / (unsigned)NW, 32u);  // units per active warp
+    const unsigned nwa = nunit >> (31 - __clz(TW));
+    const unsigned nit = TW >> 5;  // units per lane: a power of two, <= 8 for every tile shape
+    const int itb = 31 - __clz(nit);
+    const unsigned tpar = (unsigned)((tpop ^ p.sector) & 1);
+    struct Unit {
+        double2 x0, x1, b0, b1, c0, c1;
+        unsigned a0, a1;
+    };
+    for (int si = 0; si < p.nslots; ++si) {
+        const PassSlot &PS = p.ps[si];
+#ifdef GF_CHECKS
+        {
+            const int ub = 31 - __clz(nunit);
+            for (int i = 0; i < ub; ++i) GF_DCHECK(PS.col[i] < T);
+            GF_DCHECK(PS.so < T && PS.so != 0u && PS.mode == PM_UNIT && nit <= 8u);
+        }
+#endif
+        // this CTA's running partial of the slot (tiles after its first): read
+        // early, added after the barrier
+        double prev = 0.0;
+        double *pdst = nullptr;
+        if constexpr (HD || HH) {
+            if (tid < 32 * NH) {
+                const int hole = tid >> 5;
+                if ((hole == 0 && HD) || (hole >= 1 && HH)) {
+                    pdst = (hole == 0 ? p.partD : p.partH) + (u64)PS.slot * p.nvec * p.ctas * 32 + pofs + (tid & 31);
+                    if (accum) prev = *pdst;
+                }
+            }
+        }
+        double2 dD[NA][4], dH[NA][4];
+#pragma unroll
+        for (int k = 0; k < NA; ++k)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) dD[k][i] = dH[k][i] = czero();
+        if ((unsigned)warp < nwa) {
+            double2 a00, a01, a10, a11, z00 = czero(), z01 = czero(), z10 = czero(), z11 = czero();
+            if constexpr (PIPE) {
+                const double2 *mt = umat + (si * 4 + b + 2 * flip) * 8;
+                a00 = mt[0]; a01 = mt[1]; a10 = mt[2]; a11 = mt[3];
+                if constexpr (CHI || ASC) {
+                    z00 = mt[4]; z01 = mt[5]; z10 = mt[6]; z11 = mt[7];
+                }
+            } else {
+                if (flip) sub2(p.mat[si][0], b, a11, a10, a01, a00);
+                else sub2(p.mat[si][0], b, a00, a01, a10, a11);
+                if constexpr (CHI || ASC) {
+                    if (flip) sub2(p.mat[si][2], b, z11, z10, z01, z00);
+                    else sub2(p.mat[si][2], b, z00, z01, z10, z11);
+                }
+            }
+            const unsigned dso = PS.so;
+            unsigned a = ((PS.upar && tpar) ? PS.col[0] : 0u) ^ (flip ? dso : 0u);
+#pragma unroll
+            for (int i = 0; i < 5; ++i)
+                if ((lane >> i) & 1) a ^= PS.col[i];
+#pragma unroll
+            for (int i = 0; i < NWB; ++i)
+                if ((warp >> i) & 1) a ^= PS.col[5 + itb + i];
+            // the lane's units in Gray-code order: one XOR per unit
+            const unsigned g0 = PS.col[5], g1 = PS.col[6], g2 = PS.col[7];
+            unsigned cnt = 0;
+            auto advance = [&]() {
+                ++cnt;
+                a ^= (cnt & 1u) ? g0 : ((cnt & 2u) ? g1 : g2);
+            };
+            auto load = [&](Unit &u) {
+                u.a0 = a;
+                u.a1 = a ^ dso;
+                GF_DCHECK(u.a0 < T && u.a1 < T);
+                u.x0 = t0[u.a0];
+                u.x1 = t0[u.a1];
+                if constexpr (!FWD) {
+                    u.b0 = t1[u.a0];
+                    u.b1 = t1[u.a1];
+                }
+                if constexpr (CHI || ASC) {
+                    u.c0 = t2[u.a0];
+                    u.c1 = t2[u.a1];
+                }
+            };
+            auto work = [&](const Unit &u, double2 *eD, double2 *eH) {
+                if constexpr (FWD) {
+                    t0[u.a0] = cfma(a01, u.x1, cmul(a00, u.x0));
+                    t0[u.a1] = cfma(a11, u.x1, cmul(a10, u.x0));
+                } else if constexpr (REV) {
+                    // psi <- G^dag psi
+                    const double2 y0 = cfma(a01, u.x1, cmul(a00, u.x0));
+                    const double2 y1 = cfma(a11, u.x1, cmul(a10, u.x0));
+                    t0[u.a0] = y0;
+                    t0[u.a1] = y1;
+                    if constexpr (HD) {  // D += hole(bra, psi)
+                        eD[0] = cfma(u.b0, y0, eD[0]);
+                        eD[1] = cfma(u.b0, y1, eD[1]);
+                        eD[2] = cfma(u.b1, y0, eD[2]);
+                        eD[3] = cfma(u.b1, y1, eD[3]);
+                    }
+                    if constexpr (CHI) {  // H += hole(chi, psi); chi <- G^T chi + Z^T bra
+                        eH[0] = cfma(u.c0, y0, eH[0]);
+                        eH[1] = cfma(u.c0, y1, eH[1]);
+                        eH[2] = cfma(u.c1, y0, eH[2]);
+                        eH[3] = cfma(u.c1, y1, eH[3]);
+                        double2 n0 = cfma(z01, u.b1, cmul(z00, u.b0));
+                        double2 n1 = cfma(z11, u.b1, cmul(z10, u.b0));
+                        n0 = cfmac(a01, u.c1, cfmac(a00, u.c0, n0));
+                        n1 = cfmac(a11, u.c1, cfmac(a10, u.c0, n1));
+                        t2[u.a0] = n0;
+                        t2[u.a1] = n1;
+                    }
+                    // bra <- G^T bra
+                    t1[u.a0] = cfmac(a01, u.b1, cmulc(a00, u.b0));
+                    t1[u.a1] = cfmac(a11, u.b1, cmulc(a10, u.b0));
+                } else {
+                    // bra <- conj(G) bra; H += hole(bra, v); v <- G v + Z psi; psi <- G psi
+                    const double2 q0 = cfma(a01, u.b1, cmul(a00, u.b0));
+                    const double2 q1 = cfma(a11, u.b1, cmul(a10, u.b0));
+                    t1[u.a0] = q0;
+                    t1[u.a1] = q1;
+                    eH[0] = cfma(q0, u.c0, eH[0]);
+                    eH[1] = cfma(q0, u.c1, eH[1]);
+                    eH[2] = cfma(q1, u.c0, eH[2]);
+                    eH[3] = cfma(q1, u.c1, eH[3]);
+                    double2 n0 = cfma(z01, u.x1, cmul(z00, u.x0));
+                    double2 n1 = cfma(z11, u.x1, cmul(z10, u.x0));
+                    n0 = cfmac(a01, u.c1, cfmac(a00, u.c0, n0));
+                    n1 = cfmac(a11, u.c1, cfmac(a10, u.c0, n1));
+                    t2[u.a0] = n0;
+                    t2[u.a1] = n1;
+                    t0[u.a0] = cfmac(a01, u.x1, cmulc(a00, u.x0));
+                    t0[u.a1] = cfmac(a11, u.x1, cmulc(a10, u.x0));
+                }
+            };
+            if (PIPE && nit >= 4) {
+                // two units per step (independent FMA chains and accumulator
+                // sets), the next two already loading
+                Unit u0, u1, u2, u3;
+                load(u0);
+                advance();
+                load(u1);
+                advance();
+                for (unsigned it = 0; it < nit; it += 4) {
+                    load(u2);
+                    advance();
+                    load(u3);
+                    advance();
+                    work(u0, dD[0], dH[0]);
+                    work(u1, dD[NA - 1], dH[NA - 1]);
+                    if (it + 4 < nit) {
+                        load(u0);
+                        advance();
+                        load(u1);
+                        advance();
+                    }
+                    work(u2, dD[0], dH[0]);
+                    work(u3, dD[NA - 1], dH[NA - 1]);
+                }
+            } else {
+                for (unsigned it = 0; it < nit; ++it) {
+                    Unit u;
+                    load(u);
+                    work(u, dD[0], dH[0]);
+                    advance();
+                }
+            }
+            if constexpr (NA > 1) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    dD[0][i] = cadd(dD[0][i], dD[NA - 1][i]);
+                    dH[0][i] = cadd(dH[0][i], dH[NA - 1][i]);
+                }
+            }
+        }
+        if constexpr (HD || HH) {
+            // Per hole a lane holds a 2x2 complex block as 8 doubles
+            // v[4 r' + 2 s' + part].  Reduce-scatter over lane bits 4 (r), 3 (s),
+            // 2 (part), then add over bit 1 (fixed order: deterministic); lane
+            // (b4 b3 b2 0 b) owns entry (r, s, part) = (b4, b3, b2) of block b,
+            // i.e. entry (i_r, i_s) of the 4x4 hole, (i_0, i_1) = b ? (1, 2) : (0, 3).
+            // The other 16 lanes write the off-pattern zeros.
+            double *sbuf = scratch + (si & 1) * (NH * NW * 32);
+            auto fold_store = [&](int hole, const double2 d[4]) {
+                double v[4];
+                // bit 4: every lane keeps r' = 0 (its own r).  The partner's flip
+                // is the opposite one, so its s' is reversed too: local (0, s')
+                // pairs with the partner's (1, s' ^ 1)
+                v[0] = d[0].x + __shfl_xor_sync(0xffffffffu, d[3].x, 16);
+                v[1] = d[0].y + __shfl_xor_sync(0xffffffffu, d[3].y, 16);
+                v[2] = d[1].x + __shfl_xor_sync(0xffffffffu, d[2].x, 16);
+                v[3] = d[1].y + __shfl_xor_sync(0xffffffffu, d[2].y, 16);
+                // bit 3: keep s = b3, local s' = b3 ^ flip
+                const bool up3 = (((lane >> 3) ^ flip) & 1) != 0;
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const double send = up3 ? v[i] : v[i + 2];
+                    const double keep = up3 ? v[i + 2] : v[i];
+                    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+                }
+                const bool up2 = (lane & 4) != 0;
+                const double send = up2 ? v[0] : v[1];
+                const double keep = up2 ? v[1] : v[0];
+                double tot = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+                tot += __shfl_xor_sync(0xffffffffu, tot, 2);
+                double *dst = sbuf + (hole * NW + warp) * 32;
+                if (!(lane & 2)) {
+                    const int r = (lane >> 4) & 1, s2 = (lane >> 3) & 1, part = (lane >> 2) & 1;
+                    const int ir = b ? 1 + r : 3 * r, is = b ? 1 + s2 : 3 * s2;
+                    dst[2 * (4 * ir + is) + part] = tot;
+                } else {
+                    // off-pattern complex entries {1, 2, 4, 7, 8, 11, 13, 14}
+                    const int w = ((lane >> 2) & 7) | (b << 3);  // 0..15
+                    const int e = (0xEDB87421u >> (4 * (w >> 1))) & 15;
+                    dst[2 * e + (w & 1)] = 0.0;
+                }
+            };
+            if ((unsigned)warp < nwa) {
+                if constexpr (HD) fold_store(0, dD[0]);
+                if constexpr (HH) fold_store(1, dH[0]);
+            }
+            __syncthreads();
+            if (pdst) {
+                const int hole = tid >> 5, i = tid & 31;
+                double sum = 0.0;
+                for (unsigned ww = 0; ww < nwa; ++ww) sum += sbuf[(hole * NW + ww) * 32 + i];
+                *pdst = prev + sum;
+            }
+        } else {
+            __syncthreads();
+        }
+    }
+}
+
 // (measured: asking for 4 CTAs per SM in the forward passes, <= 64 registers,
 // left the forward sweep unchanged -- 24.1 vs 23.6 TFLOP/s)
 // GF_NT512_M11 (experiment): 512-thread CTAs at two per SM for the 2^11-tile
@@ -1062,7 +1361,8 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
 #define GF_NT512_M11 0
 #endif
 template <int OP, bool FIRST, int NT, int ND, int VAR>
-__global__ void __launch_bounds__(NT, (GF_NT512_M11 && NT == 512) ? 2 : 512 / NT) k_fused(const FusedParams p)
+__global__ void __launch_bounds__(NT, (GF_NT512_M11 && NT == 512) ? 2 : ((VAR == 4 && NT < 256) ? 2 : 512 / NT))
+    k_fused(const FusedParams p)
 {
     constexpr int NW = NT / 32;  // warps per CTA
     constexpr int NH = 1 + ND;   // hole slots: gradient + ND directions
@@ -1079,6 +1379,18 @@ __global__ void __launch_bounds__(NT, (GF_NT512_M11 && NT == 512) ? 2 : 512 / NT
     double *scratch = reinterpret_cast<double *>(t0 + NV * T);  // [NH][NW][64]
     u64 *hiofs = reinterpret_cast<u64 *>(scratch + NH * NW * 64);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double2 *umat = reinterpret_cast<double2 *>(hiofs + (1 << (p.m - p.c)));
+    if constexpr (VAR == 4 && unit_pipe(NT)) {
+        // 2x2 blocks of every slot matrix for block b and both amplitude orders
+        for (int e = tid; e < p.nslots * 32; e += NT) {
+            const int si = e >> 5, var = (e >> 3) & 3, k = e & 7;
+            const int bb = var & 1, fl = var >> 1;
+            const int r = ((k >> 1) & 1) ^ fl, s2 = (k & 1) ^ fl;
+            const int ir = bb ? 1 + r : 3 * r, is = bb ? 1 + s2 : 3 * s2;
+            constexpr bool HASZ = (OP == OP_REV_GH || OP == OP_REV_H || OP == OP_ASC_H);
+            umat[e] = (k < 4) ? p.mat[si][0].m[4 * ir + is] : (HASZ ? p.mat[si][2].m[4 * ir + is] : czero());
+        }
+    }
     const u64 vb = (u64)blockIdx.y * p.N;
     double2 *psi = p.psi + vb;
     double2 *bra = p.bra + vb;
@@ -1154,8 +1466,12 @@ __global__ void __launch_bounds__(NT, (GF_NT512_M11 && NT == 512) ? 2 : 512 / NT
         }
         __syncthreads();
 
-        run_slots<OP, NT, ND, VAR>(p, t0, t1, t2, scratch, ((u64)blockIdx.y * p.ctas + blockIdx.x) * 32,
-                                   tile != blockIdx.x, tpop, T);
+        if constexpr (VAR == 4)
+            run_units<OP, NT>(p, t0, t1, t2, scratch, umat, ((u64)blockIdx.y * p.ctas + blockIdx.x) * 32,
+                              tile != blockIdx.x, tpop, T);
+        else
+            run_slots<OP, NT, ND, VAR>(p, t0, t1, t2, scratch, ((u64)blockIdx.y * p.ctas + blockIdx.x) * 32,
+                                       tile != blockIdx.x, tpop, T);
 
         const int sm = p.store_mask;
         for (unsigned l = tid; l < T && !p.exp_noio; l += NT) {
@@ -1340,6 +1656,8 @@ struct gf_plan {
     bool sparse_fma = true;  // parity-sparse slots as FMA (else dense DMMA with structural zeros)
     bool c1q_dmma = true;    // parity-controlled 1q slots on the DMMA path (PM_C1QD) instead of FMA pairs
     bool pair_blocks = false; // paired parity-block DMMAs in the update phases (PassSlot::pair; GF_PAIR_BLOCKS=1)
+    bool unit_fma = false;    // sector plans: every slot as FP64-FMA units (PM_UNIT, run_units) when nd == 1
+    int unit_nt = 128;        // threads per CTA of the unit passes (GF_UNIT_NT)
     int fm = 0, fc = 0;
     // geometry only (matrices filled per eval).  The ascending HVP sweep must
     // replay exactly the reverse slot order of the reverse sweep (the two HVP
@@ -1524,7 +1842,7 @@ static void plan_free(gf_plan *p)
         if (q) cudaFree(q);
 }
 
-static std::vector<FusedParams> plan_passes(const gf_plan *p, bool reverse, int m);
+static std::vector<FusedParams> plan_passes(const gf_plan *p, bool reverse, int m, bool unit = false);
 
 // Environment knobs of the plan (diagnostics / experiments; the defaults are
 // the measured best), parsed in one place for gf_plan_create and the
@@ -1539,6 +1857,8 @@ struct PlanKnobs {
     bool sparse_dmma;  // GF_SPARSE_DMMA: parity-sparse slots on the DMMA path
     bool c1q_dmma;     // GF_C1Q_DMMA: parity-controlled 1q slots on the DMMA path
     bool pair_blocks;  // GF_PAIR_BLOCKS: paired parity-block DMMAs in the update phases
+    bool sector_fma;   // GF_SECTOR_FMA: parity-sector passes as FP64-FMA units (PM_UNIT)
+    int unit_nt;       // GF_UNIT_NT: threads per CTA of those passes (128 or 256)
 };
 
 static PlanKnobs plan_knobs(int K, int tile_bits)
@@ -1561,6 +1881,10 @@ static PlanKnobs plan_knobs(int K, int tile_bits)
     k.c1q_dmma = cq ? atoi(cq) != 0 : true;
     const char *pb = getenv("GF_PAIR_BLOCKS");
     k.pair_blocks = pb ? atoi(pb) != 0 : false;  // measured slower: c5 5.33 vs 5.01 s, c3 11.4 vs 10.6 ms
+    const char *sf = getenv("GF_SECTOR_FMA");
+    k.sector_fma = sf ? atoi(sf) != 0 : true;
+    const char *un = getenv("GF_UNIT_NT");
+    k.unit_nt = (un && atoi(un) == 256) ? 256 : 128;
     return k;
 }
 
@@ -1630,9 +1954,11 @@ extern "C" int gf_plan_create(gf_plan **out, int k, int sector, int n_slots, con
         p->sparse_fma = !kn.sparse_dmma;
         p->c1q_dmma = kn.c1q_dmma;
         p->pair_blocks = kn.pair_blocks;
+        p->unit_fma = kn.sector_fma && sector >= 0;
+        p->unit_nt = kn.unit_nt;
         if (p->fused) {
-            p->fwd_passes = plan_passes(p, false, kn.fwm);
-            p->rev_passes = plan_passes(p, true, p->fm);
+            p->fwd_passes = plan_passes(p, false, kn.fwm, p->unit_fma);
+            p->rev_passes = plan_passes(p, true, p->fm, p->unit_fma);
             p->asc_passes.assign(p->rev_passes.rbegin(), p->rev_passes.rend());
             for (auto &f : p->asc_passes) std::reverse(f.ps, f.ps + f.nslots);
             if (getenv("GF_DUMP_PLAN")) {  // diagnostic: per-pass local bits and slot targets
@@ -1652,6 +1978,11 @@ extern "C" int gf_plan_create(gf_plan **out, int k, int sector, int n_slots, con
                 p->asc_md.assign(p->rev_md.rbegin(), p->rev_md.rend());
                 for (auto &f : p->asc_md) std::reverse(f.ps, f.ps + f.nslots);
                 mmin = 10;
+            } else if (p->unit_fma) {
+                // multi-direction sweeps stay on the DMMA path: they need their own geometry
+                p->rev_md = plan_passes(p, true, p->fm);
+                p->asc_md.assign(p->rev_md.rbegin(), p->rev_md.rend());
+                for (auto &f : p->asc_md) std::reverse(f.ps, f.ps + f.nslots);
             }
             // CTAs per vector: capacity for the smallest tiles; each launch uses
             // min(capacity, its tiles), one tile per CTA by default
@@ -1912,7 +2243,72 @@ static bool plan_exact(const gf_plan *p, const std::vector<int> &order, int m, i
     return false;
 }
 
-static std::vector<FusedParams> plan_passes(const gf_plan *p, bool reverse, int m)
+// PM_UNIT geometry: the unit-index columns of a slot, ordered so that the three
+// lowest (lane bits 0..2: one quarter-warp of a 128-bit access) are linearly
+// independent modulo the eight 16-byte slots of a 128-byte bank row.
+static void unit_columns(PassSlot &ps, int m, bool c1q)
+{
+    std::vector<unsigned> cols;
+    auto indep = [](unsigned a, unsigned b, unsigned c) {
+        a &= 7u; b &= 7u; c &= 7u;
+        return a && b && c && (a ^ b) && (a ^ c) && (b ^ c) && (a ^ b ^ c);
+    };
+    memset(ps.col, 0, sizeof ps.col);
+    if (!c1q) {
+        for (int i = 0; i < m - 2; ++i) cols.push_back(swz_host(ins0u_host(ins0u_host(1u << i, ps.llo), ps.lhi)));
+        const unsigned so = swz_host(1u << ps.llo), sh = swz_host(1u << ps.lhi);
+        int bi = 0, bj = 1;
+        bool found = false;
+        for (int i = 0; i < (int)cols.size() && !found; ++i)
+            for (int j = i + 1; j < (int)cols.size() && !found; ++j)
+                if (indep(so, cols[i], cols[j])) {
+                    bi = i; bj = j; found = true;
+                }
+        ps.col[0] = so;
+        int n = 1;
+        if (cols.size() >= 2) {
+            ps.col[n++] = cols[bi];
+            ps.col[n++] = cols[bj];
+            for (int i = 0; i < (int)cols.size(); ++i)
+                if (i != bi && i != bj) ps.col[n++] = cols[i];
+        } else {
+            for (unsigned c : cols) ps.col[n++] = c;
+        }
+        ps.so = so ^ sh;  // a1 = a0 ^ (so ^ sh): {00, 11} for b = 0, {01, 10} for b = 1
+        ps.sh = 0;
+        ps.upar = 0;
+    } else {
+        for (int i = 0; i < m - 1; ++i) cols.push_back(swz_host(ins0u_host(1u << i, ps.llo)));
+        int b0 = 0, b1 = 1, b2 = 2;
+        bool found = false;
+        const int nc = (int)cols.size();
+        for (int i = 0; i < nc && !found; ++i)
+            for (int j = i + 1; j < nc && !found; ++j)
+                for (int k = j + 1; k < nc && !found; ++k)
+                    if (indep(cols[i], cols[j], cols[k])) {
+                        b0 = i; b1 = j; b2 = k; found = true;
+                    }
+        // unit u = (j', b): pair index 2 j' + (b ^ parity(j') ^ tile parity ^ sector), so every
+        // other column carries the parity bit's column as well
+        const unsigned c0 = cols[b0];
+        ps.col[0] = c0;
+        int n = 1;
+        if (nc >= 3) {
+            ps.col[n++] = cols[b1] ^ c0;
+            ps.col[n++] = cols[b2] ^ c0;
+            for (int i = 0; i < nc; ++i)
+                if (i != b0 && i != b1 && i != b2) ps.col[n++] = cols[i] ^ c0;
+        } else {
+            for (int i = 0; i < nc; ++i)
+                if (i != b0) ps.col[n++] = cols[i] ^ c0;
+        }
+        ps.so = swz_host(1u << ps.llo);
+        ps.sh = 0;
+        ps.upar = 1;
+    }
+}
+
+static std::vector<FusedParams> plan_passes(const gf_plan *p, bool reverse, int m, bool unit)
 {
     std::vector<FusedParams> out;
     const int n = p->n, K = p->K, c = p->fc;
@@ -2008,7 +2404,10 @@ static std::vector<FusedParams> plan_passes(const gf_plan *p, bool reverse, int 
             ps.mode = si.mode_c1q ? (p->c1q_dmma ? PM_C1QD : PM_C1Q) : PM_DENSE;  // sparse decided per eval
             ps.llo = lidx[si.lo];
             ps.lhi = si.mode_c1q ? 0 : lidx[si.hi];
-            if (ps.mode == PM_C1QD) {
+            if (unit) {
+                ps.mode = PM_UNIT;
+                unit_columns(ps, m, si.mode_c1q != 0);
+            } else if (ps.mode == PM_C1QD) {
                 // virtual partner bit: any other local bit (the lowest one)
                 const int vb = ps.llo == 0 ? 1 : 0, a0 = std::min(ps.llo, vb), a1 = std::max(ps.llo, vb);
                 ps.lhi = vb;
@@ -2042,7 +2441,7 @@ template <int OP, bool FIRST, int NT, int ND, int VAR>
 static int launch_fused_nt(const gf_plan *p, FusedParams &fp, int64_t nvec, cudaStream_t st)
 {
     const int nv = (OP == OP_FWD || OP == OP_FWD_DOT) ? 1 : (OP == OP_REV_G ? 2 : 2 + ND);
-    const size_t smem = fused_smem(nv, fp.m, fp.c, NT / 32, ND);
+    const size_t smem = fused_smem(nv, fp.m, fp.c, NT / 32, ND) + ((VAR == 4 && unit_pipe(NT)) ? UMAT_BYTES : 0);
     // the attribute is per device: set it once for every device this process drives
     static unsigned long long attr_done = 0ull;
     int dev = 0;
@@ -2083,10 +2482,19 @@ static int launch_fused_sp(const gf_plan *p, FusedParams &fp, int64_t nvec, cuda
 template <int OP, bool FIRST>
 static int launch_fused(const gf_plan *p, FusedParams &fp, int64_t nvec, cudaStream_t st, int nd = 1)
 {
-    bool spx = false, c1d = false;
+    bool spx = false, c1d = false, unit = fp.nslots > 0;
     for (int t = 0; t < fp.nslots; ++t) {
         spx |= (fp.ps[t].mode == PM_SPARSE);
         c1d |= (fp.ps[t].mode == PM_C1QD) || fp.ps[t].pair;
+        unit = unit && (fp.ps[t].mode == PM_UNIT);
+    }
+    if (unit) {
+        // parity-structured pass on the FMA pipe (one direction); tiles of 2^12
+        // amplitudes keep the 512-thread shape
+        if (nd != 1) return gf_fail(GF_EINVAL, "unit passes carry one direction");
+        if (fp.m >= 12) return launch_fused_nt<OP, FIRST, 512, 1, 4>(p, fp, nvec, st);
+        if (p->unit_nt == 256) return launch_fused_nt<OP, FIRST, 256, 1, 4>(p, fp, nvec, st);
+        return launch_fused_nt<OP, FIRST, 128, 1, 4>(p, fp, nvec, st);
     }
     switch ((spx ? 1 : 0) | (c1d ? 2 : 0)) {
         case 1: return launch_fused_sp<OP, FIRST, 1>(p, fp, nvec, st, nd);
@@ -2204,7 +2612,7 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
                 fp.ps[t].fa2 = fp.ps[t].fa;
                 fp.ps[t].fb = fp.ps[t].fa;
                 fp.ps[t].fz = fp.ps[t].fa;
-                if (fp.ps[t].mode != PM_C1Q && fp.ps[t].mode != PM_C1QD) fp.ps[t].mode = (p->spG[s] && p->sparse_fma) ? PM_SPARSE : PM_DENSE;
+                if (fp.ps[t].mode != PM_C1Q && fp.ps[t].mode != PM_C1QD && fp.ps[t].mode != PM_UNIT) fp.ps[t].mode = (p->spG[s] && p->sparse_fma) ? PM_SPARSE : PM_DENSE;
             }
             const bool last = !grad_like && pi == nf - 1;
             if (last) ctas_v = fp.ctas;
@@ -2251,7 +2659,7 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
                     }
                     fp.ps[t].amask = act_rev;
                     act_rev |= fp.ps[t].zmask;
-                    if (fp.ps[t].mode != PM_C1Q && fp.ps[t].mode != PM_C1QD) fp.ps[t].mode = (sp && p->sparse_fma) ? PM_SPARSE : PM_DENSE;
+                    if (fp.ps[t].mode != PM_C1Q && fp.ps[t].mode != PM_C1QD && fp.ps[t].mode != PM_UNIT) fp.ps[t].mode = (sp && p->sparse_fma) ? PM_SPARSE : PM_DENSE;
                     // paired parity blocks: one direction, parity-structured G and Z on the DMMA path
                     fp.ps[t].pair = h && nd == 1 && p->pair_blocks &&
                                     (fp.ps[t].mode == PM_C1QD || (fp.ps[t].mode == PM_DENSE && sp));
@@ -2302,7 +2710,7 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
                         }
                         fp.ps[t].amask = act_asc;
                         act_asc |= fp.ps[t].zmask;
-                        if (fp.ps[t].mode != PM_C1Q && fp.ps[t].mode != PM_C1QD) fp.ps[t].mode = (sp && p->sparse_fma) ? PM_SPARSE : PM_DENSE;
+                        if (fp.ps[t].mode != PM_C1Q && fp.ps[t].mode != PM_C1QD && fp.ps[t].mode != PM_UNIT) fp.ps[t].mode = (sp && p->sparse_fma) ? PM_SPARSE : PM_DENSE;
                         fp.ps[t].pair = nd == 1 && p->pair_blocks &&
                                         (fp.ps[t].mode == PM_C1QD || (fp.ps[t].mode == PM_DENSE && sp));
                         fp.ps[t].pblk = fp.ps[t].mode == PM_C1QD ? 1 : 0;

@@ -16,9 +16,9 @@
 //    an 8x8 GEMM with the environment as K, accumulated in 2 registers per
 //    lane; the warps' fragments are summed in a fixed order in shared memory,
 //    so the result is deterministic.
-// Parity-controlled one-qubit slots (the sector's implicit qubit) and, unless
-// GF_SPARSE_DMMA routes them to the DMMA path, parity-sparse two-qubit slots
-// are FP64 FMAs.
+// Parity-structured passes (parity sectors: every slot is parity conserving)
+// run as FP64 FMAs on two-amplitude units instead (PM_UNIT, run_units): half
+// the flops of the dense DMMA form, one shared-memory round trip per slot.
 #pragma once
 #include "gf_common.cuh"
 
@@ -30,7 +30,10 @@ constexpr int FMAXSLOTS = 16;   // max slots per pass (kernel parameter space: 1
 constexpr int FMAXGLOB = 40;
 constexpr int FMAXDIR = 3;      // HVP directions per sweep (full-Hessian columns)
 
-enum { PM_DENSE = 0, PM_SPARSE = 1, PM_C1Q = 2, PM_C1QD = 3 };
+// PM_UNIT: parity-structured slots (parity-conserving 2q gates and the sector's
+// parity-controlled 1q gates) as FP64 FMAs on *units* -- two amplitudes plus a
+// block selector b -- with the whole slot (gate, holes, updates) in registers
+enum { PM_DENSE = 0, PM_SPARSE = 1, PM_C1Q = 2, PM_C1QD = 3, PM_UNIT = 4 };
 
 // rows of the per-slot DMMA fragment table: G, G^dag, G^T, conj G, then Z_d^T
 // and Z_d per direction (row = slot * NFK + kind, 32 lanes per row)
@@ -62,8 +65,14 @@ struct PassSlot {
     // so = swz(2^llo), sh = swz(2^lhi); c1q slots: col[i] = swz(pair index 2^i
     // with a zero inserted at llo), so = swz(2^llo) -- the GF(2)-linear tile
     // addressing, precomputed on the host instead of per slot and lane
+    // PM_UNIT slots: unit index u (bit 0 = block selector b) -> swizzled tile
+    // index of the unit's first amplitude a0 = XOR_i u_i col[i] (^ col[0] when
+    // upar and the tile's parity ^ sector is odd); second amplitude a1 = a0 ^ so.
+    // The host orders the columns so that col[0..2] are independent modulo the
+    // eight 16-byte slots of a bank row (conflict-free 128-bit accesses).
     unsigned col[FMAXM - 1];
     unsigned so, sh;
+    int upar;        // PM_UNIT: parity-controlled 1q slot (block selector = parity of the pair index)
 };
 
 struct FusedParams {
