@@ -1072,12 +1072,9 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
 // path.  B = conj(A) in both sweeps (G^T = conj(G^dag), G = conj(conj G)), so
 // only A and Z are held.
 // ---------------------------------------------------------------------------
-#ifndef GF_UNIT_PIPE
-#define GF_UNIT_PIPE 1  // 128-thread variant: two units per step, the next two loading, blocks from shared memory
+#ifndef GF_UNIT_WIDTH
+#define GF_UNIT_WIDTH 2  // 128-thread variant: units per step (independent chains), as many again loading
 #endif
-__host__ __device__ constexpr bool unit_pipe(int nt) { return GF_UNIT_PIPE && nt <= 128; }
-// shared-memory table of the pass's 2x2 blocks: [slot][b + 2 flip][A00 A01 A10 A11 Z00 Z01 Z10 Z11]
-constexpr size_t UMAT_BYTES = (size_t)FMAXSLOTS * 4 * 8 * sizeof(double2);
 
 // c + conj(a) * b
 __device__ __forceinline__ double2 cfmac(double2 a, double2 b, double2 c)
@@ -1096,11 +1093,9 @@ __device__ __forceinline__ double2 cmulc(double2 a, double2 b)
 
 template <int OP, int NT>
 __device__ __forceinline__ void run_units(const FusedParams &p, double2 *t0, double2 *t1, double2 *t2, double *scratch,
-                                          const double2 *umat, const u64 pofs, const bool accum, const int tpop,
-                                          const unsigned T)
+                                          const u64 pofs, const bool accum, const int tpop, const unsigned T)
 {
     constexpr int NW = NT / 32;
-    constexpr int NWB = NW >= 16 ? 4 : (NW >= 8 ? 3 : (NW >= 4 ? 2 : (NW >= 2 ? 1 : 0)));
     constexpr bool FWD = (OP == OP_FWD || OP == OP_FWD_DOT);
     constexpr bool HD = (OP == OP_REV_G || OP == OP_REV_GH);
     constexpr bool HH = (OP == OP_REV_GH || OP == OP_REV_H || OP == OP_ASC_H);
@@ -1108,21 +1103,18 @@ __device__ __forceinline__ void run_units(const FusedParams &p, double2 *t0, dou
     constexpr bool CHI = (OP == OP_REV_GH || OP == OP_REV_H);
     constexpr bool ASC = (OP == OP_ASC_H);
     constexpr int NH = 2;
-    // 128-thread CTAs (two warps per scheduler) run two units at a time with
-    // the next two units' loads in flight (UNIT_PIPE) and read their 2x2 blocks
-    // from the shared-memory table umat
-    constexpr bool PIPE = unit_pipe(NT);
-    constexpr int NA = PIPE ? 2 : 1;  // independent hole accumulator sets
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int b = lane & 1;
-    // lanes with bit 4 set hold their unit in swapped amplitude order (a0 <-> a1,
-    // the 2x2 blocks permuted to match): their local accumulator (r', s') is
-    // hole entry (r' ^ 1, s' ^ 1), so the first reduce-scatter stage keeps
-    // r' = 0 and sends r' = 1 on every lane -- no selects
-    const int flip = (lane >> 4) & 1;
+    // units per step: 128-thread CTAs (two warps per scheduler) work on two
+    // units at a time with the next two loading; wider CTAs on one with the
+    // next one loading
+    constexpr int W = (NT <= 128) ? GF_UNIT_WIDTH : 1;
+    const int tid = threadIdx.x, lane = tid & 31;
+    // warp-uniform warp index: the block selector b = warp & 1 is uniform, so
+    // the 2x2 blocks of the slot matrices are uniform-register FMA operands
+    const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+    const int b = warp & 1;
     const unsigned nunit = T >> 1;
     const unsigned TW = max(nunit / (unsigned)NW, 32u);  // units per active warp
-    const unsigned nwa = nunit >> (31 - __clz(TW));
+    const unsigned nwa = nunit >> (31 - __clz(TW));      // >= 2 (tiles of >= 2^7 amplitudes)
     const unsigned nit = TW >> 5;  // units per lane: a power of two, <= 8 for every tile shape
     const int itb = 31 - __clz(nit);
     const unsigned tpar = (unsigned)((tpop ^ p.sector) & 1);
@@ -1136,7 +1128,7 @@ __device__ __forceinline__ void run_units(const FusedParams &p, double2 *t0, dou
         {
             const int ub = 31 - __clz(nunit);
             for (int i = 0; i < ub; ++i) GF_DCHECK(PS.col[i] < T);
-            GF_DCHECK(PS.so < T && PS.so != 0u && PS.mode == PM_UNIT && nit <= 8u);
+            GF_DCHECK(PS.so < T && PS.so != 0u && PS.mode == PM_UNIT && nit <= 8u && nwa >= 2u);
         }
 #endif
         // this CTA's running partial of the slot (tiles after its first): read
@@ -1152,37 +1144,34 @@ __device__ __forceinline__ void run_units(const FusedParams &p, double2 *t0, dou
                 }
             }
         }
-        double2 dD[NA][4], dH[NA][4];
+        double2 dD[W][4], dH[W][4];
 #pragma unroll
-        for (int k = 0; k < NA; ++k)
+        for (int k = 0; k < W; ++k)
 #pragma unroll
             for (int i = 0; i < 4; ++i) dD[k][i] = dH[k][i] = czero();
         if ((unsigned)warp < nwa) {
-            double2 a00, a01, a10, a11, z00 = czero(), z01 = czero(), z10 = czero(), z11 = czero();
-            if constexpr (PIPE) {
-                const double2 *mt = umat + (si * 4 + b + 2 * flip) * 8;
-                a00 = mt[0]; a01 = mt[1]; a10 = mt[2]; a11 = mt[3];
-                if constexpr (CHI || ASC) {
-                    z00 = mt[4]; z01 = mt[5]; z10 = mt[6]; z11 = mt[7];
-                }
-            } else {
-                if (flip) sub2(p.mat[si][0], b, a11, a10, a01, a00);
-                else sub2(p.mat[si][0], b, a00, a01, a10, a11);
-                if constexpr (CHI || ASC) {
-                    if (flip) sub2(p.mat[si][2], b, z11, z10, z01, z00);
-                    else sub2(p.mat[si][2], b, z00, z01, z10, z11);
-                }
+            // block b of A = mat[0] and Z = mat[2]: rows / columns {0, 3} or {1, 2}
+            const int i0 = b ? 1 : 0, i1 = b ? 2 : 3;
+            const Mat4 &MA = p.mat[si][0];
+            const double2 a00 = MA.m[4 * i0 + i0], a01 = MA.m[4 * i0 + i1];
+            const double2 a10 = MA.m[4 * i1 + i0], a11 = MA.m[4 * i1 + i1];
+            double2 z00 = czero(), z01 = czero(), z10 = czero(), z11 = czero();
+            if constexpr (CHI || ASC) {
+                const Mat4 &MZ = p.mat[si][2];
+                z00 = MZ.m[4 * i0 + i0]; z01 = MZ.m[4 * i0 + i1];
+                z10 = MZ.m[4 * i1 + i0]; z11 = MZ.m[4 * i1 + i1];
             }
             const unsigned dso = PS.so;
-            unsigned a = ((PS.upar && tpar) ? PS.col[0] : 0u) ^ (flip ? dso : 0u);
+            // unit index = [warp >> 1][unit of the lane][lane][b]
+            unsigned a = ((PS.upar && tpar) ? PS.col[0] : 0u) ^ (b ? PS.col[0] : 0u);
 #pragma unroll
             for (int i = 0; i < 5; ++i)
-                if ((lane >> i) & 1) a ^= PS.col[i];
+                if ((lane >> i) & 1) a ^= PS.col[1 + i];
 #pragma unroll
-            for (int i = 0; i < NWB; ++i)
-                if ((warp >> i) & 1) a ^= PS.col[5 + itb + i];
+            for (int i = 0; i < 3; ++i)
+                if ((warp >> (1 + i)) & 1) a ^= PS.col[min(6 + itb + i, FMAXM - 2)];
             // the lane's units in Gray-code order: one XOR per unit
-            const unsigned g0 = PS.col[5], g1 = PS.col[6], g2 = PS.col[7];
+            const unsigned g0 = PS.col[6], g1 = PS.col[7], g2 = PS.col[8];
             unsigned cnt = 0;
             auto advance = [&]() {
                 ++cnt;
@@ -1202,6 +1191,7 @@ __device__ __forceinline__ void run_units(const FusedParams &p, double2 *t0, dou
                     u.c0 = t2[u.a0];
                     u.c1 = t2[u.a1];
                 }
+                advance();
             };
             auto work = [&](const Unit &u, double2 *eD, double2 *eH) {
                 if constexpr (FWD) {
@@ -1254,87 +1244,62 @@ __device__ __forceinline__ void run_units(const FusedParams &p, double2 *t0, dou
                     t0[u.a1] = cfmac(a11, u.x1, cmulc(a10, u.x0));
                 }
             };
-            if (PIPE && nit >= 4) {
-                // two units per step (independent FMA chains and accumulator
-                // sets), the next two already loading
-                Unit u0, u1, u2, u3;
-                load(u0);
-                advance();
-                load(u1);
-                advance();
-                for (unsigned it = 0; it < nit; it += 4) {
-                    load(u2);
-                    advance();
-                    load(u3);
-                    advance();
-                    work(u0, dD[0], dH[0]);
-                    work(u1, dD[NA - 1], dH[NA - 1]);
-                    if (it + 4 < nit) {
-                        load(u0);
-                        advance();
-                        load(u1);
-                        advance();
+            if (nit >= 2u * W) {
+                // W units per step (independent FMA chains and accumulator
+                // sets), the next W already loading
+                Unit u[2][W];
+#pragma unroll
+                for (int k = 0; k < W; ++k) load(u[0][k]);
+                for (unsigned it = 0; it < nit; it += 2 * W) {
+#pragma unroll
+                    for (int k = 0; k < W; ++k) load(u[1][k]);
+#pragma unroll
+                    for (int k = 0; k < W; ++k) work(u[0][k], dD[k], dH[k]);
+                    if (it + 2 * W < nit) {
+#pragma unroll
+                        for (int k = 0; k < W; ++k) load(u[0][k]);
                     }
-                    work(u2, dD[0], dH[0]);
-                    work(u3, dD[NA - 1], dH[NA - 1]);
+#pragma unroll
+                    for (int k = 0; k < W; ++k) work(u[1][k], dD[k], dH[k]);
                 }
             } else {
                 for (unsigned it = 0; it < nit; ++it) {
                     Unit u;
                     load(u);
                     work(u, dD[0], dH[0]);
-                    advance();
                 }
             }
-            if constexpr (NA > 1) {
+            if constexpr (W > 1) {
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                    dD[0][i] = cadd(dD[0][i], dD[NA - 1][i]);
-                    dH[0][i] = cadd(dH[0][i], dH[NA - 1][i]);
+                    dD[0][i] = cadd(dD[0][i], dD[W - 1][i]);
+                    dH[0][i] = cadd(dH[0][i], dH[W - 1][i]);
                 }
             }
         }
         if constexpr (HD || HH) {
-            // Per hole a lane holds a 2x2 complex block as 8 doubles
-            // v[4 r' + 2 s' + part].  Reduce-scatter over lane bits 4 (r), 3 (s),
-            // 2 (part), then add over bit 1 (fixed order: deterministic); lane
-            // (b4 b3 b2 0 b) owns entry (r, s, part) = (b4, b3, b2) of block b,
-            // i.e. entry (i_r, i_s) of the 4x4 hole, (i_0, i_1) = b ? (1, 2) : (0, 3).
-            // The other 16 lanes write the off-pattern zeros.
-            double *sbuf = scratch + (si & 1) * (NH * NW * 32);
+            // Per hole a lane holds the 2x2 complex block of the warp's b as 8
+            // doubles v[4 r + 2 s + part].  Reduce-scatter over lane bits 4 (r),
+            // 3 (s), 2 (part), then add over bits 1 and 0 (fixed order:
+            // deterministic); lanes (b4 b3 b2 0 0) write entry (r, s, part) to
+            // scratch[hole][warp][8].  Entry (r, s) of block b is entry
+            // (i_r, i_s) of the 4x4 hole, (i_0, i_1) = b ? (1, 2) : (0, 3).
+            double *sbuf = scratch + (si & 1) * (NH * NW * 8);
             auto fold_store = [&](int hole, const double2 d[4]) {
-                double v[4];
-                // bit 4: every lane keeps r' = 0 (its own r).  The partner's flip
-                // is the opposite one, so its s' is reversed too: local (0, s')
-                // pairs with the partner's (1, s' ^ 1)
-                v[0] = d[0].x + __shfl_xor_sync(0xffffffffu, d[3].x, 16);
-                v[1] = d[0].y + __shfl_xor_sync(0xffffffffu, d[3].y, 16);
-                v[2] = d[1].x + __shfl_xor_sync(0xffffffffu, d[2].x, 16);
-                v[3] = d[1].y + __shfl_xor_sync(0xffffffffu, d[2].y, 16);
-                // bit 3: keep s = b3, local s' = b3 ^ flip
-                const bool up3 = (((lane >> 3) ^ flip) & 1) != 0;
+                double v[8] = {d[0].x, d[0].y, d[1].x, d[1].y, d[2].x, d[2].y, d[3].x, d[3].y};
 #pragma unroll
-                for (int i = 0; i < 2; ++i) {
-                    const double send = up3 ? v[i] : v[i + 2];
-                    const double keep = up3 ? v[i + 2] : v[i];
-                    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+                for (int s = 16, half = 4; s >= 4; s >>= 1, half >>= 1) {
+                    const bool upper = (lane & s) != 0;
+#pragma unroll
+                    for (int i = 0; i < half; ++i) {
+                        const double send = upper ? v[i] : v[i + half];
+                        const double keep = upper ? v[i + half] : v[i];
+                        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+                    }
                 }
-                const bool up2 = (lane & 4) != 0;
-                const double send = up2 ? v[0] : v[1];
-                const double keep = up2 ? v[1] : v[0];
-                double tot = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-                tot += __shfl_xor_sync(0xffffffffu, tot, 2);
-                double *dst = sbuf + (hole * NW + warp) * 32;
-                if (!(lane & 2)) {
-                    const int r = (lane >> 4) & 1, s2 = (lane >> 3) & 1, part = (lane >> 2) & 1;
-                    const int ir = b ? 1 + r : 3 * r, is = b ? 1 + s2 : 3 * s2;
-                    dst[2 * (4 * ir + is) + part] = tot;
-                } else {
-                    // off-pattern complex entries {1, 2, 4, 7, 8, 11, 13, 14}
-                    const int w = ((lane >> 2) & 7) | (b << 3);  // 0..15
-                    const int e = (0xEDB87421u >> (4 * (w >> 1))) & 15;
-                    dst[2 * e + (w & 1)] = 0.0;
-                }
+                double tot = v[0] + __shfl_xor_sync(0xffffffffu, v[0], 2);
+                tot += __shfl_xor_sync(0xffffffffu, tot, 1);
+                if (!(lane & 3)) sbuf[(hole * NW + warp) * 8 + (lane >> 2)] = tot;
             };
             if ((unsigned)warp < nwa) {
                 if constexpr (HD) fold_store(0, dD[0]);
@@ -1343,8 +1308,13 @@ __device__ __forceinline__ void run_units(const FusedParams &p, double2 *t0, dou
             __syncthreads();
             if (pdst) {
                 const int hole = tid >> 5, i = tid & 31;
+                const int row = i >> 3, colm = (i >> 1) & 3, part = i & 1;
+                const int rb = (row == 1 || row == 2), cb = (colm == 1 || colm == 2);
                 double sum = 0.0;
-                for (unsigned ww = 0; ww < nwa; ++ww) sum += sbuf[(hole * NW + ww) * 32 + i];
+                if (rb == cb) {  // on-pattern entry of block rb
+                    const int q = 4 * (row >> 1) + 2 * (colm >> 1) + part;  // r = (row >= 2), s = (col >= 2)
+                    for (unsigned ww = rb; ww < nwa; ww += 2) sum += sbuf[(hole * NW + ww) * 8 + q];
+                }
                 *pdst = prev + sum;
             }
         } else {
@@ -1379,18 +1349,6 @@ __global__ void __launch_bounds__(NT, (GF_NT512_M11 && NT == 512) ? 2 : ((VAR ==
     double *scratch = reinterpret_cast<double *>(t0 + NV * T);  // [NH][NW][64]
     u64 *hiofs = reinterpret_cast<u64 *>(scratch + NH * NW * 64);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    double2 *umat = reinterpret_cast<double2 *>(hiofs + (1 << (p.m - p.c)));
-    if constexpr (VAR == 4 && unit_pipe(NT)) {
-        // 2x2 blocks of every slot matrix for block b and both amplitude orders
-        for (int e = tid; e < p.nslots * 32; e += NT) {
-            const int si = e >> 5, var = (e >> 3) & 3, k = e & 7;
-            const int bb = var & 1, fl = var >> 1;
-            const int r = ((k >> 1) & 1) ^ fl, s2 = (k & 1) ^ fl;
-            const int ir = bb ? 1 + r : 3 * r, is = bb ? 1 + s2 : 3 * s2;
-            constexpr bool HASZ = (OP == OP_REV_GH || OP == OP_REV_H || OP == OP_ASC_H);
-            umat[e] = (k < 4) ? p.mat[si][0].m[4 * ir + is] : (HASZ ? p.mat[si][2].m[4 * ir + is] : czero());
-        }
-    }
     const u64 vb = (u64)blockIdx.y * p.N;
     double2 *psi = p.psi + vb;
     double2 *bra = p.bra + vb;
@@ -1467,7 +1425,7 @@ __global__ void __launch_bounds__(NT, (GF_NT512_M11 && NT == 512) ? 2 : ((VAR ==
         __syncthreads();
 
         if constexpr (VAR == 4)
-            run_units<OP, NT>(p, t0, t1, t2, scratch, umat, ((u64)blockIdx.y * p.ctas + blockIdx.x) * 32,
+            run_units<OP, NT>(p, t0, t1, t2, scratch, ((u64)blockIdx.y * p.ctas + blockIdx.x) * 32,
                               tile != blockIdx.x, tpop, T);
         else
             run_slots<OP, NT, ND, VAR>(p, t0, t1, t2, scratch, ((u64)blockIdx.y * p.ctas + blockIdx.x) * 32,
@@ -1954,7 +1912,8 @@ extern "C" int gf_plan_create(gf_plan **out, int k, int sector, int n_slots, con
         p->sparse_fma = !kn.sparse_dmma;
         p->c1q_dmma = kn.c1q_dmma;
         p->pair_blocks = kn.pair_blocks;
-        p->unit_fma = kn.sector_fma && sector >= 0;
+        // (tiles of >= 2^7 amplitudes: the kernel gives each block selector its own warps)
+        p->unit_fma = kn.sector_fma && sector >= 0 && p->fm >= 7 && kn.fwm >= 7;
         p->unit_nt = kn.unit_nt;
         if (p->fused) {
             p->fwd_passes = plan_passes(p, false, kn.fwm, p->unit_fma);
@@ -2243,9 +2202,10 @@ static bool plan_exact(const gf_plan *p, const std::vector<int> &order, int m, i
     return false;
 }
 
-// PM_UNIT geometry: the unit-index columns of a slot, ordered so that the three
-// lowest (lane bits 0..2: one quarter-warp of a 128-bit access) are linearly
-// independent modulo the eight 16-byte slots of a 128-byte bank row.
+// PM_UNIT geometry: the unit-index columns of a slot.  col[0] is the block
+// selector's column (warp-uniform in the kernel); col[1..3] (lane bits 0..2:
+// one quarter-warp of a 128-bit access) are chosen linearly independent modulo
+// the eight 16-byte slots of a 128-byte bank row.
 static void unit_columns(PassSlot &ps, int m, bool c1q)
 {
     std::vector<unsigned> cols;
@@ -2254,57 +2214,43 @@ static void unit_columns(PassSlot &ps, int m, bool c1q)
         return a && b && c && (a ^ b) && (a ^ c) && (b ^ c) && (a ^ b ^ c);
     };
     memset(ps.col, 0, sizeof ps.col);
+    unsigned c0;
     if (!c1q) {
         for (int i = 0; i < m - 2; ++i) cols.push_back(swz_host(ins0u_host(ins0u_host(1u << i, ps.llo), ps.lhi)));
         const unsigned so = swz_host(1u << ps.llo), sh = swz_host(1u << ps.lhi);
-        int bi = 0, bj = 1;
-        bool found = false;
-        for (int i = 0; i < (int)cols.size() && !found; ++i)
-            for (int j = i + 1; j < (int)cols.size() && !found; ++j)
-                if (indep(so, cols[i], cols[j])) {
-                    bi = i; bj = j; found = true;
-                }
-        ps.col[0] = so;
-        int n = 1;
-        if (cols.size() >= 2) {
-            ps.col[n++] = cols[bi];
-            ps.col[n++] = cols[bj];
-            for (int i = 0; i < (int)cols.size(); ++i)
-                if (i != bi && i != bj) ps.col[n++] = cols[i];
-        } else {
-            for (unsigned c : cols) ps.col[n++] = c;
-        }
+        c0 = so;
         ps.so = so ^ sh;  // a1 = a0 ^ (so ^ sh): {00, 11} for b = 0, {01, 10} for b = 1
-        ps.sh = 0;
         ps.upar = 0;
     } else {
-        for (int i = 0; i < m - 1; ++i) cols.push_back(swz_host(ins0u_host(1u << i, ps.llo)));
-        int b0 = 0, b1 = 1, b2 = 2;
-        bool found = false;
-        const int nc = (int)cols.size();
-        for (int i = 0; i < nc && !found; ++i)
-            for (int j = i + 1; j < nc && !found; ++j)
-                for (int k = j + 1; k < nc && !found; ++k)
-                    if (indep(cols[i], cols[j], cols[k])) {
-                        b0 = i; b1 = j; b2 = k; found = true;
-                    }
         // unit u = (j', b): pair index 2 j' + (b ^ parity(j') ^ tile parity ^ sector), so every
         // other column carries the parity bit's column as well
-        const unsigned c0 = cols[b0];
-        ps.col[0] = c0;
-        int n = 1;
-        if (nc >= 3) {
-            ps.col[n++] = cols[b1] ^ c0;
-            ps.col[n++] = cols[b2] ^ c0;
-            for (int i = 0; i < nc; ++i)
-                if (i != b0 && i != b1 && i != b2) ps.col[n++] = cols[i] ^ c0;
-        } else {
-            for (int i = 0; i < nc; ++i)
-                if (i != b0) ps.col[n++] = cols[i] ^ c0;
-        }
+        for (int i = 0; i < m - 1; ++i) cols.push_back(swz_host(ins0u_host(1u << i, ps.llo)));
+        c0 = cols[0];
+        cols.erase(cols.begin());
+        for (unsigned &c : cols) c ^= c0;
         ps.so = swz_host(1u << ps.llo);
-        ps.sh = 0;
         ps.upar = 1;
+    }
+    ps.sh = 0;
+    const int nc = (int)cols.size();
+    int b0 = 0, b1 = 1, b2 = 2;
+    bool found = false;
+    for (int i = 0; i < nc && !found; ++i)
+        for (int j = i + 1; j < nc && !found; ++j)
+            for (int k = j + 1; k < nc && !found; ++k)
+                if (indep(cols[i], cols[j], cols[k])) {
+                    b0 = i; b1 = j; b2 = k; found = true;
+                }
+    ps.col[0] = c0;
+    int n = 1;
+    if (nc >= 3) {
+        ps.col[n++] = cols[b0];
+        ps.col[n++] = cols[b1];
+        ps.col[n++] = cols[b2];
+        for (int i = 0; i < nc; ++i)
+            if (i != b0 && i != b1 && i != b2) ps.col[n++] = cols[i];
+    } else {
+        for (unsigned c : cols) ps.col[n++] = c;
     }
 }
 
@@ -2441,7 +2387,7 @@ template <int OP, bool FIRST, int NT, int ND, int VAR>
 static int launch_fused_nt(const gf_plan *p, FusedParams &fp, int64_t nvec, cudaStream_t st)
 {
     const int nv = (OP == OP_FWD || OP == OP_FWD_DOT) ? 1 : (OP == OP_REV_G ? 2 : 2 + ND);
-    const size_t smem = fused_smem(nv, fp.m, fp.c, NT / 32, ND) + ((VAR == 4 && unit_pipe(NT)) ? UMAT_BYTES : 0);
+    const size_t smem = fused_smem(nv, fp.m, fp.c, NT / 32, ND);
     // the attribute is per device: set it once for every device this process drives
     static unsigned long long attr_done = 0ull;
     int dev = 0;
