@@ -1091,9 +1091,32 @@ __device__ __forceinline__ double2 cmulc(double2 a, double2 b)
     return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.x, b.y, -a.y * b.x));
 }
 
+// First-unit tile index of every (slot, thread) of a unit pass: unit index =
+// [warp >> 1][unit of the lane][lane][b = warp & 1], address = XOR of the
+// slot's columns over its set bits (tile-invariant; shared memory table).
+template <int NT>
+__device__ __forceinline__ void unit_bases(const FusedParams &p, unsigned short *ubase, const unsigned T)
+{
+    constexpr int NW = NT / 32;
+    const unsigned nunit = T >> 1;
+    const unsigned TW = max(nunit / (unsigned)NW, 32u);
+    const int itb = 31 - __clz(TW >> 5);
+    for (int e = threadIdx.x; e < p.nslots * NT; e += NT) {
+        const int si = e / NT, t = e % NT, lane = t & 31, warp = t >> 5;
+        const PassSlot &PS = p.ps[si];
+        unsigned a = (warp & 1) ? PS.col[0] : 0u;
+        for (int i = 0; i < 5; ++i)
+            if ((lane >> i) & 1) a ^= PS.col[1 + i];
+        for (int i = 0; i < 3; ++i)
+            if ((warp >> (1 + i)) & 1) a ^= PS.col[min(6 + itb + i, FMAXM - 2)];
+        ubase[e] = (unsigned short)a;
+    }
+}
+
 template <int OP, int NT>
 __device__ __forceinline__ void run_units(const FusedParams &p, double2 *t0, double2 *t1, double2 *t2, double *scratch,
-                                          const u64 pofs, const bool accum, const int tpop, const unsigned T)
+                                          const unsigned short *ubase, const u64 pofs, const bool accum,
+                                          const int tpop, const unsigned T)
 {
     constexpr int NW = NT / 32;
     constexpr bool FWD = (OP == OP_FWD || OP == OP_FWD_DOT);
@@ -1163,13 +1186,9 @@ __device__ __forceinline__ void run_units(const FusedParams &p, double2 *t0, dou
             }
             const unsigned dso = PS.so;
             // unit index = [warp >> 1][unit of the lane][lane][b]
-            unsigned a = ((PS.upar && tpar) ? PS.col[0] : 0u) ^ (b ? PS.col[0] : 0u);
-#pragma unroll
-            for (int i = 0; i < 5; ++i)
-                if ((lane >> i) & 1) a ^= PS.col[1 + i];
-#pragma unroll
-            for (int i = 0; i < 3; ++i)
-                if ((warp >> (1 + i)) & 1) a ^= PS.col[min(6 + itb + i, FMAXM - 2)];
+            // (tabulated once per CTA by unit_bases; parity-controlled slots
+            // add the tile's parity)
+            unsigned a = (unsigned)ubase[si * NT + tid] ^ ((PS.upar && tpar) ? PS.col[0] : 0u);
             // the lane's units in Gray-code order: one XOR per unit
             const unsigned g0 = PS.col[6], g1 = PS.col[7], g2 = PS.col[8];
             unsigned cnt = 0;
@@ -1346,9 +1365,12 @@ __global__ void __launch_bounds__(NT, (GF_NT512_M11 && NT == 512) ? 2 : ((VAR ==
     double2 *t0 = reinterpret_cast<double2 *>(fsm);  // psi
     double2 *t1 = t0 + T;                            // bra
     double2 *t2 = t0 + 2 * T;                        // chi_d (REV) / v_d (ASC), ND tiles
-    double *scratch = reinterpret_cast<double *>(t0 + NV * T);  // [NH][NW][64]
-    u64 *hiofs = reinterpret_cast<u64 *>(scratch + NH * NW * 64);
+    double *scratch = reinterpret_cast<double *>(t0 + NV * T);  // [NH][NW][64]; unit passes [2][NH][NW][8]
+    u64 *hiofs = reinterpret_cast<u64 *>(scratch + (VAR == 4 ? 2 * NH * NW * 8 : NH * NW * 64));
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // unit passes: per-(slot, thread) tile index of the thread's first unit
+    unsigned short *ubase = reinterpret_cast<unsigned short *>(hiofs + (1 << (p.m - p.c)));
+    if constexpr (VAR == 4) unit_bases<NT>(p, ubase, T);
     const u64 vb = (u64)blockIdx.y * p.N;
     double2 *psi = p.psi + vb;
     double2 *bra = p.bra + vb;
@@ -1370,40 +1392,46 @@ __global__ void __launch_bounds__(NT, (GF_NT512_M11 && NT == 512) ? 2 : ((VAR ==
     const unsigned stid = swz((unsigned)tid);
     auto sw = [&](unsigned l) { return stid ^ swz(l ^ (unsigned)tid); };
 
-    for (u64 tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+    // the first forward and first ascending passes start from psi_0 = |j>
+    constexpr bool SYNTH = (OP == OP_FWD || OP == OP_FWD_DOT || OP == OP_ASC_H) && FIRST;
+    const u64 jb = SYNTH ? (u64)p.basis[blockIdx.y] : 0ull;
+    auto tile_base = [&](u64 tile) {
         u64 base = 0;
         for (int i = 0; i < p.nglob; ++i)
             if ((tile >> i) & 1ull) base |= 1ull << p.gpos[i];
-        const int tpop = __popcll(tile);
-        // the first forward and first ascending passes start from psi_0 = |j>
-        constexpr bool SYNTH = (OP == OP_FWD || OP == OP_FWD_DOT || OP == OP_ASC_H) && FIRST;
-        const u64 jb = SYNTH ? (u64)p.basis[blockIdx.y] : 0ull;
-        // Plain copies go global -> shared with cp.async (no register round
-        // trip, every element of the tile in flight at once); the synthesised
-        // |j>, the zero chi/v and the weighted phi0 are written by the threads.
-        if (p.exp_noio) {
-            for (unsigned l = tid; l < NV * T; l += NT) t0[l] = czero();
+        return base;
+    };
+    // Element l of a tile: plain copies go global -> shared with cp.async (no
+    // register round trip, every element in flight at once); the synthesised
+    // |j> and the zero chi / v are written by the thread.
+    auto load_elem = [&](u64 a, unsigned sl) {
+        GF_DCHECK(a < p.N && sl < T);
+        if constexpr (SYNTH)
+            t0[sl] = make_double2(a == jb ? 1.0 : 0.0, 0.0);  // psi_0 = |j>, no HBM read
+        else
+            cp_async16(&t0[sl], &psi[a]);
+        if constexpr (NV >= 2) {
+            if constexpr (!(REV && FIRST)) cp_async16(&t1[sl], &bra[a]);
         }
-        for (unsigned l = tid; l < T && !p.exp_noio; l += NT) {
-            const u64 a = base + (l & cmask) + hiofs[l >> c];
-            const unsigned sl = sw(l);
-            GF_DCHECK(a < p.N && sl < T);
-            if constexpr (SYNTH)
-                t0[sl] = make_double2(a == jb ? 1.0 : 0.0, 0.0);  // psi_0 = |j>, no HBM read
-            else
-                cp_async16(&t0[sl], &psi[a]);
-            if constexpr (NV >= 2) {
-                if constexpr (!(REV && FIRST)) cp_async16(&t1[sl], &bra[a]);
-            }
-            if constexpr (NV >= 3) {
+        if constexpr (NV >= 3) {
 #pragma unroll
-                for (int d = 0; d < ND; ++d) {
-                    if constexpr (FIRST) t2[d * T + sl] = czero();
-                    else cp_async16(&t2[d * T + sl], &aux[a + d * p.auxstride]);
-                }
+            for (int d = 0; d < ND; ++d) {
+                if constexpr (FIRST) t2[d * T + sl] = czero();
+                else cp_async16(&t2[d * T + sl], &aux[a + d * p.auxstride]);
             }
         }
-        cp_async_commit();
+    };
+    if (p.exp_noio) {
+        for (unsigned l = tid; l < NV * T; l += NT) t0[l] = czero();
+    } else if (blockIdx.x < p.ntiles) {
+        const u64 base = tile_base(blockIdx.x);
+        for (unsigned l = tid; l < T; l += NT) load_elem(base + (l & cmask) + hiofs[l >> c], sw(l));
+    }
+    cp_async_commit();
+
+    for (u64 tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+        const u64 base = tile_base(tile);
+        const int tpop = __popcll(tile);
         if constexpr (REV && FIRST) {
             // bra_0 = w phi0; the value <phi0|psi_n> is read back from the tile
             for (unsigned l = tid; l < T; l += NT) {
@@ -1425,15 +1453,24 @@ __global__ void __launch_bounds__(NT, (GF_NT512_M11 && NT == 512) ? 2 : ((VAR ==
         __syncthreads();
 
         if constexpr (VAR == 4)
-            run_units<OP, NT>(p, t0, t1, t2, scratch, ((u64)blockIdx.y * p.ctas + blockIdx.x) * 32,
+            run_units<OP, NT>(p, t0, t1, t2, scratch, ubase, ((u64)blockIdx.y * p.ctas + blockIdx.x) * 32,
                               tile != blockIdx.x, tpop, T);
         else
             run_slots<OP, NT, ND, VAR>(p, t0, t1, t2, scratch, ((u64)blockIdx.y * p.ctas + blockIdx.x) * 32,
                                        tile != blockIdx.x, tpop, T);
 
+        // Write the tile back and, element by element, start the next tile's
+        // load into the slot just read: every thread reloads exactly the
+        // elements it stored, so no barrier separates the two tiles (the last
+        // slot's barrier ordered the tile writes before these reads; the wait +
+        // barrier at the top of the next trip publishes the new tile).
         const int sm = p.store_mask;
+        const u64 next = tile + gridDim.x;
+        const bool more = next < p.ntiles && !p.exp_noio;
+        const u64 nbase = more ? tile_base(next) : 0ull;
         for (unsigned l = tid; l < T && !p.exp_noio; l += NT) {
-            const u64 a = base + (l & cmask) + hiofs[l >> c];
+            const u64 o = (l & cmask) + hiofs[l >> c];
+            const u64 a = base + o;
             const unsigned sl = sw(l);
             const double2 x = t0[sl];
             if (sm & 1) psi[a] = x;
@@ -1451,8 +1488,13 @@ __global__ void __launch_bounds__(NT, (GF_NT512_M11 && NT == 512) ? 2 : ((VAR ==
                 vim = fma(f.x, x.y, vim);
                 vim = fma(f.y, x.x, vim);
             }
+            if (more) load_elem(nbase + o, sl);
         }
-        __syncthreads();
+        if (p.exp_noio && next < p.ntiles) {
+            __syncthreads();
+            for (unsigned l = tid; l < NV * T; l += NT) t0[l] = czero();
+        }
+        cp_async_commit();
     }
 
     if constexpr (HV) {
@@ -1615,7 +1657,7 @@ struct gf_plan {
     bool c1q_dmma = true;    // parity-controlled 1q slots on the DMMA path (PM_C1QD) instead of FMA pairs
     bool pair_blocks = false; // paired parity-block DMMAs in the update phases (PassSlot::pair; GF_PAIR_BLOCKS=1)
     bool unit_fma = false;    // sector plans: every slot as FP64-FMA units (PM_UNIT, run_units) when nd == 1
-    int unit_nt = 128;        // threads per CTA of the unit passes (GF_UNIT_NT)
+    int unit_nt = 256;        // threads per CTA of the unit passes (GF_UNIT_NT)
     int fm = 0, fc = 0;
     // geometry only (matrices filled per eval).  The ascending HVP sweep must
     // replay exactly the reverse slot order of the reverse sweep (the two HVP
@@ -1816,7 +1858,7 @@ struct PlanKnobs {
     bool c1q_dmma;     // GF_C1Q_DMMA: parity-controlled 1q slots on the DMMA path
     bool pair_blocks;  // GF_PAIR_BLOCKS: paired parity-block DMMAs in the update phases
     bool sector_fma;   // GF_SECTOR_FMA: parity-sector passes as FP64-FMA units (PM_UNIT)
-    int unit_nt;       // GF_UNIT_NT: threads per CTA of those passes (128 or 256)
+    int unit_nt;       // GF_UNIT_NT: threads per CTA of those passes (256, or 128)
 };
 
 static PlanKnobs plan_knobs(int K, int tile_bits)
@@ -1842,7 +1884,7 @@ static PlanKnobs plan_knobs(int K, int tile_bits)
     const char *sf = getenv("GF_SECTOR_FMA");
     k.sector_fma = sf ? atoi(sf) != 0 : true;
     const char *un = getenv("GF_UNIT_NT");
-    k.unit_nt = (un && atoi(un) == 256) ? 256 : 128;
+    k.unit_nt = (un && atoi(un) == 128) ? 128 : 256;  // measured: c5 3.87 s (256) vs 4.41 s (128)
     return k;
 }
 
@@ -2377,8 +2419,11 @@ static std::vector<FusedParams> plan_passes(const gf_plan *p, bool reverse, int 
     return out;
 }
 
-static size_t fused_smem(int nv, int m, int c, int nw, int nd = 1)
+static size_t fused_smem(int nv, int m, int c, int nw, int nd = 1, bool unit = false)
 {
+    if (unit)  // tiles, fold scratch [2][2][nw][8], global offsets, per-(slot, thread) unit bases
+        return sizeof(double2) * ((size_t)nv << m) + sizeof(double) * (2 * 2 * nw * 8) +
+               sizeof(unsigned long long) * ((size_t)1 << (m - c)) + sizeof(unsigned short) * FMAXSLOTS * nw * 32;
     return sizeof(double2) * ((size_t)nv << m) + sizeof(double) * ((1 + nd) * nw * 64) +
            sizeof(unsigned long long) * ((size_t)1 << (m - c));
 }
@@ -2387,7 +2432,7 @@ template <int OP, bool FIRST, int NT, int ND, int VAR>
 static int launch_fused_nt(const gf_plan *p, FusedParams &fp, int64_t nvec, cudaStream_t st)
 {
     const int nv = (OP == OP_FWD || OP == OP_FWD_DOT) ? 1 : (OP == OP_REV_G ? 2 : 2 + ND);
-    const size_t smem = fused_smem(nv, fp.m, fp.c, NT / 32, ND);
+    const size_t smem = fused_smem(nv, fp.m, fp.c, NT / 32, ND, VAR == 4);
     // the attribute is per device: set it once for every device this process drives
     static unsigned long long attr_done = 0ull;
     int dev = 0;
