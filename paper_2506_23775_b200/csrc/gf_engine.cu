@@ -1349,8 +1349,15 @@ __device__ __forceinline__ void run_units(const FusedParams &p, double2 *t0, dou
 #ifndef GF_NT512_M11
 #define GF_NT512_M11 0
 #endif
+// (unit passes: the forward sweep holds one vector per tile and is bound by
+// HBM / shared-memory traffic -- GF_UNIT_FWD_CTAS CTAs of 256 threads per SM)
+#ifndef GF_UNIT_FWD_CTAS
+#define GF_UNIT_FWD_CTAS 4
+#endif
 template <int OP, bool FIRST, int NT, int ND, int VAR>
-__global__ void __launch_bounds__(NT, (GF_NT512_M11 && NT == 512) ? 2 : ((VAR == 4 && NT < 256) ? 2 : 512 / NT))
+__global__ void __launch_bounds__(NT, (GF_NT512_M11 && NT == 512) ? 2
+                                      : ((VAR == 4 && NT < 256) ? 2
+                                         : ((VAR == 4 && NT == 256 && OP <= OP_FWD_DOT) ? GF_UNIT_FWD_CTAS : 512 / NT)))
     k_fused(const FusedParams p)
 {
     constexpr int NW = NT / 32;  // warps per CTA
@@ -2483,7 +2490,8 @@ static int launch_fused(const gf_plan *p, FusedParams &fp, int64_t nvec, cudaStr
         // parity-structured pass on the FMA pipe (one direction); tiles of 2^12
         // amplitudes keep the 512-thread shape
         if (nd != 1) return gf_fail(GF_EINVAL, "unit passes carry one direction");
-        if (fp.m >= 12) return launch_fused_nt<OP, FIRST, 512, 1, 4>(p, fp, nvec, st);
+        if (fp.m >= 12 && !(OP == OP_FWD || OP == OP_FWD_DOT))
+            return launch_fused_nt<OP, FIRST, 512, 1, 4>(p, fp, nvec, st);
         if (p->unit_nt == 256) return launch_fused_nt<OP, FIRST, 256, 1, 4>(p, fp, nvec, st);
         return launch_fused_nt<OP, FIRST, 128, 1, 4>(p, fp, nvec, st);
     }
