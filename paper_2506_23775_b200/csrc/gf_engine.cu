@@ -17,8 +17,10 @@
 // memory -- one CTA per tile, two CTAs per SM -- and runs all of the pass's
 // slots on them: FP64 tensor-core (DMMA m8n8k4) gate applications and hole
 // contractions, per-slot partials written per CTA and summed in CTA order by
-// k_reduce_ctas.  The streaming engine (k_sweep, one launch per slot) serves
-// tiny state spaces and GF_ENGINE=stream.
+// k_reduce_ctas.  Parity-sector plans run the same passes as FP64 FMAs on
+// two-amplitude units instead (run_units, PM_UNIT: the block-diagonal slots of
+// a sector waste half of every DMMA).  The streaming engine (k_sweep, one
+// launch per slot) serves tiny state spaces and GF_ENGINE=stream.
 //
 // Compile-time switches (measured defaults): GF_FUSED_GH -- fused gate + hole
 // phase in the ascending passes; GF_FUSED_BLOCK -- its groups per load batch;

@@ -369,6 +369,35 @@ def test_sector_engine_vs_reference_restricted_sums(name):
         assert rel_err(np.stack(hv), g[nm + "_hvp"]) < TOL
 
 
+@pytest.mark.parametrize("knobs", [{"GF_SECTOR_FMA": "0"}, {"GF_UNIT_NT": "128"}, {"GF_FUSED_M": "8"},
+                                   {"GF_FUSED_M": "9", "GF_UNIT_NT": "128"}, {"GF_FUSED_M": "6"}])
+def test_sector_engine_variants_vs_reference_sums(monkeypatch, knobs):
+    """The parity-sector passes run as FP64-FMA units (PM_UNIT) by default.
+    The other builds of the same sweeps -- the DMMA sector path
+    (GF_SECTOR_FMA=0: structural-zero parity gates, PM_C1QD slots), 128-thread
+    unit CTAs, forced small tiles (several tiles and passes; 2^6 tiles fall
+    back to the DMMA path) -- must reproduce the reference-derived sector sums."""
+    for k_, v_ in knobs.items():
+        monkeypatch.setenv(k_, v_)
+    g = golden("sector_l6p")
+    L = int(g["L"])
+    spec, circ, rng = gf.spinful_layer_circuit(L, int(g["gates"].shape[0]), bool(g["periodic"]), seed=4, parity=True)
+    orc = gf.DenseOracle(spec, 0.25)
+    X = list(g["direction"])
+    for sect, nm in ((0, "even"), (1, "odd")):
+        rep, hv = gf.gradient_and_hvp(circ, orc, X, parity_mode=True, sector=sect)
+        ref_v = g[nm + "_value"]
+        assert abs(-rep.value - ref_v.real) < TOL * max(1, abs(ref_v))
+        assert rel_err(np.stack(rep.holomorphic_derivatives), g[nm + "_holo"]) < TOL
+        assert rel_err(np.stack(hv), g[nm + "_hvp"]) < TOL
+        grad = gf.full_gradient(circ, orc, parity_mode=True, sector=sect)  # OP_REV_G passes
+        assert rel_err(np.stack(grad.holomorphic_derivatives), g[nm + "_holo"]) < TOL
+        hv1 = gf.hessian_vector_product(circ, orc, X, sector=sect)          # OP_REV_H passes
+        assert rel_err(np.stack(hv1), g[nm + "_hvp"]) < TOL
+        val = gf.target_value(circ, orc, sector=sect)                        # OP_FWD_DOT
+        assert abs(-val - ref_v.real) < TOL * max(1, abs(ref_v))
+
+
 @pytest.mark.parametrize("name", ["sector_l4p", "sector_l6p"])
 def test_fold_engine_vs_reference_even_sum(name):
     g = golden(name)
