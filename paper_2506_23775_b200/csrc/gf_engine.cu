@@ -1404,6 +1404,8 @@ __global__ void __launch_bounds__(NT, (GF_NT512_M11 && NT == 512) ? 2
     // the first forward and first ascending passes start from psi_0 = |j>
     constexpr bool SYNTH = (OP == OP_FWD || OP == OP_FWD_DOT || OP == OP_ASC_H) && FIRST;
     const u64 jb = SYNTH ? (u64)p.basis[blockIdx.y] : 0ull;
+    u64 gmask = 0;
+    for (int i = 0; i < p.nglob; ++i) gmask |= 1ull << p.gpos[i];
     auto tile_base = [&](u64 tile) {
         u64 base = 0;
         for (int i = 0; i < p.nglob; ++i)
@@ -1461,12 +1463,19 @@ __global__ void __launch_bounds__(NT, (GF_NT512_M11 && NT == 512) ? 2
         }
         __syncthreads();
 
-        if constexpr (VAR == 4)
-            run_units<OP, NT>(p, t0, t1, t2, scratch, ubase, ((u64)blockIdx.y * p.ctas + blockIdx.x) * 32,
-                              tile != blockIdx.x, tpop, T);
-        else
-            run_slots<OP, NT, ND, VAR>(p, t0, t1, t2, scratch, ((u64)blockIdx.y * p.ctas + blockIdx.x) * 32,
-                                       tile != blockIdx.x, tpop, T);
+        // First forward pass: psi_0 = |j> lies in exactly one tile (the one
+        // whose global bits are j's); every other tile is zero, stays zero
+        // under the pass's gates and is written back as is.
+        bool live = true;
+        if constexpr (SYNTH && NV == 1) live = (jb & gmask) == base;
+        if (live) {
+            if constexpr (VAR == 4)
+                run_units<OP, NT>(p, t0, t1, t2, scratch, ubase, ((u64)blockIdx.y * p.ctas + blockIdx.x) * 32,
+                                  tile != blockIdx.x, tpop, T);
+            else
+                run_slots<OP, NT, ND, VAR>(p, t0, t1, t2, scratch, ((u64)blockIdx.y * p.ctas + blockIdx.x) * 32,
+                                           tile != blockIdx.x, tpop, T);
+        }
 
         // Write the tile back and, element by element, start the next tile's
         // load into the slot just read: every thread reloads exactly the
