@@ -357,7 +357,11 @@ __device__ __forceinline__ double2 dmma_mv2(double2 x, double b0, double b1, dou
 template <int V>
 using IC = std::integral_constant<int, V>;
 
-template <int OP, int NT, int ND, int VAR>
+// DEAD: the tile lies outside the basis state's light cone (psi = v = 0 on it,
+// k_fused): only the backward vectors move -- bra <- G^T bra and, while a later
+// pass reads chi, chi <- G^T chi + Z^T bra in the reverse sweep; bra <- conj(G)
+// bra in the ascending sweep; no holes (their contributions are exact zeros).
+template <int OP, int NT, int ND, int VAR, bool DEAD>
 __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, double2 *t1, double2 *t2, double *scratch,
                                           const u64 pofs, const bool accum, const int tpop, const unsigned T)
 {
@@ -369,7 +373,7 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
     constexpr bool CHI = (OP == OP_REV_GH || OP == OP_REV_H);  // reverse sweep carrying chi_d
     // fused gate + hole phase (dense slots): ascending sweep 3% faster; the
     // reverse sweep measured 0.5% slower with it and keeps the split phases
-    constexpr bool GH = GF_FUSED_GH && (OP == OP_ASC_H);
+    constexpr bool GH = GF_FUSED_GH && (OP == OP_ASC_H) && !DEAD;
     // VAR bit 0: the pass has parity-sparse FMA slots; bit 1: it has
     // parity-controlled one-qubit slots on the DMMA path (PM_C1QD).  Passes
     // without them compile without those branches.
@@ -382,7 +386,10 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
     const int gi = g >> 1, gpart = g & 1;
     for (int si = 0; si < p.nslots; ++si) {
         const int mode = p.ps[si].mode;
-        const int zmask = p.ps[si].zmask, amask = p.ps[si].amask;
+        int zmask = p.ps[si].zmask, amask = p.ps[si].amask;
+        if constexpr (DEAD && CHI) {
+            if (!(p.store_mask & 4)) zmask = amask = 0;  // last reverse pass: chi is dead as well
+        }
         const Mat4 &MA = p.mat[si][0];
         const Mat4 &MB = p.mat[si][1];
         const bool c1q = (mode == PM_C1Q);
@@ -691,7 +698,9 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                     // constant cache)
                     const double2 fA = __ldg(&p.frag[p.ps[si].fa * 32 + lane]);
                     const double fa0 = fA.x, fa1 = fA.y;
-                    if constexpr (OP == OP_FWD || OP == OP_FWD_DOT) {
+                    if constexpr (DEAD && REV) {
+                        // psi = 0 on the tile
+                    } else if constexpr (OP == OP_FWD || OP == OP_FWD_DOT) {
                         // forward passes: register-bound occupancy, one group at a time
                         for (unsigned gb = 0; gb < ngrp; gb += 8) {
                             const unsigned ab = addrA(gb);
@@ -723,7 +732,7 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                         }
                     }
                 }
-                if constexpr (HD || HH) if (!GH || sparse || c1d) {
+                if constexpr ((HD || HH) && !DEAD) if (!GH || sparse || c1d) {
                     __syncwarp();
                     // hole layout: lane (g, tq) = component g (amp g>>1, part g&1) of tuple tq
                     const unsigned offH = ((gi & 2) ? PS.sh : 0u) ^ ((gi & 1) ? PS.so : 0u);
@@ -831,7 +840,9 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                     __syncwarp();
                 }
                 if constexpr (GH) if (!sparse && !c1d) __syncwarp();  // fused phase reads precede the updates' writes
-                if constexpr (OP != OP_FWD && OP != OP_FWD_DOT) if (sparse) {
+                if constexpr (DEAD && OP == OP_ASC_H) {
+                    // v = psi = 0 on the tile: nothing to update
+                } else if constexpr (OP != OP_FWD && OP != OP_FWD_DOT) if (sparse) {
                     const unsigned Fl = Fw ^ Alane();
                     for (unsigned j = lane; j < TW; j += 32) {
                         const unsigned b0 = Fl ^ Ahi(j >> 5);
@@ -998,7 +1009,7 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                 }
             }
         }
-        if constexpr (HD || HH) {
+        if constexpr ((HD || HH) && !DEAD) {
             // Fold the 8x8 real fragment to the complex 4x4 hole inside the warp:
             // lane (2i, j) holds C[2i][2j..2j+1], its partner lane (2i+1, j)
             // C[2i+1][2j..2j+1]; Re D_ij = C[2i][2j] - C[2i+1][2j+1],
@@ -1115,7 +1126,7 @@ __device__ __forceinline__ void unit_bases(const FusedParams &p, unsigned short 
     }
 }
 
-template <int OP, int NT>
+template <int OP, int NT, bool DEAD>
 __device__ __forceinline__ void run_units(const FusedParams &p, double2 *t0, double2 *t1, double2 *t2, double *scratch,
                                           const unsigned short *ubase, const u64 pofs, const bool accum,
                                           const int tpop, const unsigned T)
@@ -1160,7 +1171,7 @@ __device__ __forceinline__ void run_units(const FusedParams &p, double2 *t0, dou
         // early, added after the barrier
         double prev = 0.0;
         double *pdst = nullptr;
-        if constexpr (HD || HH) {
+        if constexpr ((HD || HH) && !DEAD) {
             if (tid < 32 * NH) {
                 const int hole = tid >> 5;
                 if ((hole == 0 && HD) || (hole >= 1 && HH)) {
@@ -1265,7 +1276,32 @@ __device__ __forceinline__ void run_units(const FusedParams &p, double2 *t0, dou
                     t0[u.a1] = cfmac(a11, u.x1, cmulc(a10, u.x0));
                 }
             };
-            if (nit >= 2u * W) {
+            if constexpr (DEAD) {
+                // dead tile (psi = v = 0): the backward vectors only
+                const bool chi_on = CHI && (p.store_mask & 4);
+                for (unsigned it = 0; it < nit; ++it) {
+                    const unsigned a0 = a, a1 = a ^ dso;
+                    GF_DCHECK(a0 < T && a1 < T);
+                    const double2 b0 = t1[a0], b1 = t1[a1];
+                    if constexpr (REV) {
+                        if (chi_on) {
+                            const double2 c0 = t2[a0], c1 = t2[a1];
+                            double2 n0 = cfma(z01, b1, cmul(z00, b0));
+                            double2 n1 = cfma(z11, b1, cmul(z10, b0));
+                            n0 = cfmac(a01, c1, cfmac(a00, c0, n0));
+                            n1 = cfmac(a11, c1, cfmac(a10, c0, n1));
+                            t2[a0] = n0;
+                            t2[a1] = n1;
+                        }
+                        t1[a0] = cfmac(a01, b1, cmulc(a00, b0));
+                        t1[a1] = cfmac(a11, b1, cmulc(a10, b0));
+                    } else {
+                        t1[a0] = cfma(a01, b1, cmul(a00, b0));
+                        t1[a1] = cfma(a11, b1, cmul(a10, b0));
+                    }
+                    advance();
+                }
+            } else if (nit >= 2u * W) {
                 // W units per step (independent FMA chains and accumulator
                 // sets), the next W already loading
                 Unit u[2][W];
@@ -1298,7 +1334,7 @@ __device__ __forceinline__ void run_units(const FusedParams &p, double2 *t0, dou
                 }
             }
         }
-        if constexpr (HD || HH) {
+        if constexpr ((HD || HH) && !DEAD) {
             // Per hole a lane holds the 2x2 complex block of the warp's b as 8
             // doubles v[4 r + 2 s + part].  Reduce-scatter over lane bits 4 (r),
             // 3 (s), 2 (part), then add over bits 1 and 0 (fixed order:
@@ -1403,32 +1439,45 @@ __global__ void __launch_bounds__(NT, (GF_NT512_M11 && NT == 512) ? 2
 
     // the first forward and first ascending passes start from psi_0 = |j>
     constexpr bool SYNTH = (OP == OP_FWD || OP == OP_FWD_DOT || OP == OP_ASC_H) && FIRST;
-    const u64 jb = SYNTH ? (u64)p.basis[blockIdx.y] : 0ull;
-    u64 gmask = 0;
-    for (int i = 0; i < p.nglob; ++i) gmask |= 1ull << p.gpos[i];
+    constexpr bool FWDOP = (OP == OP_FWD || OP == OP_FWD_DOT);
+    constexpr bool ASC = (OP == OP_ASC_H);
+    const u64 jb = (u64)p.basis[blockIdx.y];
     auto tile_base = [&](u64 tile) {
         u64 base = 0;
         for (int i = 0; i < p.nglob; ++i)
             if ((tile >> i) & 1ull) base |= 1ull << p.gpos[i];
         return base;
     };
+    // Light cone of the basis state (p.fixmask, plan_passes): the forward
+    // states psi (and the forward tangent v) of summand j vanish wherever a
+    // qubit no applied slot has touched differs from j.  A tile whose global
+    // bits disagree with j on such a bit is *dead*: psi = v = 0 on it before
+    // and after the pass, so the pass only has to carry the backward vectors
+    // (bra, chi) through it.  Dead tiles hold exact zeros in HBM already (the
+    // first forward / ascending pass writes them), so psi / v are neither
+    // loaded nor stored there.
+    auto is_live = [&](u64 base) { return ((jb ^ base) & p.fixmask) == 0ull; };
+    const int sm = p.store_mask;
     // Element l of a tile: plain copies go global -> shared with cp.async (no
     // register round trip, every element in flight at once); the synthesised
     // |j> and the zero chi / v are written by the thread.
-    auto load_elem = [&](u64 a, unsigned sl) {
+    auto load_elem = [&](u64 a, unsigned sl, bool live) {
         GF_DCHECK(a < p.N && sl < T);
         if constexpr (SYNTH)
             t0[sl] = make_double2(a == jb ? 1.0 : 0.0, 0.0);  // psi_0 = |j>, no HBM read
-        else
+        else if (live)
             cp_async16(&t0[sl], &psi[a]);
         if constexpr (NV >= 2) {
             if constexpr (!(REV && FIRST)) cp_async16(&t1[sl], &bra[a]);
         }
         if constexpr (NV >= 3) {
+            // chi is carried through dead tiles while a later pass reads it
+            // (store_mask bit 2); v is zero there
+            const bool need = ASC ? live : (live || (sm & 4));
 #pragma unroll
             for (int d = 0; d < ND; ++d) {
                 if constexpr (FIRST) t2[d * T + sl] = czero();
-                else cp_async16(&t2[d * T + sl], &aux[a + d * p.auxstride]);
+                else if (need) cp_async16(&t2[d * T + sl], &aux[a + d * p.auxstride]);
             }
         }
     };
@@ -1436,13 +1485,16 @@ __global__ void __launch_bounds__(NT, (GF_NT512_M11 && NT == 512) ? 2
         for (unsigned l = tid; l < NV * T; l += NT) t0[l] = czero();
     } else if (blockIdx.x < p.ntiles) {
         const u64 base = tile_base(blockIdx.x);
-        for (unsigned l = tid; l < T; l += NT) load_elem(base + (l & cmask) + hiofs[l >> c], sw(l));
+        const bool live = is_live(base);
+        if (!(FWDOP && !FIRST && !live))
+            for (unsigned l = tid; l < T; l += NT) load_elem(base + (l & cmask) + hiofs[l >> c], sw(l), live);
     }
     cp_async_commit();
 
     for (u64 tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
         const u64 base = tile_base(tile);
         const int tpop = __popcll(tile);
+        const bool live = is_live(base);
         if constexpr (REV && FIRST) {
             // bra_0 = w phi0; the value <phi0|psi_n> is read back from the tile
             for (unsigned l = tid; l < T; l += NT) {
@@ -1450,7 +1502,7 @@ __global__ void __launch_bounds__(NT, (GF_NT512_M11 && NT == 512) ? 2
                 t1[sw(l)] = cscale(phi0[a], w);
             }
             cp_async_wait<0>();
-            for (unsigned l = tid; l < T; l += NT) {
+            for (unsigned l = tid; l < T && live; l += NT) {
                 const unsigned sl = sw(l);
                 const double2 x = t0[sl], b = t1[sl];
                 vre = fma(b.x, x.x, vre);
@@ -1463,18 +1515,30 @@ __global__ void __launch_bounds__(NT, (GF_NT512_M11 && NT == 512) ? 2
         }
         __syncthreads();
 
-        // First forward pass: psi_0 = |j> lies in exactly one tile (the one
-        // whose global bits are j's); every other tile is zero, stays zero
-        // under the pass's gates and is written back as is.
-        bool live = true;
-        if constexpr (SYNTH && NV == 1) live = (jb & gmask) == base;
+        const u64 pofs = ((u64)blockIdx.y * p.ctas + blockIdx.x) * 32;
         if (live) {
             if constexpr (VAR == 4)
-                run_units<OP, NT>(p, t0, t1, t2, scratch, ubase, ((u64)blockIdx.y * p.ctas + blockIdx.x) * 32,
-                                  tile != blockIdx.x, tpop, T);
+                run_units<OP, NT, false>(p, t0, t1, t2, scratch, ubase, pofs, tile != blockIdx.x, tpop, T);
             else
-                run_slots<OP, NT, ND, VAR>(p, t0, t1, t2, scratch, ((u64)blockIdx.y * p.ctas + blockIdx.x) * 32,
-                                           tile != blockIdx.x, tpop, T);
+                run_slots<OP, NT, ND, VAR, false>(p, t0, t1, t2, scratch, pofs, tile != blockIdx.x, tpop, T);
+        } else if constexpr (!FWDOP) {
+            // dead tile: backward vectors only; its hole partials are exact zeros
+            if (tile == blockIdx.x) {
+                constexpr bool HDP = (OP == OP_REV_G || OP == OP_REV_GH);
+                constexpr bool HHP = (OP == OP_REV_GH || OP == OP_REV_H || OP == OP_ASC_H);
+                for (int e = tid; e < p.nslots * 32 * NH; e += NT) {
+                    const int si = e / (32 * NH), hole = (e / 32) % NH, i = e & 31;
+                    if ((hole == 0 && HDP) || (hole >= 1 && HHP)) {
+                        double *dst = (hole == 0 ? p.partD : p.partH + (u64)(hole - 1) * p.hstride) +
+                                      (u64)p.ps[si].slot * p.nvec * p.ctas * 32 + pofs + i;
+                        *dst = 0.0;
+                    }
+                }
+            }
+            if constexpr (VAR == 4)
+                run_units<OP, NT, true>(p, t0, t1, t2, scratch, ubase, pofs, tile != blockIdx.x, tpop, T);
+            else
+                run_slots<OP, NT, ND, VAR, true>(p, t0, t1, t2, scratch, pofs, tile != blockIdx.x, tpop, T);
         }
 
         // Write the tile back and, element by element, start the next tile's
@@ -1482,31 +1546,38 @@ __global__ void __launch_bounds__(NT, (GF_NT512_M11 && NT == 512) ? 2
         // elements it stored, so no barrier separates the two tiles (the last
         // slot's barrier ordered the tile writes before these reads; the wait +
         // barrier at the top of the next trip publishes the new tile).
-        const int sm = p.store_mask;
         const u64 next = tile + gridDim.x;
         const bool more = next < p.ntiles && !p.exp_noio;
         const u64 nbase = more ? tile_base(next) : 0ull;
+        const bool nlive = more ? is_live(nbase) : true;
+        const bool reload = more && !(FWDOP && !FIRST && !nlive);
+        // psi / v of a dead tile: zeros written by the first pass, untouched later
+        const bool wpsi = (sm & 1) && (live || SYNTH);
+        const bool waux = (sm & 4) && (ASC ? (live || FIRST) : true);
+        const bool skip = FWDOP && !FIRST && !live;  // nothing was loaded
         for (unsigned l = tid; l < T && !p.exp_noio; l += NT) {
             const u64 o = (l & cmask) + hiofs[l >> c];
             const u64 a = base + o;
             const unsigned sl = sw(l);
-            const double2 x = t0[sl];
-            if (sm & 1) psi[a] = x;
-            if constexpr (NV >= 2) if (sm & 2) bra[a] = t1[sl];
-            if constexpr (NV >= 3) {
-                if (sm & 4) {
+            if (!skip) {
+                const double2 x = t0[sl];
+                if (wpsi) psi[a] = x;
+                if constexpr (NV >= 2) if (sm & 2) bra[a] = t1[sl];
+                if constexpr (NV >= 3) {
+                    if (waux) {
 #pragma unroll
-                    for (int d = 0; d < ND; ++d) aux[a + d * p.auxstride] = t2[d * T + sl];
+                        for (int d = 0; d < ND; ++d) aux[a + d * p.auxstride] = t2[d * T + sl];
+                    }
+                }
+                if constexpr (OP == OP_FWD_DOT) {
+                    const double2 f = cscale(phi0[a], w);
+                    vre = fma(f.x, x.x, vre);
+                    vre = fma(-f.y, x.y, vre);
+                    vim = fma(f.x, x.y, vim);
+                    vim = fma(f.y, x.x, vim);
                 }
             }
-            if constexpr (OP == OP_FWD_DOT) {
-                const double2 f = cscale(phi0[a], w);
-                vre = fma(f.x, x.x, vre);
-                vre = fma(-f.y, x.y, vre);
-                vim = fma(f.x, x.y, vim);
-                vim = fma(f.y, x.x, vim);
-            }
-            if (more) load_elem(nbase + o, sl);
+            if (reload) load_elem(nbase + o, sl, nlive);
         }
         if (p.exp_noio && next < p.ntiles) {
             __syncthreads();
@@ -1674,6 +1745,7 @@ struct gf_plan {
     bool sparse_fma = true;  // parity-sparse slots as FMA (else dense DMMA with structural zeros)
     bool c1q_dmma = true;    // parity-controlled 1q slots on the DMMA path (PM_C1QD) instead of FMA pairs
     bool pair_blocks = false; // paired parity-block DMMAs in the update phases (PassSlot::pair; GF_PAIR_BLOCKS=1)
+    bool lightcone = true;    // skip the psi / v work of tiles outside the basis state's light cone (GF_LIGHTCONE)
     bool unit_fma = false;    // sector plans: every slot as FP64-FMA units (PM_UNIT, run_units) when nd == 1
     int unit_nt = 256;        // threads per CTA of the unit passes (GF_UNIT_NT)
     int fm = 0, fc = 0;
@@ -1875,6 +1947,7 @@ struct PlanKnobs {
     bool sparse_dmma;  // GF_SPARSE_DMMA: parity-sparse slots on the DMMA path
     bool c1q_dmma;     // GF_C1Q_DMMA: parity-controlled 1q slots on the DMMA path
     bool pair_blocks;  // GF_PAIR_BLOCKS: paired parity-block DMMAs in the update phases
+    bool lightcone;    // GF_LIGHTCONE: dead-tile skipping (FusedParams::fixmask)
     bool sector_fma;   // GF_SECTOR_FMA: parity-sector passes as FP64-FMA units (PM_UNIT)
     int unit_nt;       // GF_UNIT_NT: threads per CTA of those passes (256, or 128)
 };
@@ -1899,6 +1972,8 @@ static PlanKnobs plan_knobs(int K, int tile_bits)
     k.c1q_dmma = cq ? atoi(cq) != 0 : true;
     const char *pb = getenv("GF_PAIR_BLOCKS");
     k.pair_blocks = pb ? atoi(pb) != 0 : false;  // measured slower: c5 5.33 vs 5.01 s, c3 11.4 vs 10.6 ms
+    const char *lc = getenv("GF_LIGHTCONE");
+    k.lightcone = lc ? atoi(lc) != 0 : true;
     const char *sf = getenv("GF_SECTOR_FMA");
     k.sector_fma = sf ? atoi(sf) != 0 : true;
     const char *un = getenv("GF_UNIT_NT");
@@ -1972,6 +2047,7 @@ extern "C" int gf_plan_create(gf_plan **out, int k, int sector, int n_slots, con
         p->sparse_fma = !kn.sparse_dmma;
         p->c1q_dmma = kn.c1q_dmma;
         p->pair_blocks = kn.pair_blocks;
+        p->lightcone = kn.lightcone;
         // (tiles of >= 2^7 amplitudes: the kernel gives each block selector its own warps)
         p->unit_fma = kn.sector_fma && sector >= 0 && p->fm >= 7 && kn.fwm >= 7;
         p->unit_nt = kn.unit_nt;
@@ -2434,6 +2510,33 @@ static std::vector<FusedParams> plan_passes(const gf_plan *p, bool reverse, int 
         }
         out.push_back(fp);
     }
+    // Light cone of the basis state: psi (and the forward tangent v) entering a
+    // pass equal |j> on every qubit no applied slot has touched, so tiles whose
+    // global bits disagree with j on such a qubit are zero (k_fused skips the
+    // psi / v work there).  Forward sweep: slots of the earlier passes are
+    // applied.  Reverse sweep (psi is un-computed pass by pass): the slots of
+    // this and the later passes are still applied; the ascending sweep replays
+    // the reverse passes backwards and sees the same set.
+    if (p->lightcone) {
+        auto slot_mask = [&](int s) {
+            const SlotInfo &si = p->slots[s];
+            return si.mode_c1q ? (1ull << si.lo) : ((1ull << si.lo) | (1ull << si.hi));
+        };
+        const size_t np = out.size();
+        std::vector<unsigned long long> touched(np + 1, 0ull);  // by the passes' own slots
+        for (size_t i = 0; i < np; ++i)
+            for (int t = 0; t < out[i].nslots; ++t) touched[i] |= slot_mask(out[i].ps[t].slot);
+        for (size_t i = 0; i < np; ++i) {
+            unsigned long long applied = 0ull, gmask = 0ull;
+            if (!reverse) {
+                for (size_t j = 0; j < i; ++j) applied |= touched[j];
+            } else {
+                for (size_t j = i; j < np; ++j) applied |= touched[j];
+            }
+            for (int g = 0; g < out[i].nglob; ++g) gmask |= 1ull << out[i].gpos[g];
+            out[i].fixmask = gmask & ~applied;
+        }
+    }
     return out;
 }
 
@@ -2493,6 +2596,8 @@ static int launch_fused(const gf_plan *p, FusedParams &fp, int64_t nvec, cudaStr
 {
     bool spx = false, c1d = false, unit = fp.nslots > 0;
     for (int t = 0; t < fp.nslots; ++t) {
+        // the FMA forms kept for experiments (GF_SPARSE_DMMA=0, GF_C1Q_DMMA=0) have no dead-tile variant
+        if (fp.ps[t].mode == PM_SPARSE || fp.ps[t].mode == PM_C1Q) fp.fixmask = 0ull;
         spx |= (fp.ps[t].mode == PM_SPARSE);
         c1d |= (fp.ps[t].mode == PM_C1QD) || fp.ps[t].pair;
         unit = unit && (fp.ps[t].mode == PM_UNIT);

@@ -85,6 +85,10 @@ struct FusedParams {
     double *qD, *qH, *qV;    // per-(slot, vector) sums (k_reduce_ctas)
     unsigned long long N;
     unsigned long long ntiles;  // 2^(K-m)
+    // light cone: global bit positions on which psi (and v) entering this pass
+    // still equal the basis state (no applied slot has touched them); a tile
+    // that disagrees with j on one of them holds psi = v = 0 (0 = disabled)
+    unsigned long long fixmask;
     int nvec, ctas, sector;
     int m, c, nglob, nslots;
     int exp_noio;    // timing diagnostic (GF_EXP_NOIO): skip the tile loads and stores
