@@ -357,11 +357,7 @@ __device__ __forceinline__ double2 dmma_mv2(double2 x, double b0, double b1, dou
 template <int V>
 using IC = std::integral_constant<int, V>;
 
-// DEAD: the tile lies outside the basis state's light cone (psi = v = 0 on it,
-// k_fused): only the backward vectors move -- bra <- G^T bra and, while a later
-// pass reads chi, chi <- G^T chi + Z^T bra in the reverse sweep; bra <- conj(G)
-// bra in the ascending sweep; no holes (their contributions are exact zeros).
-template <int OP, int NT, int ND, int VAR, bool DEAD>
+template <int OP, int NT, int ND, int VAR>
 __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, double2 *t1, double2 *t2, double *scratch,
                                           const u64 pofs, const bool accum, const int tpop, const unsigned T)
 {
@@ -373,7 +369,7 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
     constexpr bool CHI = (OP == OP_REV_GH || OP == OP_REV_H);  // reverse sweep carrying chi_d
     // fused gate + hole phase (dense slots): ascending sweep 3% faster; the
     // reverse sweep measured 0.5% slower with it and keeps the split phases
-    constexpr bool GH = GF_FUSED_GH && (OP == OP_ASC_H) && !DEAD;
+    constexpr bool GH = GF_FUSED_GH && (OP == OP_ASC_H);
     // VAR bit 0: the pass has parity-sparse FMA slots; bit 1: it has
     // parity-controlled one-qubit slots on the DMMA path (PM_C1QD).  Passes
     // without them compile without those branches.
@@ -386,10 +382,7 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
     const int gi = g >> 1, gpart = g & 1;
     for (int si = 0; si < p.nslots; ++si) {
         const int mode = p.ps[si].mode;
-        int zmask = p.ps[si].zmask, amask = p.ps[si].amask;
-        if constexpr (DEAD && CHI) {
-            if (!(p.store_mask & 4)) zmask = amask = 0;  // last reverse pass: chi is dead as well
-        }
+        const int zmask = p.ps[si].zmask, amask = p.ps[si].amask;
         const Mat4 &MA = p.mat[si][0];
         const Mat4 &MB = p.mat[si][1];
         const bool c1q = (mode == PM_C1Q);
@@ -698,9 +691,7 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                     // constant cache)
                     const double2 fA = __ldg(&p.frag[p.ps[si].fa * 32 + lane]);
                     const double fa0 = fA.x, fa1 = fA.y;
-                    if constexpr (DEAD && REV) {
-                        // psi = 0 on the tile
-                    } else if constexpr (OP == OP_FWD || OP == OP_FWD_DOT) {
+                    if constexpr (OP == OP_FWD || OP == OP_FWD_DOT) {
                         // forward passes: register-bound occupancy, one group at a time
                         for (unsigned gb = 0; gb < ngrp; gb += 8) {
                             const unsigned ab = addrA(gb);
@@ -732,7 +723,7 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                         }
                     }
                 }
-                if constexpr ((HD || HH) && !DEAD) if (!GH || sparse || c1d) {
+                if constexpr (HD || HH) if (!GH || sparse || c1d) {
                     __syncwarp();
                     // hole layout: lane (g, tq) = component g (amp g>>1, part g&1) of tuple tq
                     const unsigned offH = ((gi & 2) ? PS.sh : 0u) ^ ((gi & 1) ? PS.so : 0u);
@@ -840,9 +831,7 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                     __syncwarp();
                 }
                 if constexpr (GH) if (!sparse && !c1d) __syncwarp();  // fused phase reads precede the updates' writes
-                if constexpr (DEAD && OP == OP_ASC_H) {
-                    // v = psi = 0 on the tile: nothing to update
-                } else if constexpr (OP != OP_FWD && OP != OP_FWD_DOT) if (sparse) {
+                if constexpr (OP != OP_FWD && OP != OP_FWD_DOT) if (sparse) {
                     const unsigned Fl = Fw ^ Alane();
                     for (unsigned j = lane; j < TW; j += 32) {
                         const unsigned b0 = Fl ^ Ahi(j >> 5);
@@ -1009,7 +998,7 @@ __device__ __forceinline__ void run_slots(const FusedParams &p, double2 *t0, dou
                 }
             }
         }
-        if constexpr ((HD || HH) && !DEAD) {
+        if constexpr (HD || HH) {
             // Fold the 8x8 real fragment to the complex 4x4 hole inside the warp:
             // lane (2i, j) holds C[2i][2j..2j+1], its partner lane (2i+1, j)
             // C[2i+1][2j..2j+1]; Re D_ij = C[2i][2j] - C[2i+1][2j+1],
@@ -1126,7 +1115,7 @@ __device__ __forceinline__ void unit_bases(const FusedParams &p, unsigned short 
     }
 }
 
-template <int OP, int NT, bool DEAD>
+template <int OP, int NT>
 __device__ __forceinline__ void run_units(const FusedParams &p, double2 *t0, double2 *t1, double2 *t2, double *scratch,
                                           const unsigned short *ubase, const u64 pofs, const bool accum,
                                           const int tpop, const unsigned T)
@@ -1171,7 +1160,7 @@ __device__ __forceinline__ void run_units(const FusedParams &p, double2 *t0, dou
         // early, added after the barrier
         double prev = 0.0;
         double *pdst = nullptr;
-        if constexpr ((HD || HH) && !DEAD) {
+        if constexpr (HD || HH) {
             if (tid < 32 * NH) {
                 const int hole = tid >> 5;
                 if ((hole == 0 && HD) || (hole >= 1 && HH)) {
@@ -1276,32 +1265,7 @@ __device__ __forceinline__ void run_units(const FusedParams &p, double2 *t0, dou
                     t0[u.a1] = cfmac(a11, u.x1, cmulc(a10, u.x0));
                 }
             };
-            if constexpr (DEAD) {
-                // dead tile (psi = v = 0): the backward vectors only
-                const bool chi_on = CHI && (p.store_mask & 4);
-                for (unsigned it = 0; it < nit; ++it) {
-                    const unsigned a0 = a, a1 = a ^ dso;
-                    GF_DCHECK(a0 < T && a1 < T);
-                    const double2 b0 = t1[a0], b1 = t1[a1];
-                    if constexpr (REV) {
-                        if (chi_on) {
-                            const double2 c0 = t2[a0], c1 = t2[a1];
-                            double2 n0 = cfma(z01, b1, cmul(z00, b0));
-                            double2 n1 = cfma(z11, b1, cmul(z10, b0));
-                            n0 = cfmac(a01, c1, cfmac(a00, c0, n0));
-                            n1 = cfmac(a11, c1, cfmac(a10, c0, n1));
-                            t2[a0] = n0;
-                            t2[a1] = n1;
-                        }
-                        t1[a0] = cfmac(a01, b1, cmulc(a00, b0));
-                        t1[a1] = cfmac(a11, b1, cmulc(a10, b0));
-                    } else {
-                        t1[a0] = cfma(a01, b1, cmul(a00, b0));
-                        t1[a1] = cfma(a11, b1, cmul(a10, b0));
-                    }
-                    advance();
-                }
-            } else if (nit >= 2u * W) {
+            if (nit >= 2u * W) {
                 // W units per step (independent FMA chains and accumulator
                 // sets), the next W already loading
                 Unit u[2][W];
@@ -1334,7 +1298,7 @@ __device__ __forceinline__ void run_units(const FusedParams &p, double2 *t0, dou
                 }
             }
         }
-        if constexpr ((HD || HH) && !DEAD) {
+        if constexpr (HD || HH) {
             // Per hole a lane holds the 2x2 complex block of the warp's b as 8
             // doubles v[4 r + 2 s + part].  Reduce-scatter over lane bits 4 (r),
             // 3 (s), 2 (part), then add over bits 1 and 0 (fixed order:
@@ -1448,19 +1412,26 @@ __global__ void __launch_bounds__(NT, (GF_NT512_M11 && NT == 512) ? 2
             if ((tile >> i) & 1ull) base |= 1ull << p.gpos[i];
         return base;
     };
-    // Light cone of the basis state (p.fixmask, plan_passes): the forward
+    // Light cone of the basis state (p.fixmask, plan_passes).  The forward
     // states psi (and the forward tangent v) of summand j vanish wherever a
-    // qubit no applied slot has touched differs from j.  A tile whose global
-    // bits disagree with j on such a bit is *dead*: psi = v = 0 on it before
-    // and after the pass, so the pass only has to carry the backward vectors
-    // (bra, chi) through it.  Dead tiles hold exact zeros in HBM already (the
-    // first forward / ascending pass writes them), so psi / v are neither
-    // loaded nor stored there.
+    // qubit b that no applied slot has touched differs from j.  A tile whose
+    // global bits disagree with j on such a qubit is *dead*:
+    //  * psi = v = 0 on it before and after the pass, so its holes are zero;
+    //  * no remaining slot of the sweep touches b, so nothing ever flows from
+    //    the tile's amplitudes into amplitudes that agree with j on b: chi on
+    //    them is never read against a nonzero psi;
+    //  * the reverse pass and the ascending pass that replays it have the same
+    //    tiles and fixmask, and on one tile they are exact inverses on the bra
+    //    (conj(G) G^T = 1), with everything in between nested inside them:
+    //    skipping both leaves the bra of every later pass unchanged.
+    // So a dead tile is skipped altogether -- no loads, no slots, no stores --
+    // except in the first pass of a sweep, which initialises HBM: zeros for
+    // psi (forward, ascending) and chi / v, w phi0 for the bra.
     auto is_live = [&](u64 base) { return ((jb ^ base) & p.fixmask) == 0ull; };
     const int sm = p.store_mask;
-    // Element l of a tile: plain copies go global -> shared with cp.async (no
-    // register round trip, every element in flight at once); the synthesised
-    // |j> and the zero chi / v are written by the thread.
+    // Element l of a live tile: plain copies go global -> shared with cp.async
+    // (no register round trip, every element in flight at once); the
+    // synthesised |j> and the zero chi / v are written by the thread.
     auto load_elem = [&](u64 a, unsigned sl, bool live) {
         GF_DCHECK(a < p.N && sl < T);
         if constexpr (SYNTH)
@@ -1468,16 +1439,15 @@ __global__ void __launch_bounds__(NT, (GF_NT512_M11 && NT == 512) ? 2
         else if (live)
             cp_async16(&t0[sl], &psi[a]);
         if constexpr (NV >= 2) {
-            if constexpr (!(REV && FIRST)) cp_async16(&t1[sl], &bra[a]);
+            if constexpr (!(REV && FIRST)) {
+                if (live) cp_async16(&t1[sl], &bra[a]);
+            }
         }
         if constexpr (NV >= 3) {
-            // chi is carried through dead tiles while a later pass reads it
-            // (store_mask bit 2); v is zero there
-            const bool need = ASC ? live : (live || (sm & 4));
 #pragma unroll
             for (int d = 0; d < ND; ++d) {
                 if constexpr (FIRST) t2[d * T + sl] = czero();
-                else if (need) cp_async16(&t2[d * T + sl], &aux[a + d * p.auxstride]);
+                else if (live) cp_async16(&t2[d * T + sl], &aux[a + d * p.auxstride]);
             }
         }
     };
@@ -1486,7 +1456,7 @@ __global__ void __launch_bounds__(NT, (GF_NT512_M11 && NT == 512) ? 2
     } else if (blockIdx.x < p.ntiles) {
         const u64 base = tile_base(blockIdx.x);
         const bool live = is_live(base);
-        if (!(FWDOP && !FIRST && !live))
+        if (live || FIRST)
             for (unsigned l = tid; l < T; l += NT) load_elem(base + (l & cmask) + hiofs[l >> c], sw(l), live);
     }
     cp_async_commit();
@@ -1518,11 +1488,11 @@ __global__ void __launch_bounds__(NT, (GF_NT512_M11 && NT == 512) ? 2
         const u64 pofs = ((u64)blockIdx.y * p.ctas + blockIdx.x) * 32;
         if (live) {
             if constexpr (VAR == 4)
-                run_units<OP, NT, false>(p, t0, t1, t2, scratch, ubase, pofs, tile != blockIdx.x, tpop, T);
+                run_units<OP, NT>(p, t0, t1, t2, scratch, ubase, pofs, tile != blockIdx.x, tpop, T);
             else
-                run_slots<OP, NT, ND, VAR, false>(p, t0, t1, t2, scratch, pofs, tile != blockIdx.x, tpop, T);
+                run_slots<OP, NT, ND, VAR>(p, t0, t1, t2, scratch, pofs, tile != blockIdx.x, tpop, T);
         } else if constexpr (!FWDOP) {
-            // dead tile: backward vectors only; its hole partials are exact zeros
+            // the hole partials of a dead tile are exact zeros
             if (tile == blockIdx.x) {
                 constexpr bool HDP = (OP == OP_REV_G || OP == OP_REV_GH);
                 constexpr bool HHP = (OP == OP_REV_GH || OP == OP_REV_H || OP == OP_ASC_H);
@@ -1535,10 +1505,6 @@ __global__ void __launch_bounds__(NT, (GF_NT512_M11 && NT == 512) ? 2
                     }
                 }
             }
-            if constexpr (VAR == 4)
-                run_units<OP, NT, true>(p, t0, t1, t2, scratch, ubase, pofs, tile != blockIdx.x, tpop, T);
-            else
-                run_slots<OP, NT, ND, VAR, true>(p, t0, t1, t2, scratch, pofs, tile != blockIdx.x, tpop, T);
         }
 
         // Write the tile back and, element by element, start the next tile's
@@ -1550,19 +1516,19 @@ __global__ void __launch_bounds__(NT, (GF_NT512_M11 && NT == 512) ? 2
         const bool more = next < p.ntiles && !p.exp_noio;
         const u64 nbase = more ? tile_base(next) : 0ull;
         const bool nlive = more ? is_live(nbase) : true;
-        const bool reload = more && !(FWDOP && !FIRST && !nlive);
-        // psi / v of a dead tile: zeros written by the first pass, untouched later
+        const bool reload = more && (nlive || FIRST);
+        // dead tile in a first pass: zeros for psi (synthesised sweeps) and chi / v, w phi0 for the bra
         const bool wpsi = (sm & 1) && (live || SYNTH);
-        const bool waux = (sm & 4) && (ASC ? (live || FIRST) : true);
-        const bool skip = FWDOP && !FIRST && !live;  // nothing was loaded
+        const bool wbra = (sm & 2) && (live || (REV && FIRST));
+        const bool waux = (sm & 4) && (live || FIRST);
+        const bool skip = !live && !FIRST;  // nothing was loaded, nothing changes
         for (unsigned l = tid; l < T && !p.exp_noio; l += NT) {
             const u64 o = (l & cmask) + hiofs[l >> c];
             const u64 a = base + o;
             const unsigned sl = sw(l);
             if (!skip) {
-                const double2 x = t0[sl];
-                if (wpsi) psi[a] = x;
-                if constexpr (NV >= 2) if (sm & 2) bra[a] = t1[sl];
+                if (wpsi) psi[a] = t0[sl];
+                if constexpr (NV >= 2) if (wbra) bra[a] = t1[sl];
                 if constexpr (NV >= 3) {
                     if (waux) {
 #pragma unroll
@@ -1570,11 +1536,14 @@ __global__ void __launch_bounds__(NT, (GF_NT512_M11 && NT == 512) ? 2
                     }
                 }
                 if constexpr (OP == OP_FWD_DOT) {
-                    const double2 f = cscale(phi0[a], w);
-                    vre = fma(f.x, x.x, vre);
-                    vre = fma(-f.y, x.y, vre);
-                    vim = fma(f.x, x.y, vim);
-                    vim = fma(f.y, x.x, vim);
+                    if (live) {
+                        const double2 x = t0[sl];
+                        const double2 f = cscale(phi0[a], w);
+                        vre = fma(f.x, x.x, vre);
+                        vre = fma(-f.y, x.y, vre);
+                        vim = fma(f.x, x.y, vim);
+                        vim = fma(f.y, x.x, vim);
+                    }
                 }
             }
             if (reload) load_elem(nbase + o, sl, nlive);
