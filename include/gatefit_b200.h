@@ -167,6 +167,15 @@ int gf_plan_phase_times(gf_plan *plan, double *ms4, int64_t *launches4);
 int gf_plan_describe(const gf_plan *plan, int *fused, int *tile_bits, int *n_fwd_passes, int *n_rev_passes,
                      int *ctas);
 
+/* Light cone of the basis states (new; no reference counterpart: the
+ * reference applies every slot to the whole vector, objective.py:310-337).
+ * psi_l = G_l ... G_1 |j> vanishes wherever a qubit no applied slot has touched
+ * differs from j, so the fused engine skips the tiles that disagree with j on
+ * such a qubit.  frac3 = fraction of the slot work still executed in the
+ * forward, reverse and ascending sweeps (1.0 = nothing skipped; GF_LIGHTCONE=0
+ * disables the rule). */
+int gf_plan_live_fraction(const gf_plan *plan, double *frac3);
+
 /* Host-only query of the fused pass plan (no device work): the passes the
  * engine would run for slots (t1[s], t2[s]) on k qubits (sector -1/0/1) with
  * 2^tile_bits-amplitude tiles; sweep 0 = forward, 1 = reverse.  Writes the

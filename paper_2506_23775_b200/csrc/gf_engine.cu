@@ -30,6 +30,7 @@
 #include <type_traits>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -2216,8 +2217,12 @@ struct PassChoice {
 // FMAXSLOTS).  Expands every S from the best `beam` states per depth and stops
 // at the first depth that executes all slots.  Used when the sets are few
 // (c2: C(13, 8) = 1287 at m = 11, c = 3) and the slots fit a 64-bit mask.
+// With the light-cone rule (FusedParams::fixmask) plans of equal pass count
+// differ in how much slot work their dead tiles skip: `cost` = sum over passes
+// of slots x 2^-(fixed global bits), minimised among the plans of the first
+// complete depth.
 static bool plan_exact(const gf_plan *p, const std::vector<int> &order, int m, int c, int max_depth,
-                       std::vector<PassChoice> &out)
+                       std::vector<PassChoice> &out, bool reverse)
 {
     const int n = (int)order.size(), K = p->K, nf = K - c, kf = m - c;
     if (n > 64 || nf > 40 || kf < 0 || kf > nf) return false;
@@ -2263,10 +2268,25 @@ static bool plan_exact(const gf_plan *p, const std::vector<int> &order, int m, i
     const unsigned long long all = n == 64 ? ~0ull : ((1ull << n) - 1ull);
     struct St {
         unsigned long long done;
+        double cost;
         std::vector<std::pair<unsigned long long, unsigned long long>> hist;  // (taken, S)
+    };
+    const unsigned long long allbits = K >= 64 ? ~0ull : ((1ull << K) - 1ull);
+    // slot work of a pass weighted by its live-tile fraction
+    auto pass_cost = [&](unsigned long long done, unsigned long long tk, unsigned long long S) {
+        if (!p->lightcone) return (double)__builtin_popcountll(tk);
+        unsigned long long applied = 0ull;
+        for (int t = 0; t < n; ++t) {
+            const bool is_done = (done >> t) & 1ull;
+            // forward: slots of the earlier passes; reverse: every slot not yet undone (this pass included)
+            if (reverse ? !is_done : is_done) applied |= bits[t];
+        }
+        const int fixed = __builtin_popcountll(~S & allbits & ~applied);
+        return __builtin_popcountll(tk) * std::ldexp(1.0, -fixed);
     };
     std::vector<St> cur(1);
     cur[0].done = 0ull;
+    cur[0].cost = 0.0;
     const size_t beam = 1500;
     for (int depth = 1; depth <= max_depth; ++depth) {
         std::map<unsigned long long, size_t> seen;
@@ -2276,10 +2296,21 @@ static bool plan_exact(const gf_plan *p, const std::vector<int> &order, int m, i
                 const unsigned long long tk = execute(s.done, S);
                 if (!tk) continue;
                 const unsigned long long nd = s.done | tk;
-                if (seen.count(nd)) continue;
+                const double cost = s.cost + pass_cost(s.done, tk, S);
+                auto it = seen.find(nd);
+                if (it != seen.end()) {
+                    St &o = nxt[it->second];
+                    if (cost < o.cost - 1e-12) {  // same slots done, cheaper passes
+                        o.cost = cost;
+                        o.hist = s.hist;
+                        o.hist.push_back({tk, S});
+                    }
+                    continue;
+                }
                 seen[nd] = nxt.size();
                 St e;
                 e.done = nd;
+                e.cost = cost;
                 e.hist = s.hist;
                 e.hist.push_back({tk, S});
                 nxt.push_back(std::move(e));
@@ -2288,7 +2319,9 @@ static bool plan_exact(const gf_plan *p, const std::vector<int> &order, int m, i
         if (nxt.empty()) return false;
         std::stable_sort(nxt.begin(), nxt.end(), [](const St &a, const St &b) {
             const int pa = __builtin_popcountll(a.done), pb = __builtin_popcountll(b.done);
-            return pa != pb ? pa > pb : a.done < b.done;
+            if (pa != pb) return pa > pb;
+            if (a.cost != b.cost) return a.cost < b.cost;
+            return a.done < b.done;
         });
         if (nxt[0].done == all) {
             out.clear();
@@ -2424,7 +2457,8 @@ static std::vector<FusedParams> plan_passes(const gf_plan *p, bool reverse, int 
         std::vector<int> order;
         for (int i = 0; i < n; ++i) order.push_back(reverse ? n - 1 - i : i);
         std::vector<PassChoice> ex;
-        if (choice.size() > 1 && !getenv("GF_PLAN_GREEDY") && plan_exact(p, order, m, c, (int)choice.size() - 1, ex))
+        if (choice.size() > 1 && !getenv("GF_PLAN_GREEDY") &&
+            plan_exact(p, order, m, c, (int)choice.size() - (p->lightcone ? 0 : 1), ex, reverse))
             choice = ex;
     }
     for (const PassChoice &pc : choice) {
@@ -3001,6 +3035,7 @@ extern "C" int gf_plan_layout(int k, int sector, int n_slots, const int32_t *t1,
     tmp.fm = kn.fm;
     tmp.fc = kn.fc;
     tmp.c1q_dmma = kn.c1q_dmma;
+    tmp.lightcone = kn.lightcone;
     std::vector<FusedParams> passes = plan_passes(&tmp, sweep != 0, tmp.fm);
     if ((int)passes.size() > max_passes) return gf_fail(GF_EINVAL, "%zu passes exceed the output room", passes.size());
     *n_passes = (int)passes.size();
@@ -3012,6 +3047,26 @@ extern "C" int gf_plan_layout(int k, int sector, int n_slots, const int32_t *t1,
         pass_bits[i] = bits;
         for (int t = 0; t < passes[i].nslots; ++t) slot_order[o++] = passes[i].ps[t].slot;
     }
+    return GF_OK;
+}
+
+// Live fraction of the slot work per sweep under the light-cone rule
+// (FusedParams::fixmask): sum over passes of slots x 2^-popcount(fixmask),
+// divided by the slot count.  frac3 = {forward, reverse, ascending}.
+extern "C" int gf_plan_live_fraction(const gf_plan *p, double *frac3)
+{
+    if (!p || !frac3) return gf_fail(GF_EINVAL, "null argument");
+    auto frac = [&](const std::vector<FusedParams> &v) {
+        double live = 0.0, tot = 0.0;
+        for (const FusedParams &f : v) {
+            live += f.nslots * std::ldexp(1.0, -__builtin_popcountll(f.fixmask));
+            tot += f.nslots;
+        }
+        return tot > 0.0 ? live / tot : 1.0;
+    };
+    frac3[0] = p->fused ? frac(p->fwd_passes) : 1.0;
+    frac3[1] = p->fused ? frac(p->rev_passes) : 1.0;
+    frac3[2] = p->fused ? frac(p->asc_passes) : 1.0;
     return GF_OK;
 }
 

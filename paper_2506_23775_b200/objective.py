@@ -233,7 +233,10 @@ class EnginePlan:
         v = (ctypes.c_int * 5)()
         _lib.check(_lib.lib.gf_plan_describe(self.h, ctypes.byref(v, 0), ctypes.byref(v, 4), ctypes.byref(v, 8),
                                              ctypes.byref(v, 12), ctypes.byref(v, 16)))
-        return {"fused": bool(v[0]), "tile_bits": v[1], "fwd_passes": v[2], "rev_passes": v[3], "ctas": v[4]}
+        f = (ctypes.c_double * 3)()
+        _lib.check(_lib.lib.gf_plan_live_fraction(self.h, f))
+        return {"fused": bool(v[0]), "tile_bits": v[1], "fwd_passes": v[2], "rev_passes": v[3], "ctas": v[4],
+                "live_fraction": {"forward": f[0], "reverse": f[1], "ascending": f[2]}}
 
     def last_launches(self) -> int:
         return int(_lib.lib.gf_plan_last_launches(self.h))
