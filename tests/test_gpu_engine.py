@@ -398,6 +398,40 @@ def test_sector_engine_variants_vs_reference_sums(monkeypatch, knobs):
         assert abs(-val - ref_v.real) < TOL * max(1, abs(ref_v))
 
 
+@pytest.mark.parametrize("case", ["c2_slice", "sector"])
+def test_light_cone_rule_changes_nothing(monkeypatch, case):
+    """Dead-tile skipping (tiles outside the basis state's light cone hold
+    psi = v = 0 and are skipped in the reverse and ascending sweeps alike) is
+    exact: value, gradient and HVP agree with GF_LIGHTCONE=0 to rounding, and
+    the plan reports how much slot work is left."""
+    from paper_2506_23775_b200 import objective as obj
+
+    if case == "c2_slice":
+        spec, circ, rng = gf.spinful_layer_circuit(8, 5, False, seed=1)
+        orc = gf.ChebyshevOracle(spec, 0.25)
+        kw = dict(basis=np.arange(96, dtype=np.int64) * 677 % 65536)
+        parity = False
+    else:
+        spec, circ, rng = gf.spinful_layer_circuit(7, 4, True, seed=11, parity=True)
+        orc = gf.ChebyshevOracle(spec, 0.25)
+        kw = dict(sector=0, basis=(np.arange(40, dtype=np.int64) * 211 % (1 << 13), None))
+        parity = True
+    X = [manifold.project_tangent_gate(g.matrix, rng.normal(size=(4, 4)) + 1j * rng.normal(size=(4, 4)), parity)
+         for g in circ.logical_gates]
+    out = {}
+    for lc in ("1", "0"):
+        monkeypatch.setenv("GF_LIGHTCONE", lc)
+        rep, hv = gf.gradient_and_hvp(circ, orc, X, parity_mode=parity, **kw)
+        live = list(obj._PLANS.values())[-1].describe()["live_fraction"]
+        out[lc] = (rep.value, np.stack(rep.holomorphic_derivatives), np.stack(hv), live)
+    assert abs(out["1"][0] - out["0"][0]) < 1e-12 * max(1.0, abs(out["0"][0]))
+    assert rel_err(out["1"][1], out["0"][1]) < 1e-12
+    assert rel_err(out["1"][2], out["0"][2]) < 1e-12
+    assert all(v == 1.0 for v in out["0"][3].values())
+    assert all(0.0 < v <= 1.0 for v in out["1"][3].values()) and out["1"][3]["forward"] < 1.0
+    assert out["1"][3]["reverse"] == out["1"][3]["ascending"]
+
+
 @pytest.mark.parametrize("name", ["sector_l4p", "sector_l6p"])
 def test_fold_engine_vs_reference_even_sum(name):
     g = golden(name)
