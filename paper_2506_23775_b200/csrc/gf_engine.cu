@@ -1378,6 +1378,40 @@ __global__ void __launch_bounds__(NT, (GF_NT512_M11 && NT == 512) ? 2
     double *scratch = reinterpret_cast<double *>(t0 + NV * T);  // [NH][NW][64]; unit passes [2][NH][NW][8]
     u64 *hiofs = reinterpret_cast<u64 *>(scratch + (VAR == 4 ? 2 * NH * NW * 8 : NH * NW * 64));
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // A CTA whose tiles are all dead (light cone, below) has nothing to do
+    // outside a sweep's first pass: leave before building the tables.  Its
+    // hole partials are exact zeros.
+    if constexpr (!FIRST) {
+        if (p.fixmask) {
+            const u64 jb0 = (u64)p.basis[blockIdx.y];
+            bool any = false;
+            for (u64 tile = blockIdx.x; tile < p.ntiles && !any; tile += gridDim.x) {
+                u64 base = 0;
+                for (int i = 0; i < p.nglob; ++i)
+                    if ((tile >> i) & 1ull) base |= 1ull << p.gpos[i];
+                any = ((jb0 ^ base) & p.fixmask) == 0ull;
+            }
+            if (!any) {
+                constexpr bool HDP = (OP == OP_REV_G || OP == OP_REV_GH);
+                constexpr bool HHP = (OP == OP_REV_GH || OP == OP_REV_H || OP == OP_ASC_H);
+                if constexpr (HDP || HHP) {
+                    const u64 pofs = ((u64)blockIdx.y * p.ctas + blockIdx.x) * 32;
+                    for (int e = tid; e < p.nslots * 32 * NH; e += NT) {
+                        const int si = e / (32 * NH), hole = (e / 32) % NH, i = e & 31;
+                        if ((hole == 0 && HDP) || (hole >= 1 && HHP)) {
+                            double *dst = (hole == 0 ? p.partD : p.partH + (u64)(hole - 1) * p.hstride) +
+                                          (u64)p.ps[si].slot * p.nvec * p.ctas * 32 + pofs + i;
+                            *dst = 0.0;
+                        }
+                    }
+                }
+                if constexpr (HV) {
+                    if (tid < 2) p.partV[((u64)blockIdx.y * p.ctas + blockIdx.x) * 2 + tid] = 0.0;
+                }
+                return;
+            }
+        }
+    }
     // unit passes: per-(slot, thread) tile index of the thread's first unit
     unsigned short *ubase = reinterpret_cast<unsigned short *>(hiofs + (1 << (p.m - p.c)));
     if constexpr (VAR == 4) unit_bases<NT>(p, ubase, T);
