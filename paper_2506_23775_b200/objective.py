@@ -288,7 +288,9 @@ def _default_batch(N: int, total: int) -> int:
     env = os.environ.get("GF_BATCH")
     if env:
         return max(1, min(int(env), total))
-    budget = 512 * 2**20  # bytes per workspace vector (3 resident): batch 512 at 16 qubits
+    # bytes per workspace vector (3 resident): batch 2048 at 16 qubits (measured at c2:
+    # 50 355 / 51 250 / 51 827 / 51 860 summand-evals/s at batch 512 / 1024 / 2048 / 4096)
+    budget = 2048 * 2**20
     return max(1, min(total, budget // (16 * N)))
 
 

@@ -1,7 +1,7 @@
 """BASELINE configs at their stated sizes against independent paths (GPU).
 
-* c2 (configs[1]): 1024 seeded summands at the bench's launch shape (batch
-  512, two batches, the exact 3-pass plan) against the CPU oracle port of the
+* c2 (configs[1]): 1024 seeded summands on the bench's plan (the exact 3-pass
+  plan; batch 512, two batches -- the bench runs batches of 2048) against the CPU oracle port of the
   reference's cached-pass drivers (_gradient_chunk / _hvp_chunk,
   objective.py:322-337, 432-482).
 * c3 (configs[2]): L=12 open, 24 qubits, even sector compressed to 2^23
@@ -63,7 +63,7 @@ def test_c2_1024_summands_bench_shape_vs_oracle_port():
     cache = gf.models.CachedTargetColumns(orc, k, 0, idx.size, indices=idx, batch=512)
     rep, hv = gf.gradient_and_hvp(circ, cache, X, basis=(idx, None), batch=512)
     plan = list(obj._PLANS.values())[-1]
-    assert plan.batch == 512 and plan.describe()["rev_passes"] == 3  # the bench's launch shape
+    assert plan.batch == 512 and plan.describe()["rev_passes"] == 3  # the bench's plan (it runs batches of 2048)
     P = cache.rows.cpu().numpy()
     oplan = _oracle_plan(circ)
     fn = lambda jj: P[np.searchsorted(idx, jj)]
