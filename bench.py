@@ -536,6 +536,10 @@ def run_b200(args):
     ms4 = np.zeros(4)
     l4 = np.zeros(4, dtype=np.int64)
     gf._lib.check(gf._lib.lib.gf_plan_phase_times(plan.h, ms4.ctypes.data, l4.ctypes.data))
+    import ctypes as _ct
+    r1_ms, r1_l, r1_v, r1_s = _ct.c_double(0), _ct.c_int64(0), _ct.c_int64(0), _ct.c_int(0)
+    gf._lib.check(gf._lib.lib.gf_plan_first_reverse_pass(plan.h, _ct.byref(r1_ms), _ct.byref(r1_l), _ct.byref(r1_v),
+                                                         _ct.byref(r1_s)))
     gf._lib.check(gf._lib.lib.gf_plan_set_profiling(plan.h, 0))
     n = circ.num_slots
     my_summands = (p1 - p0) * args.steps
@@ -568,6 +572,17 @@ def run_b200(args):
             phases[nm]["hbm_gbs_pass_model"] = round(pass_bytes[nm] * l4[i] / (ms4[i] * 1e-3) / 1e9, 1)
     dom = max(("forward", "reverse", "ascending"), key=lambda k: ms4[names.index(k)])
     achieved = phases[dom]["fp64_tflops"]
+    # the dominant launch: the reverse sweep's first pass (every tile live, so
+    # executed = algorithmic flops): 6 units of 32 flop per amplitude per slot
+    rev1 = None
+    if r1_ms.value > 0 and r1_l.value > 0:
+        fl = 6 * 32.0 * N * r1_s.value * r1_v.value
+        rev1 = {"kernel": "k_fused<OP_REV_GH, FIRST>: first reverse pass, %d slots, every tile live" % r1_s.value,
+                "launches": int(r1_l.value), "ms_per_launch": round(r1_ms.value / r1_l.value, 4),
+                "share_of_step": round(r1_ms.value / ms4.sum(), 4) if ms4.sum() else None,
+                "fp64_tflops": round(fl / (r1_ms.value * 1e-3) / 1e12, 3)}
+        if dom == "reverse":
+            achieved = rev1["fp64_tflops"]
     traffic = None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tf):
@@ -657,7 +672,11 @@ def run_b200(args):
             "engine": dict(plan_shape, batch=batch, chunk=chunk, oracle_setup_s=round(oracle_setup_s, 3),
                            l2="inputs larger than L2 (phi0 cache %d MiB per GPU; workspace 3 x batch x 1 MiB)" %
                               ((p1 - p0) * N * 16 >> 20)),
-            "roofline": {"bound": "tensor", "kernel": f"k_fused ({dom} sweep: fused tile passes, FP64 DMMA)",
+            "roofline": {"bound": "tensor",
+                         "kernel": (rev1["kernel"] if (rev1 and dom == "reverse") else
+                                    f"k_fused ({dom} sweep: fused tile passes, FP64 DMMA)"),
+                         "dominant_launch": rev1,
+                         "sweep_executed_tflops": phases[dom]["fp64_tflops"],
                          "achieved": achieved, "peak": peaks64["dmma_tflops"], "unit": "TFLOP/s",
                          "frac": round(achieved / peaks64["dmma_tflops"], 4), "traffic": traffic,
                          "peak_source": "measured in this run: back-to-back DMMA.8x8x4 on all SMs "
@@ -667,10 +686,12 @@ def run_b200(args):
                          "live_fraction": phases[dom]["live_fraction"],
                          "algorithmic_flops": "32 flop per amplitude per dense gate / hole (SURVEY 8(d) units); "
                                               "reverse sweep 6, ascending 5, forward 1 per slot; x 2^16 amplitudes x "
-                                              "36 slots x summands.  `achieved` counts the flops the engine "
-                                              "executes: it skips the tiles outside the basis state's light cone "
-                                              "(psi = 0 there), live_fraction of the slot work; algorithmic_tflops "
-                                              "counts the full-vector passes of the reference",
+                                              "36 slots x summands.  `achieved` is the dominant launch (the "
+                                              "reverse sweep's first pass: every tile live, executed = algorithmic "
+                                              "flops over its CUDA-event time); sweep_executed_tflops counts the "
+                                              "flops the whole sweep executes (it skips the tiles outside the basis "
+                                              "state's light cone, psi = 0 there: live_fraction of the slot work); "
+                                              "algorithmic_tflops counts the full-vector passes of the reference",
                          "hbm_view": {"peak_gbs": peak, "peak_source": peak_src,
                                       "note": "HBM bytes per fused pass = 32 B x vectors touched x amplitudes; the "
                                               "fused sweeps make ~5 HBM round trips per 36 slots, so they are not "

@@ -162,6 +162,10 @@ int64_t gf_plan_last_launches(const gf_plan *plan);
  * [forward sweep, reverse sweep, ascending sweep, reductions]. */
 int gf_plan_set_profiling(gf_plan *plan, int on);
 int gf_plan_phase_times(gf_plan *plan, double *ms4, int64_t *launches4);
+/* Profiling detail (new): the first reverse pass of the profiled evaluations
+ * -- the sweep's dominant launch, every tile live -- accumulated device time
+ * in ms, launches, summand vectors processed and the slots of the pass. */
+int gf_plan_first_reverse_pass(gf_plan *plan, double *ms, int64_t *launches, int64_t *vectors, int *slots);
 /* Engine shape of a plan: fused tile engine on/off, local (tile) bits, number
  * of fused passes per forward / reverse sweep, CTAs per summand. */
 int gf_plan_describe(const gf_plan *plan, int *fused, int *tile_bits, int *n_fwd_passes, int *n_rev_passes,

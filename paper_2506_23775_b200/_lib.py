@@ -41,6 +41,7 @@ EXPORTS = (
     "gf_plan_phase_times",
     "gf_plan_describe",
     "gf_plan_live_fraction",
+    "gf_plan_first_reverse_pass",
     "gf_plan_layout",
     "gf_plan_destroy",
     "gf_hess_plan_create",
@@ -109,6 +110,7 @@ for _name, _args in {
     "gf_hess_plan_destroy": [_vp],
     "gf_plan_describe": [_vp, _vp, _vp, _vp, _vp, _vp],
     "gf_plan_live_fraction": [_vp, _vp],
+    "gf_plan_first_reverse_pass": [_vp, _vp, _vp, _vp, _vp],
     "gf_plan_layout": [_i, _i, _i, _vp, _vp, _i, _i, _i, _vp, _vp, _vp, _vp],
     "gf_plan_set_profiling": [_vp, _i],
     "gf_plan_phase_times": [_vp, _vp, _vp],

@@ -1476,6 +1476,8 @@ __global__ void __launch_bounds__(NT, (GF_NT512_M11 && NT == 512) ? 2
         if constexpr (NV >= 2) {
             if constexpr (!(REV && FIRST)) {
                 if (live) cp_async16(&t1[sl], &bra[a]);
+            } else {
+                if (!p.weights) cp_async16(&t1[sl], &phi0[a]);  // bra_0 = phi0 (unit weight): plain copy
             }
         }
         if constexpr (NV >= 3) {
@@ -1502,9 +1504,11 @@ __global__ void __launch_bounds__(NT, (GF_NT512_M11 && NT == 512) ? 2
         const bool live = is_live(base);
         if constexpr (REV && FIRST) {
             // bra_0 = w phi0; the value <phi0|psi_n> is read back from the tile
-            for (unsigned l = tid; l < T; l += NT) {
-                const u64 a = base + (l & cmask) + hiofs[l >> c];
-                t1[sw(l)] = cscale(phi0[a], w);
+            if (p.weights) {
+                for (unsigned l = tid; l < T; l += NT) {
+                    const u64 a = base + (l & cmask) + hiofs[l >> c];
+                    t1[sw(l)] = cscale(phi0[a], w);
+                }
             }
             cp_async_wait<0>();
             for (unsigned l = tid; l < T && live; l += NT) {
@@ -1770,6 +1774,12 @@ struct gf_plan {
     bool profiling = false;
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     double phase_ms[4] = {0, 0, 0, 0};  // accumulated: forward, reverse, ascending, reduce
+    // the first reverse pass alone (the sweep's dominant launch: every tile is live)
+    cudaEvent_t ev_rev1 = nullptr;
+    bool rev1_pending = false;
+    double rev1_ms = 0.0;
+    int64_t rev1_launches = 0, rev1_vectors = 0;
+    int rev1_slots = 0;
     int64_t phase_launches[4] = {0, 0, 0, 0};
     int pending = 0;
 };
@@ -1930,6 +1940,7 @@ static void plan_free(gf_plan *p)
     cudaFree(p->d_frag);
     for (auto &e : p->ev)
         if (e) cudaEventDestroy(e);
+    if (p->ev_rev1) cudaEventDestroy(p->ev_rev1);
     void *ptrs[] = {p->psi, p->bra, p->aux, p->partD, p->partHd, p->partHa, p->partV,
                     p->qD, p->qHd, p->qHa, p->qV, p->d_lstart, p->d_lslots, p->d_swapped};
     for (void *q : ptrs)
@@ -2834,6 +2845,13 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
                     if (pi == 0) { int rc_ = launch_fused<OP_REV_G, true>(p, fp, nvec, st); if (rc_) return rc_; }
                     else { int rc_ = launch_fused<OP_REV_G, false>(p, fp, nvec, st); if (rc_) return rc_; }
                 }
+                if (pi == 0 && p->profiling && p->ev_rev1) {
+                    GF_CUDA(cudaEventRecord(p->ev_rev1, st));
+                    p->rev1_pending = true;
+                    p->rev1_slots = fp.nslots;
+                    p->rev1_vectors += nvec;
+                    p->rev1_launches += 1;
+                }
                 ++launches;
             }
             l_rev = launches - l_fwd;
@@ -2994,6 +3012,12 @@ static int collect_phases(gf_plan *p)
         GF_CUDA(cudaEventElapsedTime(&ms, p->ev[i], p->ev[i + 1]));
         p->phase_ms[i] += ms;
     }
+    if (p->rev1_pending) {
+        float ms = 0.f;
+        GF_CUDA(cudaEventElapsedTime(&ms, p->ev[1], p->ev_rev1));
+        p->rev1_ms += ms;
+        p->rev1_pending = false;
+    }
     p->pending = 0;
     return GF_OK;
 }
@@ -3003,8 +3027,12 @@ extern "C" int gf_plan_set_profiling(gf_plan *p, int on)
     if (!p) return gf_fail(GF_EINVAL, "null plan");
     if (on && !p->ev[0])
         for (auto &e : p->ev) GF_CUDA(cudaEventCreate(&e));
+    if (on && !p->ev_rev1) GF_CUDA(cudaEventCreate(&p->ev_rev1));
     p->profiling = on != 0;
     p->pending = 0;
+    p->rev1_pending = false;
+    p->rev1_ms = 0.0;
+    p->rev1_launches = p->rev1_vectors = 0;
     for (int i = 0; i < 4; ++i) {
         p->phase_ms[i] = 0.0;
         p->phase_launches[i] = 0;
@@ -3021,6 +3049,22 @@ extern "C" int gf_plan_phase_times(gf_plan *p, double *ms4, int64_t *launches4)
         ms4[i] = p->phase_ms[i];
         if (launches4) launches4[i] = p->phase_launches[i];
     }
+    return GF_OK;
+}
+
+// First reverse pass of the profiled evaluations: accumulated device time,
+// launches, summand vectors processed and the slots of the pass.
+extern "C" int gf_plan_first_reverse_pass(gf_plan *p, double *ms, int64_t *launches, int64_t *vectors, int *slots)
+{
+    if (!p) return gf_fail(GF_EINVAL, "null plan");
+    if (p->pending) {
+        int rc = collect_phases(p);
+        if (rc) return rc;
+    }
+    if (ms) *ms = p->rev1_ms;
+    if (launches) *launches = p->rev1_launches;
+    if (vectors) *vectors = p->rev1_vectors;
+    if (slots) *slots = p->rev1_slots;
     return GF_OK;
 }
 

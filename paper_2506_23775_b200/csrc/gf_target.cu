@@ -568,15 +568,28 @@ __global__ void __launch_bounds__(1024) k_nb_series(double2 *__restrict__ out, c
     double2 *cur = nb_smem, *prev = nb_smem + D;
     double2 *row = out + b * D;
     const double2 c0 = coefs[0];
-    for (long long x = threadIdx.x; x < D; x += blockDim.x) {
-        const double v = (x == b) ? 1.0 : 0.0;
-        cur[x] = make_double2(v, 0.0);
-        row[x] = make_double2(c0.x * v, c0.y * v);
+    // the thread's entries of the result row accumulate in registers (D <= 6400,
+    // at least 32 threads per 32 entries: at most NB_ACC entries per thread)
+    constexpr int NB_ACC = 8;
+    double2 acc[NB_ACC];
+#pragma unroll
+    for (int i = 0; i < NB_ACC; ++i) acc[i] = make_double2(0.0, 0.0);
+    {
+        int i = 0;
+        for (long long x = threadIdx.x; x < D; x += blockDim.x, ++i) {
+            const double v = (x == b) ? 1.0 : 0.0;
+            cur[x] = make_double2(v, 0.0);
+            const double2 a0 = make_double2(c0.x * v, c0.y * v);
+#pragma unroll
+            for (int q = 0; q < NB_ACC; ++q)
+                if (q == i) acc[q] = a0;
+        }
     }
     __syncthreads();
     for (int m = 1; m <= norder; ++m) {
         const double2 cm = coefs[m];
-        for (long long x = threadIdx.x; x < D; x += blockDim.x) {
+        int i = 0;
+        for (long long x = threadIdx.x; x < D; x += blockDim.x, ++i) {
             const double2 cc = cur[x];
             double2 h = cscale(cc, diag[x]);
             const int k = cnt[x];
@@ -594,16 +607,26 @@ __global__ void __launch_bounds__(1024) k_nb_series(double2 *__restrict__ out, c
                 h.y = 2.0 * h.y - p.y;
             }
             prev[x] = h;
-            double2 a = row[x];
             const double2 ch = cmul(cm, h);
-            a.x += ch.x;
-            a.y += ch.y;
-            row[x] = a;
+#pragma unroll
+            for (int q = 0; q < NB_ACC; ++q)
+                if (q == i) {
+                    acc[q].x += ch.x;
+                    acc[q].y += ch.y;
+                }
         }
         __syncthreads();
         double2 *t = cur;
         cur = prev;
         prev = t;
+    }
+    {
+        int i = 0;
+        for (long long x = threadIdx.x; x < D; x += blockDim.x, ++i) {
+#pragma unroll
+            for (int q = 0; q < NB_ACC; ++q)
+                if (q == i) row[x] = acc[q];
+        }
     }
 }
 
