@@ -1774,6 +1774,15 @@ struct gf_plan {
     bool profiling = false;
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     double phase_ms[4] = {0, 0, 0, 0};  // accumulated: forward, reverse, ascending, reduce
+    // one event set per profiled evaluation, collected without a host sync per
+    // evaluation (ev / ev_rev1 alias the current set)
+    struct EvSet {
+        cudaEvent_t ev[5];
+        cudaEvent_t rev1;
+        bool has_rev1;
+    };
+    std::vector<EvSet> evsets;
+    size_t ev_used = 0;
     // the first reverse pass alone (the sweep's dominant launch: every tile is live)
     cudaEvent_t ev_rev1 = nullptr;
     bool rev1_pending = false;
@@ -1938,9 +1947,12 @@ static int upload_frags(gf_plan *p, cudaStream_t st)
 static void plan_free(gf_plan *p)
 {
     cudaFree(p->d_frag);
-    for (auto &e : p->ev)
-        if (e) cudaEventDestroy(e);
-    if (p->ev_rev1) cudaEventDestroy(p->ev_rev1);
+    for (auto &es : p->evsets) {
+        for (auto &e : es.ev)
+            if (e) cudaEventDestroy(e);
+        if (es.rev1) cudaEventDestroy(es.rev1);
+    }
+    p->evsets.clear();
     void *ptrs[] = {p->psi, p->bra, p->aux, p->partD, p->partHd, p->partHa, p->partV,
                     p->qD, p->qHd, p->qHa, p->qV, p->d_lstart, p->d_lslots, p->d_swapped};
     for (void *q : ptrs)
@@ -2319,7 +2331,7 @@ static bool plan_exact(const gf_plan *p, const std::vector<int> &order, int m, i
     const unsigned long long allbits = K >= 64 ? ~0ull : ((1ull << K) - 1ull);
     // slot work of a pass weighted by its live-tile fraction
     auto pass_cost = [&](unsigned long long done, unsigned long long tk, unsigned long long S) {
-        if (!p->lightcone) return (double)__builtin_popcountll(tk);
+        if (!p->lightcone) return (double)__builtin_popcountll(tk) + 1.0;
         unsigned long long applied = 0ull;
         for (int t = 0; t < n; ++t) {
             const bool is_done = (done >> t) & 1ull;
@@ -2327,62 +2339,92 @@ static bool plan_exact(const gf_plan *p, const std::vector<int> &order, int m, i
             if (reverse ? !is_done : is_done) applied |= bits[t];
         }
         const int fixed = __builtin_popcountll(~S & allbits & ~applied);
-        return __builtin_popcountll(tk) * std::ldexp(1.0, -fixed);
+        // + the pass's tile round trip on its live tiles, in slot equivalents
+        return (__builtin_popcountll(tk) + 1.0) * std::ldexp(1.0, -fixed);
     };
-    std::vector<St> cur(1);
-    cur[0].done = 0ull;
-    cur[0].cost = 0.0;
     const size_t beam = 1500;
-    for (int depth = 1; depth <= max_depth; ++depth) {
-        std::map<unsigned long long, size_t> seen;
-        std::vector<St> nxt;
-        for (const St &s : cur) {
-            for (unsigned long long S : sets) {
-                const unsigned long long tk = execute(s.done, S);
-                if (!tk) continue;
-                const unsigned long long nd = s.done | tk;
-                const double cost = s.cost + pass_cost(s.done, tk, S);
-                auto it = seen.find(nd);
-                if (it != seen.end()) {
-                    St &o = nxt[it->second];
-                    if (cost < o.cost - 1e-12) {  // same slots done, cheaper passes
-                        o.cost = cost;
-                        o.hist = s.hist;
-                        o.hist.push_back({tk, S});
+    typedef std::vector<std::pair<unsigned long long, unsigned long long>> Hist;
+    // mode 0: fewest passes (states ranked by slots done, then cost; stops at the
+    // first complete depth).  mode 1: cheapest plan within `limit` passes, ranked
+    // by cost plus a guess for the slots still to run -- with dead tiles for
+    // free, one more pass near the |j> end can cost less than a fuller live one.
+    auto search = [&](int mode, int limit, double &best_cost, Hist &best_hist) {
+        bool found = false;
+        std::vector<St> cur(1);
+        cur[0].done = 0ull;
+        cur[0].cost = 0.0;
+        for (int depth = 1; depth <= limit; ++depth) {
+            std::map<unsigned long long, size_t> seen;
+            std::vector<St> nxt;
+            for (const St &s : cur) {
+                for (unsigned long long S : sets) {
+                    const unsigned long long tk = execute(s.done, S);
+                    if (!tk) continue;
+                    const unsigned long long nd = s.done | tk;
+                    const double cost = s.cost + pass_cost(s.done, tk, S);
+                    if (nd == all) {  // complete: keep the cheapest, nothing to expand
+                        if (!found || cost < best_cost - 1e-12) {
+                            found = true;
+                            best_cost = cost;
+                            best_hist = s.hist;
+                            best_hist.push_back({tk, S});
+                        }
+                        continue;
                     }
-                    continue;
+                    auto it = seen.find(nd);
+                    if (it != seen.end()) {
+                        St &o = nxt[it->second];
+                        if (cost < o.cost - 1e-12) {  // same slots done, cheaper passes
+                            o.cost = cost;
+                            o.hist = s.hist;
+                            o.hist.push_back({tk, S});
+                        }
+                        continue;
+                    }
+                    seen[nd] = nxt.size();
+                    St e;
+                    e.done = nd;
+                    e.cost = cost;
+                    e.hist = s.hist;
+                    e.hist.push_back({tk, S});
+                    nxt.push_back(std::move(e));
                 }
-                seen[nd] = nxt.size();
-                St e;
-                e.done = nd;
-                e.cost = cost;
-                e.hist = s.hist;
-                e.hist.push_back({tk, S});
-                nxt.push_back(std::move(e));
             }
+            if (found && mode == 0) return true;
+            if (nxt.empty()) break;
+            std::stable_sort(nxt.begin(), nxt.end(), [&](const St &a, const St &b) {
+                const int pa = __builtin_popcountll(a.done), pb = __builtin_popcountll(b.done);
+                if (mode == 0) {
+                    if (pa != pb) return pa > pb;
+                    if (a.cost != b.cost) return a.cost < b.cost;
+                    return a.done < b.done;
+                }
+                const double ka = a.cost + 0.6 * (n - pa), kb = b.cost + 0.6 * (n - pb);
+                if (ka != kb) return ka < kb;
+                return a.done < b.done;
+            });
+            if (nxt.size() > beam) nxt.resize(beam);
+            cur.swap(nxt);
         }
-        if (nxt.empty()) return false;
-        std::stable_sort(nxt.begin(), nxt.end(), [](const St &a, const St &b) {
-            const int pa = __builtin_popcountll(a.done), pb = __builtin_popcountll(b.done);
-            if (pa != pb) return pa > pb;
-            if (a.cost != b.cost) return a.cost < b.cost;
-            return a.done < b.done;
-        });
-        if (nxt[0].done == all) {
-            out.clear();
-            for (const auto &h : nxt[0].hist) {
-                PassChoice pc;
-                pc.S = h.second;
-                for (int t = 0; t < n; ++t)
-                    if ((h.first >> t) & 1ull) pc.slots.push_back(order[t]);
-                out.push_back(pc);
-            }
-            return true;
-        }
-        if (nxt.size() > beam) nxt.resize(beam);
-        cur.swap(nxt);
+        return found;
+    };
+    double cost0 = 0.0, cost1 = 0.0;
+    Hist h0, h1;
+    if (!search(0, max_depth, cost0, h0)) return false;
+    const Hist *pick = &h0;
+    if (p->lightcone && !getenv("GF_PLAN_MINPASS")) {
+        // one pass more than the minimum, if that is cheaper
+        if (search(1, (int)h0.size() + 1, cost1, h1) && cost1 < cost0 - 1e-9) pick = &h1;
     }
-    return false;
+    out.clear();
+    for (const auto &h : *pick) {
+        PassChoice pc;
+        pc.S = h.second;
+        for (int t = 0; t < n; ++t)
+            if ((h.first >> t) & 1ull) pc.slots.push_back(order[t]);
+        out.push_back(pc);
+    }
+    return true;
 }
 
 // PM_UNIT geometry: the unit-index columns of a slot.  col[0] is the block
@@ -2713,7 +2755,19 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
     const size_t pstride = (size_t)32 * p->ctas * nvec;
 
     if (p->profiling) {
-        if (p->pending) collect_phases(p);
+        if (p->ev_used >= 4096) collect_phases(p);
+        if (p->ev_used == p->evsets.size()) {
+            gf_plan::EvSet es;
+            for (auto &e : es.ev) GF_CUDA(cudaEventCreate(&e));
+            GF_CUDA(cudaEventCreate(&es.rev1));
+            es.has_rev1 = false;
+            p->evsets.push_back(es);
+        }
+        gf_plan::EvSet &es = p->evsets[p->ev_used++];
+        es.has_rev1 = false;
+        for (int i = 0; i < 5; ++i) p->ev[i] = es.ev[i];
+        p->ev_rev1 = es.rev1;
+        p->pending = 1;
         GF_CUDA(cudaEventRecord(p->ev[0], st));
     }
     if (!(p->fused && n > 0)) {
@@ -2847,7 +2901,7 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
                 }
                 if (pi == 0 && p->profiling && p->ev_rev1) {
                     GF_CUDA(cudaEventRecord(p->ev_rev1, st));
-                    p->rev1_pending = true;
+                    p->evsets[p->ev_used - 1].has_rev1 = true;
                     p->rev1_slots = fp.nslots;
                     p->rev1_vectors += nvec;
                     p->rev1_launches += 1;
@@ -2991,7 +3045,6 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
     }
     if (p->profiling) {
         GF_CUDA(cudaEventRecord(p->ev[4], st));
-        p->pending = 1;
         p->phase_launches[0] += l_fwd;
         p->phase_launches[1] += l_rev;
         p->phase_launches[2] += l_asc;
@@ -3005,19 +3058,22 @@ extern "C" int gf_plan_eval(gf_plan *p, int flags, int64_t nvec, const int64_t *
 
 static int collect_phases(gf_plan *p)
 {
-    if (!p->pending) return GF_OK;
-    GF_CUDA(cudaEventSynchronize(p->ev[4]));
-    for (int i = 0; i < 4; ++i) {
-        float ms = 0.f;
-        GF_CUDA(cudaEventElapsedTime(&ms, p->ev[i], p->ev[i + 1]));
-        p->phase_ms[i] += ms;
+    if (!p->pending || p->ev_used == 0) return GF_OK;
+    GF_CUDA(cudaEventSynchronize(p->evsets[p->ev_used - 1].ev[4]));
+    for (size_t k = 0; k < p->ev_used; ++k) {
+        const gf_plan::EvSet &es = p->evsets[k];
+        for (int i = 0; i < 4; ++i) {
+            float ms = 0.f;
+            GF_CUDA(cudaEventElapsedTime(&ms, es.ev[i], es.ev[i + 1]));
+            p->phase_ms[i] += ms;
+        }
+        if (es.has_rev1) {
+            float ms = 0.f;
+            GF_CUDA(cudaEventElapsedTime(&ms, es.ev[1], es.rev1));
+            p->rev1_ms += ms;
+        }
     }
-    if (p->rev1_pending) {
-        float ms = 0.f;
-        GF_CUDA(cudaEventElapsedTime(&ms, p->ev[1], p->ev_rev1));
-        p->rev1_ms += ms;
-        p->rev1_pending = false;
-    }
+    p->ev_used = 0;
     p->pending = 0;
     return GF_OK;
 }
@@ -3025,11 +3081,9 @@ static int collect_phases(gf_plan *p)
 extern "C" int gf_plan_set_profiling(gf_plan *p, int on)
 {
     if (!p) return gf_fail(GF_EINVAL, "null plan");
-    if (on && !p->ev[0])
-        for (auto &e : p->ev) GF_CUDA(cudaEventCreate(&e));
-    if (on && !p->ev_rev1) GF_CUDA(cudaEventCreate(&p->ev_rev1));
     p->profiling = on != 0;
     p->pending = 0;
+    p->ev_used = 0;
     p->rev1_pending = false;
     p->rev1_ms = 0.0;
     p->rev1_launches = p->rev1_vectors = 0;

@@ -57,6 +57,19 @@ def slot_bits(circ, sector, s):
     return bs, bs
 
 
+def check_plan_env(circ, sector, m, sweep, env):
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        return check_plan(circ, sector, m, sweep)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
 def check_plan(circ, sector, m, sweep):
     sizes, order, pbits = layout(circ, sector, m, sweep)
     n = circ.num_slots
@@ -86,10 +99,14 @@ def test_c2_plan_is_three_passes_and_valid(sweep):
     # BASELINE configs[1]: L=8 spinful, 5 layers, 16 qubits, 36 slots; the exact
     # beam over local sets finds 3 passes per sweep (the greedy search needs 4)
     _, circ, _ = models.spinful_layer_circuit(8, 5, False, seed=1)
-    sizes = check_plan(circ, -1, 11, sweep)
+    sizes = check_plan_env(circ, -1, 11, sweep, {"GF_PLAN_MINPASS": "1"})
     assert len(sizes) == 3
     greedy, _, _ = layout(circ, -1, 11, sweep, env={"GF_PLAN_GREEDY": "1"})
     assert len(greedy) >= len(sizes)
+    # default: with the light-cone rule dead tiles are free, so the planner may
+    # spend one more pass near the |j> end when that leaves less live slot work
+    lc = check_plan(circ, -1, 11, sweep)
+    assert len(sizes) <= len(lc) <= len(sizes) + 1 and sum(lc) == sum(sizes) == 36
 
 
 @pytest.mark.parametrize("L,layers,periodic,sector,m", [
