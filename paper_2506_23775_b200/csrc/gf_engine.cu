@@ -2413,8 +2413,10 @@ static bool plan_exact(const gf_plan *p, const std::vector<int> &order, int m, i
     if (!search(0, max_depth, cost0, h0)) return false;
     const Hist *pick = &h0;
     if (p->lightcone && !getenv("GF_PLAN_MINPASS")) {
-        // one pass more than the minimum, if that is cheaper
-        if (search(1, (int)h0.size() + 1, cost1, h1) && cost1 < cost0 - 1e-9) pick = &h1;
+        // up to GF_PLAN_EXTRA (default 1) passes more than the minimum, if that is cheaper
+        const char *xe = getenv("GF_PLAN_EXTRA");
+        const int extra = xe ? std::max(0, atoi(xe)) : 1;
+        if (extra > 0 && search(1, (int)h0.size() + extra, cost1, h1) && cost1 < cost0 - 1e-9) pick = &h1;
     }
     out.clear();
     for (const auto &h : *pick) {

@@ -254,7 +254,7 @@ _PLANS: dict = {}
 # environment knobs read by gf_plan_create (csrc/gf_engine.cu plan_knobs): part
 # of the plan cache key so a changed knob never reuses a plan built without it
 _PLAN_KNOBS = ("GF_ENGINE", "GF_FUSED_M", "GF_FWD_M", "GF_FUSED_C", "GF_FUSED_CTAS", "GF_PLAN_GREEDY",
-               "GF_SPARSE_DMMA", "GF_C1Q_DMMA", "GF_PAIR_BLOCKS", "GF_SECTOR_FMA", "GF_UNIT_NT", "GF_LIGHTCONE", "GF_PLAN_MINPASS")
+               "GF_SPARSE_DMMA", "GF_C1Q_DMMA", "GF_PAIR_BLOCKS", "GF_SECTOR_FMA", "GF_UNIT_NT", "GF_LIGHTCONE", "GF_PLAN_MINPASS", "GF_PLAN_EXTRA")
 
 
 def _get_plan(circuit: Circuit, sector: int, batch: int, chunk: int) -> EnginePlan:
