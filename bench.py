@@ -621,6 +621,32 @@ def run_b200(args):
     # consistency: same objective from both paths
     assert abs(rep_e.value - rep.value) <= 1e-10 * max(1.0, abs(rep.value)), (rep_e.value, rep.value)
 
+    # the same evaluation with the light-cone rule off (every slot applied to
+    # every tile, as the reference applies it to the whole vector): the results
+    # must agree -- the rule only skips exact zeros -- and its rate is reported
+    no_lc = None
+    if rank == 0 and world == 1 and os.environ.get("GF_LIGHTCONE", "1") != "0" and not args.no_lightcone_check:
+        os.environ["GF_LIGHTCONE"] = "0"
+        try:
+            rep0, hv0 = gf.gradient_and_hvp(circ, cache, X, **kw)  # plan + warm-up
+            torch.cuda.synchronize()
+            e0.record(stream)
+            rep0, hv0 = gf.gradient_and_hvp(circ, cache, X, **kw)
+            e1.record(stream)
+            torch.cuda.synchronize()
+        finally:
+            os.environ.pop("GF_LIGHTCONE", None)
+        ms0 = e0.elapsed_time(e1)
+        g1, g0 = np.stack(rep.holomorphic_derivatives), np.stack(rep0.holomorphic_derivatives)
+        h1, h0 = np.stack(hv), np.stack(hv0)
+        dev_g = float(np.abs(g1 - g0).max() / np.abs(g0).max())
+        dev_h = float(np.abs(h1 - h0).max() / np.abs(h0).max())
+        dev_v = abs(rep.value - rep0.value) / max(1.0, abs(rep0.value))
+        assert max(dev_g, dev_h, dev_v) < 1e-10, (dev_v, dev_g, dev_h)
+        no_lc = {"value": summands / (ms0 * 1e-3), "unit": UNIT, "ms_per_step": ms0,
+                 "max_rel_dev_vs_light_cone": {"value": dev_v, "gradient": dev_g, "hvp": dev_h},
+                 "note": "GF_LIGHTCONE=0: every slot applied to every tile; one timed step"}
+
     del cache
     obj._PLANS.clear()
     torch.cuda.empty_cache()
@@ -703,6 +729,7 @@ def run_b200(args):
                             "target column regenerated on device each evaluation" % type(oracle).__name__},
             "gpu_launches": launches_all,
             "clocks": clocks,
+            "no_light_cone": no_lc,
             "gate_apply": gate_sweep,
             "c5": c5,
             "cpu_baseline": cpu,
@@ -728,6 +755,7 @@ def main():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-c5", action="store_true")
+    ap.add_argument("--no-lightcone-check", action="store_true")
     ap.add_argument("--summands", type=int, default=None,
                     help="profiling only: restrict each step to the first S basis states")
     args = ap.parse_args()
